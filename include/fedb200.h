@@ -1,0 +1,137 @@
+/*
+ * libfedb200 — C ABI of the B200-native (sm_100a) federated-round hot path.
+ *
+ * Drop-in boundary for the reference `fedforge` (arXiv 2405.10853). The reference
+ * has no FFI of its own (pure Python over numpy / torch-CPU), so each entry point
+ * below names the Python call site it replaces; the Python shim
+ * `paper_2405_10853_b200` binds these through ctypes.
+ *
+ * Conventions
+ *   - plain pointers and sizes; every pointer argument named d_* is DEVICE memory
+ *     owned by the caller; the library never allocates or frees in a hot call
+ *   - every entry returns int (fb_status); fb_last_error() has the message
+ *   - every entry takes an explicit CUDA stream (cudaStream_t passed as void*)
+ *   - entries are reentrant; no global mutable state except a tensor-map cache
+ */
+#ifndef FEDB200_H
+#define FEDB200_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum fb_status { FB_OK = 0, FB_BAD_ARG = 1, FB_CUDA_ERROR = 2, FB_NONFINITE = 3, FB_UNSUPPORTED = 4 };
+
+#define FB_ABI_VERSION 1
+#define FB_MAX_CLIENTS 64
+#define FB_RED_BLOCKS 1184 /* fixed reduction grid: 148 SMs x 8, deterministic partials */
+
+const char* fb_last_error(void);
+int fb_abi_version(void);
+int fb_device_check(void); /* FB_OK iff device 0 is sm_100 (B200) */
+
+/* ---- server: aggregation + outer optimizer (K13) ---------------------------------
+ * Replaces AggregatorState.finalize  (fedforge/fedopt.py:129-144)
+ *      then server_step              (fedforge/fedopt.py:167-201)
+ * client weights w_k (f32) arrive in the order the pairwise tree / running sum uses
+ * (deterministic: ascending client id; streaming: arrival order). The f64 pseudo-
+ * gradient  sum_k n_k (f64(w) - f64(w_k)) / sum n_k  and the outer step run in f64
+ * registers; m' is rounded to f32 before it feeds w' (fedopt.py:189-196).
+ * d_stats (optional, 3 doubles): ||pg||^2, ||w'||^2, ||m'||^2.
+ * d_first_bad (optional, 1 int64): lowest index with a non-finite w' or m' (or n).
+ * Returns FB_OK; the caller checks d_first_bad (no host sync inside). */
+int fb_fedagg_step_f32(const float* const* d_client_w, const int64_t* n_k, int n_clients,
+                       int deterministic, const float* d_w, const float* d_m, float* d_w_out,
+                       float* d_m_out, int64_t n, double eta, double mu, int nesterov,
+                       double* d_stats, int64_t* d_first_bad, void* stream);
+/* Same contract for reference-format f64 deltas (ClientUpdate.delta, fedopt.py:26-46). */
+int fb_fedagg_step_f64delta(const double* const* d_deltas, const int64_t* n_k, int n_clients,
+                            int deterministic, const float* d_w, const float* d_m, float* d_w_out,
+                            float* d_m_out, int64_t n, double eta, double mu, int nesterov,
+                            double* d_stats, int64_t* d_first_bad, void* stream);
+
+/* ---- client optimizer (K10-K12) --------------------------------------------------- */
+/* d_partials[FB_RED_BLOCKS] = per-block sum of x^2 (f64). l2_norm: params.py:126-133 */
+int fb_sumsq_partials(const float* d_x, int64_t n, double* d_partials, void* stream);
+/* one block: sum the partials in fixed order -> d_out[0] (f64) */
+int fb_sum_partials(const double* d_partials, int n_partials, double* d_out, void* stream);
+
+typedef struct {
+  double beta1, beta2, eps, weight_decay, clip_norm;
+} fb_adamw_cfg; /* AdamWConfig, localopt.py:22-38 */
+
+/* Per-step device control block: written by fb_step_prepare on device, read by AdamW. */
+typedef struct {
+  double lr, bc1, bc2;       /* lr_at(offset+s); 1-beta1^t; 1-beta2^t (host-computed) */
+  double grad_sumsq;         /* ||g||^2 of the micro-batch-mean gradient */
+  double clip_scale;         /* max_norm/raw when raw > max_norm */
+  int32_t clip_active;       /* raw > max_norm (strict, localopt.py:140) */
+  int32_t pad;
+} fb_step_ctl;
+
+/* Reduce d_partials (grad sum of squares) -> ctl->grad_sumsq, clip decision. */
+int fb_step_prepare(const double* d_partials, double lr, double bc1, double bc2,
+                    double clip_norm, fb_step_ctl* d_ctl, void* stream);
+/* Fused AdamW over the flat vector (localopt.py:61-96, clip localopt.py:132-143):
+ * f64 math, f32 p/m1/m2, optional bf16 shadow of p'. Per-block partials of ||u||^2
+ * and ||p'||^2 go to d_part_u / d_part_p ([FB_RED_BLOCKS] each, optional);
+ * d_first_bad (optional) gets the lowest index with non-finite p'. */
+int fb_adamw_step(float* d_p, const float* d_g, float* d_m1, float* d_m2, void* d_shadow_bf16,
+                  int64_t n, fb_adamw_cfg cfg, const fb_step_ctl* d_ctl, double* d_part_u,
+                  double* d_part_p, int64_t* d_first_bad, void* stream);
+/* f32 -> bf16 copy (shadow weights at round start) */
+int fb_cast_bf16(const float* d_x, void* d_y, int64_t n, void* stream);
+
+/* ---- dense GEMM on tcgen05 (K3, K5, K6, K7, LM head) -------------------------------
+ * D[m,n] = sum_k A(m,k) * B(n,k), bf16 inputs, fp32 accumulation in TMEM.
+ * a_major/b_major: 0 = K-major (A stored [M][lda], B stored [N][ldb]),
+ *                  1 = MN-major (A stored [K][lda], B stored [K][ldb]).
+ * Epilogues (fused in the TMEM->register drain): */
+enum fb_epilogue {
+  FB_EPI_BF16 = 0,       /* C(bf16) = acc */
+  FB_EPI_F32 = 1,        /* C(f32) = acc */
+  FB_EPI_ACC_F32 = 2,    /* C(f32) += acc   (wgrad micro-batch accumulation) */
+  FB_EPI_RESID_F32 = 3,  /* C(f32) = aux(f32) + acc  (residual add; aux may alias C) */
+  FB_EPI_GELU = 4,       /* C(bf16) = gelu_erf(acc); aux_out(bf16) = acc (pre-activation) */
+  FB_EPI_DGELU = 5,      /* C(bf16) = acc * gelu_erf'(aux(bf16)) */
+  FB_EPI_RESID_F32_BF16 = 6 /* C(f32) = aux(f32) + acc and aux_out(bf16) = same */
+};
+int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, int a_major,
+                 const void* d_B, int64_t ldb, int b_major, void* d_C, int64_t ldc, int epilogue,
+                 const void* d_aux, void* d_aux_out, int64_t ld_aux, void* stream);
+
+/* ---- transformer pieces (model.py:75-150, :222-229) --------------------------------- */
+int fb_embed_fwd(const int32_t* d_tok, const float* d_emb, const float* d_pos, float* d_x,
+                 int n_tok, int T, int d, void* stream);
+int fb_embed_bwd(const int32_t* d_tok, const float* d_dx, float* d_gemb, float* d_gpos,
+                 int n_tok, int T, int d, int vocab, void* stream);
+/* LayerNorm eps 1e-5 (model.py:81,84,113): y(bf16) = LN(x), saves mean/rstd */
+int fb_ln_fwd(const float* d_x, const float* d_gamma, const float* d_beta, void* d_y_bf16,
+              float* d_mean, float* d_rstd, int rows, int d, void* stream);
+/* dx(f32) = dres(f32, optional) + LN'(dy); optional bf16 copy of dx; dgamma/dbeta += */
+int fb_ln_bwd(const float* d_x, const float* d_gamma, const float* d_mean, const float* d_rstd,
+              const float* d_dy, const float* d_dres, float* d_dx, void* d_dx_bf16,
+              float* d_dgamma, float* d_dbeta, float* d_work, int rows, int d, void* stream);
+/* Causal attention with the reference's ALiBi slopes 2^(-8(h+1)/H) (model.py:46-65, 92-98).
+ * qkv: [B*T][3d] bf16 (q|k|v, head h at columns h*dh); o: [B*T][d] bf16; lse: [B][H][T] f32 */
+int fb_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int H, int dh,
+                int use_alibi, void* stream);
+int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
+                void* d_dqkv, float* d_work, int B, int T, int H, int dh, int use_alibi,
+                void* stream);
+/* Mean next-token CE over B*(T-1) positions (model.py:226-229): logits f32 [rows][V]
+ * for a chunk of rows [row0, row0+rows) of a B x T batch; writes dlogits(bf16) =
+ * scale*(softmax - onehot) (0 on each sequence's last position) and adds the summed
+ * loss of the chunk into d_loss_sum (f64). */
+int fb_ce_fwd_bwd(const float* d_logits, const int32_t* d_tok, void* d_dlogits, int row0,
+                  int rows, int T, int V, float scale, double* d_loss_sum, void* stream);
+
+/* ---- data feed: BatchIterator.next_batch on device (data.py:152-161) ----------------
+ * rows = order[(cursor + i) mod n_order]; tok[i][t] = corpus[rows[i]*T + t] */
+int fb_gather_batch(const uint16_t* d_corpus, const int64_t* d_order, int64_t n_order,
+                    int64_t cursor, int batch, int T, int32_t* d_tok, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

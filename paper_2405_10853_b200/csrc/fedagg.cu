@@ -1,0 +1,291 @@
+// K13: fused pseudo-gradient aggregation + server outer step, one HBM pass.
+//
+// Reference math (fedforge/fedopt.py):
+//   delta_k = f64(w) - f64(w_k)                                  trainer.py:352
+//   deterministic finalize: pairwise tree over n_k*delta_k in id order, / total  fedopt.py:135-143
+//   streaming finalize:     running sum in arrival order, / total               fedopt.py:95, 144
+//   single contribution:    delta_0 unchanged                                   fedopt.py:133-134
+//   m' = f32(mu*f64(m) + pg); w' = f32(f64(w) - eta*(mu*f64(m') + pg)) [Nesterov]
+//                                  or f32(f64(w) - eta*f64(m'))                  fedopt.py:189-196
+// All arithmetic uses explicit round-to-nearest f64 intrinsics (no FMA contraction)
+// so results are bit-identical to numpy's.
+//
+// B200 design: memory-bound streaming kernel. Each thread owns 4 consecutive
+// parameters (128-bit loads of every client vector, w and m; 128-bit streaming
+// stores of w', m'); grid = 148 SMs x 8 resident CTAs, grid-stride. The
+// pairwise tree is evaluated on the fly with a binary-counter stack of depth
+// <= 7 (same association as the level-by-level pairing), so K clients cost K
+// loads and no extra traffic. Algorithmic bytes: (4K + 16) N.
+#include "common.cuh"
+
+namespace fb {
+
+template <typename TIn>
+struct AggParams {
+  const TIn* src[FB_MAX_CLIENTS];
+  double nk[FB_MAX_CLIENTS];
+};
+
+constexpr int kStack = 7;  // 2^7 > FB_MAX_CLIENTS
+
+struct TreeAcc {
+  double slot[kStack];
+  __device__ __forceinline__ void push(double t, int k) {
+    // k = index of this term; slots occupied = bits of k
+    double carry = t;
+    bool done = false;
+#pragma unroll
+    for (int L = 0; L < kStack; ++L) {
+      if (!done) {
+        if ((k >> L) & 1) {
+          carry = __dadd_rn(slot[L], carry);
+        } else {
+          slot[L] = carry;
+          done = true;
+        }
+      }
+    }
+  }
+  __device__ __forceinline__ double result(int K) const {
+    // merge occupied slots right-to-left: lowest level is the rightmost block
+    double acc = 0.0;
+    bool have = false;
+#pragma unroll
+    for (int L = 0; L < kStack; ++L) {
+      if ((K >> L) & 1) {
+        acc = have ? __dadd_rn(slot[L], acc) : slot[L];
+        have = true;
+      }
+    }
+    return acc;
+  }
+};
+
+template <typename TIn>
+__device__ __forceinline__ double delta_of(const TIn* p, int64_t j, double wg);
+template <>
+__device__ __forceinline__ double delta_of<float>(const float* p, int64_t j, double wg) {
+  return __dsub_rn(wg, (double)__ldg(p + j));
+}
+template <>
+__device__ __forceinline__ double delta_of<double>(const double* p, int64_t j, double) {
+  return __ldg(p + j);
+}
+
+struct StepOut {
+  float w, m;
+  double pg;
+};
+
+__device__ __forceinline__ StepOut outer_step(float w32, float m32, double pg, double eta, double mu,
+                                              int nesterov) {
+  StepOut o;
+  double m64 = __dadd_rn(__dmul_rn(mu, (double)m32), pg);
+  o.m = __double2float_rn(m64);
+  double upd;
+  if (nesterov)
+    upd = __dmul_rn(eta, __dadd_rn(__dmul_rn(mu, (double)o.m), pg));
+  else
+    upd = __dmul_rn(eta, (double)o.m);
+  o.w = __double2float_rn(__dsub_rn((double)w32, upd));
+  o.pg = pg;
+  return o;
+}
+
+template <typename TIn, int VEC>
+__global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, int deterministic,
+                                                     double inv_total_unused, double total,
+                                                     const float* __restrict__ w,
+                                                     const float* __restrict__ m,
+                                                     float* __restrict__ w_out,
+                                                     float* __restrict__ m_out, int64_t n,
+                                                     double eta, double mu, int nesterov,
+                                                     double* stats, unsigned long long* first_bad) {
+  __shared__ double red[3][8];
+  double s_pg = 0.0, s_w = 0.0, s_m = 0.0;
+  unsigned long long bad = ~0ull;
+  const int64_t nvec = n / VEC;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j0 = v * VEC;
+    float wv[VEC], mv[VEC];
+    if constexpr (VEC == 4) {
+      float4 a = ld_stream_f4(w + j0), b = ld_stream_f4(m + j0);
+      wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w;
+      mv[0] = b.x; mv[1] = b.y; mv[2] = b.z; mv[3] = b.w;
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) { wv[e] = w[j0 + e]; mv[e] = m[j0 + e]; }
+    }
+    double pg[VEC];
+    if (K == 1) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) pg[e] = delta_of<TIn>(P.src[0], j0 + e, (double)wv[e]);
+    } else if (deterministic) {
+      TreeAcc acc[VEC];
+      for (int k = 0; k < K; ++k) {
+        const TIn* src = P.src[k];
+        double dk[VEC];
+        if constexpr (VEC == 4 && sizeof(TIn) == 4) {
+          float4 c = ld_stream_f4(reinterpret_cast<const float*>(src) + j0);
+          dk[0] = __dsub_rn((double)wv[0], (double)c.x);
+          dk[1] = __dsub_rn((double)wv[1], (double)c.y);
+          dk[2] = __dsub_rn((double)wv[2], (double)c.z);
+          dk[3] = __dsub_rn((double)wv[3], (double)c.w);
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) dk[e] = delta_of<TIn>(src, j0 + e, (double)wv[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) acc[e].push(__dmul_rn(P.nk[k], dk[e]), k);
+      }
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) pg[e] = __ddiv_rn(acc[e].result(K), total);
+    } else {
+      double sum[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) sum[e] = 0.0;
+      for (int k = 0; k < K; ++k) {
+        const TIn* src = P.src[k];
+        if constexpr (VEC == 4 && sizeof(TIn) == 4) {
+          float4 c = ld_stream_f4(reinterpret_cast<const float*>(src) + j0);
+          float cv[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+          for (int e = 0; e < VEC; ++e)
+            sum[e] = __dadd_rn(sum[e], __dmul_rn(P.nk[k], __dsub_rn((double)wv[e], (double)cv[e])));
+        } else {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e)
+            sum[e] = __dadd_rn(sum[e], __dmul_rn(P.nk[k], delta_of<TIn>(src, j0 + e, (double)wv[e])));
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) pg[e] = __ddiv_rn(sum[e], total);
+    }
+    float wo[VEC], mo[VEC];
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      StepOut o = outer_step(wv[e], mv[e], pg[e], eta, mu, nesterov);
+      wo[e] = o.w;
+      mo[e] = o.m;
+      s_pg += pg[e] * pg[e];
+      s_w += (double)o.w * (double)o.w;
+      s_m += (double)o.m * (double)o.m;
+      if (!(isfinite(o.w) && isfinite(o.m)) && (unsigned long long)(j0 + e) < bad)
+        bad = (unsigned long long)(j0 + e);
+    }
+    if constexpr (VEC == 4) {
+      st_stream_f4(w_out + j0, make_float4(wo[0], wo[1], wo[2], wo[3]));
+      st_stream_f4(m_out + j0, make_float4(mo[0], mo[1], mo[2], mo[3]));
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) { w_out[j0 + e] = wo[e]; m_out[j0 + e] = mo[e]; }
+    }
+  }
+  // scalar tail (only when VEC == 4 and n % 4 != 0)
+  if (VEC > 1 && blockIdx.x == 0 && threadIdx.x < (n % VEC)) {
+    int64_t j = nvec * VEC + threadIdx.x;
+    double wg = (double)w[j];
+    double pgv;
+    if (K == 1) {
+      pgv = delta_of<TIn>(P.src[0], j, wg);
+    } else if (deterministic) {
+      TreeAcc acc;
+      for (int k = 0; k < K; ++k) acc.push(__dmul_rn(P.nk[k], delta_of<TIn>(P.src[k], j, wg)), k);
+      pgv = __ddiv_rn(acc.result(K), total);
+    } else {
+      double s = 0.0;
+      for (int k = 0; k < K; ++k) s = __dadd_rn(s, __dmul_rn(P.nk[k], delta_of<TIn>(P.src[k], j, wg)));
+      pgv = __ddiv_rn(s, total);
+    }
+    StepOut o = outer_step(w[j], m[j], pgv, eta, mu, nesterov);
+    w_out[j] = o.w;
+    m_out[j] = o.m;
+    s_pg += pgv * pgv;
+    s_w += (double)o.w * (double)o.w;
+    s_m += (double)o.m * (double)o.m;
+    if (!(isfinite(o.w) && isfinite(o.m)) && (unsigned long long)j < bad) bad = (unsigned long long)j;
+  }
+  if (first_bad) {
+    // warp-min then one atomic per warp
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long t = __shfl_xor_sync(0xffffffffu, bad, o);
+      bad = t < bad ? t : bad;
+    }
+    if ((threadIdx.x & 31) == 0 && bad != ~0ull) atomicMin(first_bad, bad);
+  }
+  if (stats) {
+    s_pg = warp_sum(s_pg);
+    s_w = warp_sum(s_w);
+    s_m = warp_sum(s_m);
+    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) { red[0][wid] = s_pg; red[1][wid] = s_w; red[2][wid] = s_m; }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      double t = 0.0;
+      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[threadIdx.x][i];
+      atomicAdd(stats + threadIdx.x, t);
+    }
+  }
+}
+
+template <typename TIn>
+static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int deterministic,
+                         const float* w, const float* m, float* w_out, float* m_out, int64_t n,
+                         double eta, double mu, int nesterov, double* stats, int64_t* first_bad,
+                         cudaStream_t st) {
+  FB_REQUIRE(K >= 1 && K <= FB_MAX_CLIENTS, "n_clients=%d outside [1, %d]", K, FB_MAX_CLIENTS);
+  FB_REQUIRE(n > 0, "model length must be positive, got %lld", (long long)n);
+  FB_REQUIRE(eta > 0.0, "server eta must be > 0, got %g", eta);
+  FB_REQUIRE(mu >= 0.0 && mu < 1.0, "server mu must be in [0, 1), got %g", mu);
+  AggParams<TIn> P;
+  double total = 0.0;
+  int64_t itotal = 0;
+  bool aligned = ((uintptr_t)w % 16 == 0) && ((uintptr_t)m % 16 == 0) && ((uintptr_t)w_out % 16 == 0) &&
+                 ((uintptr_t)m_out % 16 == 0);
+  for (int k = 0; k < K; ++k) {
+    FB_REQUIRE(n_k[k] >= 1, "client %d: n_k must be >= 1, got %lld", k, (long long)n_k[k]);
+    FB_REQUIRE(src[k] != nullptr, "client %d: null pointer", k);
+    P.src[k] = src[k];
+    P.nk[k] = (double)n_k[k];
+    itotal += n_k[k];
+    aligned = aligned && ((uintptr_t)src[k] % 16 == 0);
+  }
+  total = (double)itotal;
+  if (stats) FB_CUDA_TRY(cudaMemsetAsync(stats, 0, 3 * sizeof(double), st));
+  if (first_bad) FB_CUDA_TRY(cudaMemsetAsync(first_bad, 0x7f, sizeof(int64_t), st));
+  const int threads = 256;
+  if (aligned && sizeof(TIn) == 4) {
+    int64_t work = (n / 4 + threads - 1) / threads;
+    int blocks = (int)(work < kNumSMs * 8 ? (work > 0 ? work : 1) : kNumSMs * 8);
+    fedagg_kernel<TIn, 4><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, m_out, n,
+                                                      eta, mu, nesterov, stats,
+                                                      (unsigned long long*)first_bad);
+  } else {
+    int64_t work = (n + threads - 1) / threads;
+    int blocks = (int)(work < kNumSMs * 8 ? (work > 0 ? work : 1) : kNumSMs * 8);
+    fedagg_kernel<TIn, 1><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, m_out, n,
+                                                      eta, mu, nesterov, stats,
+                                                      (unsigned long long*)first_bad);
+  }
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
+}  // namespace fb
+
+extern "C" int fb_fedagg_step_f32(const float* const* d_client_w, const int64_t* n_k, int n_clients,
+                                  int deterministic, const float* d_w, const float* d_m, float* d_w_out,
+                                  float* d_m_out, int64_t n, double eta, double mu, int nesterov,
+                                  double* d_stats, int64_t* d_first_bad, void* stream) {
+  return fb::launch_fedagg<float>(d_client_w, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n,
+                                  eta, mu, nesterov, d_stats, d_first_bad, (cudaStream_t)stream);
+}
+
+extern "C" int fb_fedagg_step_f64delta(const double* const* d_deltas, const int64_t* n_k, int n_clients,
+                                       int deterministic, const float* d_w, const float* d_m, float* d_w_out,
+                                       float* d_m_out, int64_t n, double eta, double mu, int nesterov,
+                                       double* d_stats, int64_t* d_first_bad, void* stream) {
+  return fb::launch_fedagg<double>(d_deltas, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n,
+                                   eta, mu, nesterov, d_stats, d_first_bad, (cudaStream_t)stream);
+}

@@ -1,0 +1,419 @@
+// Dense bf16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// Replaces every nn.Linear of the reference TinyLM (fedforge/model.py:82-86, :114)
+// in forward (X W^T), dgrad (dY W) and wgrad (dY^T X) form, with the elementwise
+// work that follows each one fused into the TMEM drain (GELU-erf, dGELU, residual
+// add, fp32 wgrad accumulation across micro-batches).
+//
+// Kernel anatomy (persistent, warp-specialised, one CTA per SM):
+//   warp 0      TMA producer: STAGES-deep ring of {A 128x64, B BNx64} bf16 tiles,
+//               128B-swizzled, K-major or MN-major (3-D tensor map so an MN-major
+//               tile is a single TMA), completion via mbarrier expect_tx
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (128xBNx16 UMMAs),
+//               tcgen05.commit frees smem slots / publishes finished accumulators
+//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> registers -> fused op -> global
+//   TMEM        2 x BN fp32 columns: the accumulator is double-buffered so the
+//               epilogue of tile i overlaps the main loop of tile i+1
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace fb {
+using namespace sm100;
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kGemmThreads = 192;
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : 6;
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*barriers*/ + 1024 /*align slack*/;
+  static constexpr int TMEM_COLS = 2 * BN;
+};
+
+struct EpiArgs {
+  void* C;
+  int64_t ldc;
+  const void* aux;
+  void* aux_out;
+  int64_t ld_aux;
+};
+
+__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+__device__ __forceinline__ float gelu_erf_grad(float x) {
+  const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
+  const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
+  return cdf + x * pdf;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Process 32 consecutive columns [col, col+32) of one row held in registers.
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int64_t row, int col, int N, const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  const bool full = col + 32 <= N;
+  if constexpr (EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU) {
+    __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(e.C) + row * e.ldc + col;
+    float o[32];
+    if constexpr (EPI == FB_EPI_GELU) {
+      __nv_bfloat16* P = reinterpret_cast<__nv_bfloat16*>(e.aux_out) + row * e.ld_aux + col;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 pk = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+          *reinterpret_cast<uint4*>(P + 8 * q) = pk;
+        }
+      } else {
+        _Pragma("unroll") for (int i = 0; i < 32; ++i) if (col + i < N) P[i] = __float2bfloat16_rn(v[i]);
+      }
+      // GELU of the bf16-rounded pre-activation so forward and backward see the same input
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = gelu_erf(__bfloat162float(__float2bfloat16_rn(v[i])));
+    } else if constexpr (EPI == FB_EPI_DGELU) {
+      const __nv_bfloat16* P = reinterpret_cast<const __nv_bfloat16*>(e.aux) + row * e.ld_aux + col;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 pk = *reinterpret_cast<const uint4*>(P + 8 * q);
+          const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&pk);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) o[8 * q + i] = v[8 * q + i] * gelu_erf_grad(__bfloat162float(pb[i]));
+        }
+      } else {
+        _Pragma("unroll") for (int i = 0; i < 32; ++i) o[i] = (col + i < N) ? v[i] * gelu_erf_grad(__bfloat162float(P[i])) : 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[i] = v[i];
+    }
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 pk = make_uint4(pack_bf16(o[8 * q], o[8 * q + 1]), pack_bf16(o[8 * q + 2], o[8 * q + 3]),
+                              pack_bf16(o[8 * q + 4], o[8 * q + 5]), pack_bf16(o[8 * q + 6], o[8 * q + 7]));
+        *reinterpret_cast<uint4*>(C + 8 * q) = pk;
+      }
+    } else {
+      _Pragma("unroll") for (int i = 0; i < 32; ++i) if (col + i < N) C[i] = __float2bfloat16_rn(o[i]);
+    }
+  } else {
+    float* C = reinterpret_cast<float*>(e.C) + row * e.ldc + col;
+    if constexpr (EPI == FB_EPI_ACC_F32) {
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 c = *reinterpret_cast<const float4*>(C + 4 * q);
+          v[4 * q] += c.x; v[4 * q + 1] += c.y; v[4 * q + 2] += c.z; v[4 * q + 3] += c.w;
+        }
+      } else {
+        _Pragma("unroll") for (int i = 0; i < 32; ++i) if (col + i < N) v[i] += C[i];
+      }
+    } else if constexpr (EPI == FB_EPI_RESID_F32 || EPI == FB_EPI_RESID_F32_BF16) {
+      const float* R = reinterpret_cast<const float*>(e.aux) + row * e.ld_aux + col;
+      if (full) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float4 c = *reinterpret_cast<const float4*>(R + 4 * q);
+          v[4 * q] += c.x; v[4 * q + 1] += c.y; v[4 * q + 2] += c.z; v[4 * q + 3] += c.w;
+        }
+      } else {
+        _Pragma("unroll") for (int i = 0; i < 32; ++i) if (col + i < N) v[i] += R[i];
+      }
+      if constexpr (EPI == FB_EPI_RESID_F32_BF16) {
+        __nv_bfloat16* Ob = reinterpret_cast<__nv_bfloat16*>(e.aux_out) + row * e.ldc + col;
+        if (full) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 pk = make_uint4(pack_bf16(v[8 * q], v[8 * q + 1]), pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                                  pack_bf16(v[8 * q + 4], v[8 * q + 5]), pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+            *reinterpret_cast<uint4*>(Ob + 8 * q) = pk;
+          }
+        } else {
+          _Pragma("unroll") for (int i = 0; i < 32; ++i) if (col + i < N) Ob[i] = __float2bfloat16_rn(v[i]);
+        }
+      }
+    }
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<float4*>(C + 4 * q) = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    } else {
+      _Pragma("unroll") for (int i = 0; i < 32; ++i) if (col + i < N) C[i] = v[i];
+    }
+  }
+}
+
+template <int BN, int A_MN, int B_MN, int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm_bf16_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                        int N, int K, EpiArgs ep) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
+  uint8_t* tiles = smem;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty_bar = full_bar + STAGES;
+  uint64_t* tfull_bar = empty_bar + STAGES;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int num_m = (M + BM - 1) / BM;
+  const int num_n = (N + BN - 1) / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+        const int m0 = (tile % num_m) * BM;
+        const int n0 = (tile / num_m) * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = tiles + stage * Cfg::STAGE_BYTES;
+          uint8_t* sb = sa + Cfg::A_BYTES;
+          mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+          const int k0 = kb * BK;
+          if (A_MN) tma_load_3d(sa, &tmA, &full_bar[stage], 0, k0, m0 / 64);
+          else      tma_load_2d(sa, &tmA, &full_bar[stage], k0, m0);
+          if (B_MN) tma_load_3d(sb, &tmB, &full_bar[stage], 0, k0, n0 / 64);
+          else      tma_load_2d(sb, &tmB, &full_bar[stage], k0, n0);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = idesc_bf16_f32(BM, BN, A_MN, B_MN);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int buf = it & 1;
+      const uint32_t use = it >> 1;
+      mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + buf * BN;
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&full_bar[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(tiles + stage * Cfg::STAGE_BYTES);
+          const uint32_t sb = sa + Cfg::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            // K-major SW128: rows 128B apart, 8-row atoms SBO=1024; k-step = +32B
+            // MN-major SW128: 64-elem MN chunks LBO=64*128B, 8-k-row groups SBO=1024; k-step = +2048B
+            const uint64_t ad = A_MN ? smem_desc_sw128(sa + kk * 2048, BK * 128, 1024)
+                                     : smem_desc_sw128(sa + kk * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc_sw128(sb + kk * 2048, BK * 128, 1024)
+                                     : smem_desc_sw128(sb + kk * 32, 16, 1024);
+            umma_f16(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+          }
+          umma_commit(&empty_bar[stage]);
+        }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) umma_commit(&tfull_bar[buf]);
+      __syncwarp();
+    }
+  } else {
+    // ---------------- epilogue warps 2..5 ----------------
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    int it = 0;
+    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+      const int m0 = (tile % num_m) * BM;
+      const int n0 = (tile / num_m) * BN;
+      const int buf = it & 1;
+      const uint32_t use = it >> 1;
+      mbar_wait(&tfull_bar[buf], use & 1);
+      tc_fence_after();
+      const int64_t row = m0 + quad * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tmem_ld_wait();
+        if (c == BN / 32 - 1) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty_bar[buf]);
+        }
+        const int col = n0 + c * 32;
+        if (row < M && col < N) epilogue_chunk<EPI>(ep, row, col, N, r);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int get_encoder() {
+  if (g_encode) return FB_OK;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  FB_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return FB_CUDA_ERROR;
+  }
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return FB_OK;
+}
+
+// K-major operand stored [rows][ld] (K contiguous): box {64 k, box_rows}
+static int make_map_kmajor(CUtensorMap* m, const void* ptr, int rows, int K, int64_t ld, int box_rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(K-major rows=%d K=%d ld=%lld) failed: %d", rows, K, (long long)ld, (int)r);
+    return FB_CUDA_ERROR;
+  }
+  return FB_OK;
+}
+
+// MN-major operand stored [K][ld] (MN contiguous), viewed 3-D {64 mn, K, mn/64}
+static int make_map_mnmajor(CUtensorMap* m, const void* ptr, int mn, int K, int64_t ld, int box_mn) {
+  cuuint64_t dims[3] = {64, (cuuint64_t)K, (cuuint64_t)(mn / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)BK, (cuuint32_t)(box_mn / 64)};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(MN-major mn=%d K=%d ld=%lld) failed: %d", mn, K, (long long)ld, (int)r);
+    return FB_CUDA_ERROR;
+  }
+  return FB_OK;
+}
+
+template <int BN, int A_MN, int B_MN, int EPI>
+static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiArgs& ep,
+                         cudaStream_t st) {
+  using Cfg = GemmCfg<BN>;
+  auto kern = gemm_bf16_tc_kernel<BN, A_MN, B_MN, EPI>;
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+    attr_set = true;
+  }
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int grid = tiles < kNumSMs ? tiles : kNumSMs;
+  kern<<<grid, kGemmThreads, Cfg::SMEM, st>>>(ta, tb, M, N, K, ep);
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
+template <int BN, int A_MN, int B_MN>
+static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                        const EpiArgs& ep, cudaStream_t st) {
+  switch (epi) {
+    case FB_EPI_BF16: return launch_gemm_t<BN, A_MN, B_MN, FB_EPI_BF16>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_F32: return launch_gemm_t<BN, A_MN, B_MN, FB_EPI_F32>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_ACC_F32: return launch_gemm_t<BN, A_MN, B_MN, FB_EPI_ACC_F32>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_RESID_F32: return launch_gemm_t<BN, A_MN, B_MN, FB_EPI_RESID_F32>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_GELU: return launch_gemm_t<BN, A_MN, B_MN, FB_EPI_GELU>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_DGELU: return launch_gemm_t<BN, A_MN, B_MN, FB_EPI_DGELU>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_RESID_F32_BF16: return launch_gemm_t<BN, A_MN, B_MN, FB_EPI_RESID_F32_BF16>(ta, tb, M, N, K, ep, st);
+  }
+  set_error("unknown epilogue %d", epi);
+  return FB_BAD_ARG;
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, int a_major, const void* d_B,
+                            int64_t ldb, int b_major, void* d_C, int64_t ldc, int epilogue, const void* d_aux,
+                            void* d_aux_out, int64_t ld_aux, void* stream) {
+  FB_REQUIRE(M > 0 && N > 0 && K > 0, "gemm: non-positive shape %d x %d x %d", M, N, K);
+  FB_REQUIRE(d_A && d_B && d_C, "gemm: null operand");
+  FB_REQUIRE(((uintptr_t)d_A % 16 == 0) && ((uintptr_t)d_B % 16 == 0) && ((uintptr_t)d_C % 16 == 0),
+             "gemm: operands must be 16-byte aligned");
+  FB_REQUIRE(lda % 8 == 0 && ldb % 8 == 0, "gemm: lda/ldb must be multiples of 8 elements");
+  FB_REQUIRE(ldc % 8 == 0, "gemm: ldc must be a multiple of 8 elements");
+  FB_REQUIRE(a_major == 0 || M % 64 == 0, "gemm: MN-major A needs M %% 64 == 0 (M=%d)", M);
+  FB_REQUIRE(b_major == 0 || N % 64 == 0, "gemm: MN-major B needs N %% 64 == 0 (N=%d)", N);
+  const bool need_aux = epilogue == FB_EPI_RESID_F32 || epilogue == FB_EPI_DGELU || epilogue == FB_EPI_RESID_F32_BF16;
+  const bool need_aux_out = epilogue == FB_EPI_GELU || epilogue == FB_EPI_RESID_F32_BF16;
+  FB_REQUIRE(!need_aux || d_aux, "gemm: epilogue %d needs aux", epilogue);
+  FB_REQUIRE(!need_aux_out || d_aux_out, "gemm: epilogue %d needs aux_out", epilogue);
+  int rc = get_encoder();
+  if (rc) return rc;
+  // tile width: 256 columns when that still fills the machine, else 128
+  const int tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256);
+  const int BN = (N >= 256 && tiles256 >= kNumSMs) ? 256 : 128;
+  CUtensorMap ta, tb;
+  rc = a_major ? make_map_mnmajor(&ta, d_A, M, K, lda, BM) : make_map_kmajor(&ta, d_A, M, K, lda, BM);
+  if (rc) return rc;
+  rc = b_major ? make_map_mnmajor(&tb, d_B, N, K, ldb, BN) : make_map_kmajor(&tb, d_B, N, K, ldb, BN);
+  if (rc) return rc;
+  EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux};
+  cudaStream_t st = (cudaStream_t)stream;
+  const int key = (BN == 256 ? 4 : 0) | (a_major ? 2 : 0) | (b_major ? 1 : 0);
+  switch (key) {
+    case 0: return dispatch_epi<128, 0, 0>(epilogue, ta, tb, M, N, K, ep, st);
+    case 1: return dispatch_epi<128, 0, 1>(epilogue, ta, tb, M, N, K, ep, st);
+    case 2: return dispatch_epi<128, 1, 0>(epilogue, ta, tb, M, N, K, ep, st);
+    case 3: return dispatch_epi<128, 1, 1>(epilogue, ta, tb, M, N, K, ep, st);
+    case 4: return dispatch_epi<256, 0, 0>(epilogue, ta, tb, M, N, K, ep, st);
+    case 5: return dispatch_epi<256, 0, 1>(epilogue, ta, tb, M, N, K, ep, st);
+    case 6: return dispatch_epi<256, 1, 0>(epilogue, ta, tb, M, N, K, ep, st);
+    case 7: return dispatch_epi<256, 1, 1>(epilogue, ta, tb, M, N, K, ep, st);
+  }
+  return FB_BAD_ARG;
+}

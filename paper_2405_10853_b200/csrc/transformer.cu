@@ -1,0 +1,296 @@
+// Non-GEMM transformer pieces of the reference TinyLM (fedforge/model.py):
+//   embedding gather / scatter-add      model.py:109, :145 (+ pos_embed :111, :147)
+//   LayerNorm eps=1e-5 fwd / bwd        model.py:81, :84, :113 (applied :90, :100, :150)
+//   mean next-token cross-entropy       model.py:226-229  (logits[:, :-1] vs tokens[:, 1:])
+//
+// B200 design: all row kernels are one warp per row with coalesced 32-lane
+// strides (HBM-bound; the fp32 residual stream is read once per kernel). LN
+// keeps the row in registers for a two-pass mean/variance (same formula torch
+// uses), writes the bf16 GEMM operand and saves mean/rstd for the backward.
+// dgamma/dbeta use per-CTA partial rows plus a fixed-order second pass, so they
+// are deterministic. CE reads each f32 logits row twice (max/sum pass, then the
+// softmax-minus-onehot pass) while it is L2-resident and writes bf16 dlogits for
+// the head dgrad/wgrad GEMMs; per-row losses go to a buffer that is reduced in
+// fixed order (no float atomics).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace fb {
+
+// ------------------------------------------------------------------ embedding
+__global__ void embed_fwd_kernel(const int32_t* __restrict__ tok, const float* __restrict__ emb,
+                                 const float* __restrict__ pos, float* __restrict__ x, int n_tok, int T, int d) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_tok) return;
+  const float* e = emb + (int64_t)tok[row] * d;
+  const float* p = pos ? pos + (int64_t)(row % T) * d : nullptr;
+  float* o = x + (int64_t)row * d;
+  for (int c = lane; c < d; c += 32) o[c] = p ? e[c] + p[c] : e[c];
+}
+
+__global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const float* __restrict__ dx,
+                                 float* __restrict__ gemb, float* __restrict__ gpos, int n_tok, int T, int d) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= n_tok) return;
+  const float* g = dx + (int64_t)row * d;
+  float* e = gemb + (int64_t)tok[row] * d;
+  float* p = gpos ? gpos + (int64_t)(row % T) * d : nullptr;
+  for (int c = lane; c < d; c += 32) {
+    const float v = g[c];
+    atomicAdd(e + c, v);
+    if (p) atomicAdd(p + c, v);
+  }
+}
+
+// ------------------------------------------------------------------ LayerNorm
+template <int NJ>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
+                                                     const float* __restrict__ beta, __nv_bfloat16* __restrict__ y,
+                                                     float* __restrict__ mean_out, float* __restrict__ rstd_out,
+                                                     int rows, int d) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* xr = x + (int64_t)row * d;
+  float v[NJ];
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int c = lane + 32 * j;
+    v[j] = c < d ? xr[c] : 0.f;
+    s += v[j];
+  }
+  const float mean = warp_sum(s) / d;
+  float q = 0.f;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int c = lane + 32 * j;
+    const float t = c < d ? v[j] - mean : 0.f;
+    q += t * t;
+  }
+  const float rstd = rsqrtf(warp_sum(q) / d + 1e-5f);
+  __nv_bfloat16* yr = y + (int64_t)row * d;
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int c = lane + 32 * j;
+    if (c < d) yr[c] = __float2bfloat16_rn((v[j] - mean) * rstd * gamma[c] + beta[c]);
+  }
+  if (lane == 0) {
+    mean_out[row] = mean;
+    rstd_out[row] = rstd;
+  }
+}
+
+// dx = dres + rstd * (g - mean(g) - xhat * mean(g * xhat)),  g = dy * gamma
+// partial dgamma/dbeta per CTA -> work[blockIdx][2][d]
+template <int NJ>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
+                                                     const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
+                                                     const float* __restrict__ dy, const float* __restrict__ dres,
+                                                     float* __restrict__ dx, __nv_bfloat16* __restrict__ dx_bf16,
+                                                     float* __restrict__ work, int rows, int d) {
+  extern __shared__ float sh_part[];  // [8 warps][2][d]
+  const int wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  float pg[NJ], pb[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) { pg[j] = 0.f; pb[j] = 0.f; }
+  for (int row = blockIdx.x * 8 + wid; row < rows; row += gridDim.x * 8) {
+    const float* xr = x + (int64_t)row * d;
+    const float* dyr = dy + (int64_t)row * d;
+    const float mu = mean_in[row], rs = rstd_in[row];
+    float xh[NJ], g[NJ];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int c = lane + 32 * j;
+      if (c < d) {
+        xh[j] = (xr[c] - mu) * rs;
+        const float dyv = dyr[c];
+        g[j] = dyv * gamma[c];
+        pg[j] += dyv * xh[j];
+        pb[j] += dyv;
+      } else {
+        xh[j] = 0.f;
+        g[j] = 0.f;
+      }
+      s1 += g[j];
+      s2 += g[j] * xh[j];
+    }
+    s1 = warp_sum(s1) / d;
+    s2 = warp_sum(s2) / d;
+    float* dxr = dx + (int64_t)row * d;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int c = lane + 32 * j;
+      if (c < d) {
+        float v = rs * (g[j] - s1 - xh[j] * s2);
+        if (dres) v += dres[(int64_t)row * d + c];
+        dxr[c] = v;
+        if (dx_bf16) dx_bf16[(int64_t)row * d + c] = __float2bfloat16_rn(v);
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int c = lane + 32 * j;
+    if (c < d) {
+      sh_part[(wid * 2 + 0) * d + c] = pg[j];
+      sh_part[(wid * 2 + 1) * d + c] = pb[j];
+    }
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float a = 0.f, b = 0.f;
+    for (int w = 0; w < 8; ++w) {
+      a += sh_part[(w * 2 + 0) * d + c];
+      b += sh_part[(w * 2 + 1) * d + c];
+    }
+    work[((int64_t)blockIdx.x * 2 + 0) * d + c] = a;
+    work[((int64_t)blockIdx.x * 2 + 1) * d + c] = b;
+  }
+}
+
+__global__ void ln_bwd_reduce_kernel(const float* __restrict__ work, int nparts, int d, float* __restrict__ dgamma,
+                                     float* __restrict__ dbeta) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d) return;
+  float a = 0.f, b = 0.f;
+  for (int p = 0; p < nparts; ++p) {
+    a += work[((int64_t)p * 2 + 0) * d + c];
+    b += work[((int64_t)p * 2 + 1) * d + c];
+  }
+  dgamma[c] += a;
+  dbeta[c] += b;
+}
+
+constexpr int kLnBwdBlocks = 296;
+
+// ------------------------------------------------------------------ cross-entropy
+// One CTA (256 threads) per logits row. Row r of the chunk is position t = (row0+r) % T.
+__global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logits, const int32_t* __restrict__ tok,
+                                                 __nv_bfloat16* __restrict__ dlogits, int row0, int T, int V,
+                                                 float scale, double* __restrict__ row_loss) {
+  __shared__ float red[8];
+  const int r = blockIdx.x;
+  const int grow = row0 + r;
+  const int t = grow % T;
+  const float* lr = logits + (int64_t)r * V;
+  __nv_bfloat16* dr = dlogits + (int64_t)r * V;
+  if (t == T - 1) {  // last position: not scored (logits[:, :-1])
+    for (int c = threadIdx.x; c < V; c += blockDim.x) dr[c] = __float2bfloat16_rn(0.f);
+    if (threadIdx.x == 0) row_loss[grow] = 0.0;
+    return;
+  }
+  const int target = tok[grow + 1];
+  float mx = -INFINITY;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, lr[c]);
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = red[0];
+  for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red[i]);
+  __syncthreads();
+  float s = 0.f;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) s += __expf(lr[c] - mx);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  s = 0.f;
+  for (int i = 0; i < 8; ++i) s += red[i];
+  const float lse = mx + logf(s);
+  const float inv = 1.0f / s;
+  for (int c = threadIdx.x; c < V; c += blockDim.x) {
+    float p = __expf(lr[c] - mx) * inv;
+    if (c == target) p -= 1.0f;
+    dr[c] = __float2bfloat16_rn(p * scale);
+  }
+  if (threadIdx.x == 0) row_loss[grow] = (double)(lse - lr[target]);
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" int fb_embed_fwd(const int32_t* d_tok, const float* d_emb, const float* d_pos, float* d_x, int n_tok,
+                            int T, int d, void* stream) {
+  FB_REQUIRE(n_tok > 0 && T > 0 && d > 0, "embed_fwd: bad shape");
+  embed_fwd_kernel<<<(n_tok + 7) / 8, 256, 0, (cudaStream_t)stream>>>(d_tok, d_emb, d_pos, d_x, n_tok, T, d);
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
+extern "C" int fb_embed_bwd(const int32_t* d_tok, const float* d_dx, float* d_gemb, float* d_gpos, int n_tok, int T,
+                            int d, int vocab, void* stream) {
+  FB_REQUIRE(n_tok > 0 && T > 0 && d > 0 && vocab > 0, "embed_bwd: bad shape");
+  embed_bwd_kernel<<<(n_tok + 7) / 8, 256, 0, (cudaStream_t)stream>>>(d_tok, d_dx, d_gemb, d_gpos, n_tok, T, d);
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
+#define LN_DISPATCH(NJ_MAX, CALL) \
+  if (nj <= NJ_MAX) { CALL(NJ_MAX); }
+
+extern "C" int fb_ln_fwd(const float* d_x, const float* d_gamma, const float* d_beta, void* d_y_bf16, float* d_mean,
+                         float* d_rstd, int rows, int d, void* stream) {
+  FB_REQUIRE(rows > 0 && d > 0 && d <= 4096, "ln_fwd: bad shape rows=%d d=%d", rows, d);
+  const int nj = (d + 31) / 32;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = (rows + 7) / 8;
+#define CALL_F(N) ln_fwd_kernel<N><<<grid, 256, 0, st>>>(d_x, d_gamma, d_beta, (__nv_bfloat16*)d_y_bf16, d_mean, d_rstd, rows, d)
+  if (nj <= 1) CALL_F(1);
+  else if (nj <= 2) CALL_F(2);
+  else if (nj <= 4) CALL_F(4);
+  else if (nj <= 8) CALL_F(8);
+  else if (nj <= 16) CALL_F(16);
+  else if (nj <= 24) CALL_F(24);
+  else if (nj <= 32) CALL_F(32);
+  else if (nj <= 64) CALL_F(64);
+  else CALL_F(128);
+#undef CALL_F
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
+extern "C" int fb_ln_bwd(const float* d_x, const float* d_gamma, const float* d_mean, const float* d_rstd,
+                         const float* d_dy, const float* d_dres, float* d_dx, void* d_dx_bf16, float* d_dgamma,
+                         float* d_dbeta, float* d_work, int rows, int d, void* stream) {
+  FB_REQUIRE(rows > 0 && d > 0 && d <= 4096, "ln_bwd: bad shape rows=%d d=%d", rows, d);
+  FB_REQUIRE(d_work != nullptr, "ln_bwd: needs a work buffer of %d floats", 2 * kLnBwdBlocks * d);
+  const int nj = (d + 31) / 32;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int grid = std::min((rows + 7) / 8, kLnBwdBlocks);
+  const size_t shm = (size_t)16 * d * sizeof(float);
+#define CALL_B(N)                                                                                       \
+  do {                                                                                                  \
+    auto k = ln_bwd_kernel<N>;                                                                          \
+    if (shm > 48 * 1024) FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm)); \
+    k<<<grid, 256, shm, st>>>(d_x, d_gamma, d_mean, d_rstd, d_dy, d_dres, d_dx, (__nv_bfloat16*)d_dx_bf16, d_work, rows, d); \
+  } while (0)
+  if (nj <= 1) CALL_B(1);
+  else if (nj <= 2) CALL_B(2);
+  else if (nj <= 4) CALL_B(4);
+  else if (nj <= 8) CALL_B(8);
+  else if (nj <= 16) CALL_B(16);
+  else if (nj <= 24) CALL_B(24);
+  else if (nj <= 32) CALL_B(32);
+  else if (nj <= 64) CALL_B(64);
+  else CALL_B(128);
+#undef CALL_B
+  FB_LAUNCH_CHECK();
+  ln_bwd_reduce_kernel<<<(d + 255) / 256, 256, 0, st>>>(d_work, grid, d, d_dgamma, d_dbeta);
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
+extern "C" int fb_ce_fwd_bwd(const float* d_logits, const int32_t* d_tok, void* d_dlogits, int row0, int rows, int T,
+                             int V, float scale, double* d_row_loss, void* stream) {
+  FB_REQUIRE(rows > 0 && T >= 2 && V > 0 && row0 >= 0, "ce: bad shape");
+  ce_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(d_logits, d_tok, (__nv_bfloat16*)d_dlogits, row0, T, V, scale,
+                                                     d_row_loss);
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}

@@ -1,0 +1,167 @@
+"""GPU parity of the individual sm_100a kernels through the C ABI.
+
+Integer/byte/f64-register paths are compared bit-exactly with the oracle /
+reference golden vectors; bf16 tensor-core GEMMs against a torch fp32 reference
+of the same op on the same bf16 inputs (tolerance stated per test)."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fb():
+    from paper_2405_10853_b200 import ext
+    ext.lib()
+    return ext
+
+
+def _ptr_array(ts):
+    arr = (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+    return arr
+
+
+@pytest.mark.parametrize("tag", ["k8", "k5", "k1", "k13"])
+@pytest.mark.parametrize("mode", ["det", "stream"])
+def test_fedagg_bitwise_vs_reference(fb, tag, mode):
+    g = golden("agg.npz")
+    w, m, wk, nk, arr = g[f"{tag}_w"], g[f"{tag}_m"], g[f"{tag}_wk"], g[f"{tag}_nk"], g[f"{tag}_arrival"]
+    order = sorted(arr) if mode == "det" else list(arr)
+    dev = torch.device("cuda")
+    W = torch.from_numpy(w).to(dev)
+    M = torch.from_numpy(m).to(dev)
+    ks = [torch.from_numpy(wk[k]).to(dev) for k in order]
+    nks = (C.c_int64 * len(order))(*[int(nk[k]) for k in order])
+    for eta, mu, nes in [(0.7, 0.9, True), (0.1, 0.9, False), (1.0, 0.0, True)]:
+        Wo, Mo = torch.empty_like(W), torch.empty_like(M)
+        stats = torch.zeros(3, dtype=torch.float64, device=dev)
+        bad = torch.zeros(1, dtype=torch.int64, device=dev)
+        fb.call("fb_fedagg_step_f32", _ptr_array(ks), nks, len(order), int(mode == "det"), W.data_ptr(),
+                M.data_ptr(), Wo.data_ptr(), Mo.data_ptr(), W.numel(), eta, mu, int(nes), stats.data_ptr(),
+                bad.data_ptr(), fb.stream_handle())
+        torch.cuda.synchronize()
+        key = f"{tag}_{mode}_{eta}_{mu}_{int(nes)}"
+        assert np.array_equal(Wo.cpu().numpy().view(np.uint32), g[key + "_w"].view(np.uint32))
+        assert np.array_equal(Mo.cpu().numpy().view(np.uint32), g[key + "_m"].view(np.uint32))
+        assert int(bad.item()) >= W.numel()
+        pg = g[f"{tag}_pg_{mode}"]
+        assert stats[0].item() == pytest.approx(float(np.dot(pg, pg)), rel=1e-12)
+
+
+def test_fedagg_f64delta_and_nonfinite(fb):
+    dev = torch.device("cuda")
+    W = torch.tensor([3.0e38, 1.0, 2.0], dtype=torch.float32, device=dev)
+    M = torch.zeros(3, dtype=torch.float32, device=dev)
+    d = torch.tensor([-3.0e38, 0.5, 0.25], dtype=torch.float64, device=dev)
+    Wo, Mo = torch.empty_like(W), torch.empty_like(M)
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    fb.call("fb_fedagg_step_f64delta", _ptr_array([d]), (C.c_int64 * 1)(5), 1, 1, W.data_ptr(), M.data_ptr(),
+            Wo.data_ptr(), Mo.data_ptr(), 3, 1.0, 0.0, 1, None, bad.data_ptr(), fb.stream_handle())
+    torch.cuda.synchronize()
+    assert bad.item() == 0
+    assert Wo[1].item() == 0.5 and Wo[2].item() == 1.75
+
+
+def test_adamw_bitwise_vs_reference(fb):
+    g = golden("adamw.npz")
+    dev = torch.device("cuda")
+    p = torch.from_numpy(g["p0"].copy()).to(dev)
+    m1, m2 = torch.zeros_like(p), torch.zeros_like(p)
+    shadow = torch.empty(p.numel(), dtype=torch.bfloat16, device=dev)
+    ctl = torch.zeros(6, dtype=torch.float64, device=dev)  # sizeof(fb_step_ctl) = 48
+    part = torch.zeros(fb.FB_RED_BLOCKS, dtype=torch.float64, device=dev)
+    pu = torch.zeros_like(part)
+    cfg = fb.AdamWCfg(float(g["beta1"]), float(g["beta2"]), float(g["eps"]), float(g["wd"]), 1e30)
+    for t in range(g["grads"].shape[0]):
+        gr = torch.from_numpy(g["grads"][t]).to(dev)
+        lr = float(g["lrs"][t])
+        fb.call("fb_sumsq_partials", gr.data_ptr(), gr.numel(), part.data_ptr(), fb.stream_handle())
+        fb.call("fb_step_prepare", part.data_ptr(), lr, 1 - float(g["beta1"]) ** (t + 1),
+                1 - float(g["beta2"]) ** (t + 1), 1e30, ctl.data_ptr(), fb.stream_handle())
+        fb.call("fb_adamw_step", p.data_ptr(), gr.data_ptr(), m1.data_ptr(), m2.data_ptr(), shadow.data_ptr(),
+                p.numel(), cfg, ctl.data_ptr(), pu.data_ptr(), None, None, fb.stream_handle())
+        torch.cuda.synchronize()
+        assert np.array_equal(p.cpu().numpy(), g["p"][t])
+        assert np.array_equal(m1.cpu().numpy(), g["m1"][t])
+        assert np.array_equal(m2.cpu().numpy(), g["m2"][t])
+        assert np.sqrt(pu.sum().item()) == pytest.approx(float(g["applied"][t]), rel=1e-12)
+    assert torch.equal(shadow, p.to(torch.bfloat16))
+
+
+def test_clip_decision(fb):
+    g = golden("adamw.npz")
+    dev = torch.device("cuda")
+    x = torch.from_numpy(g["clip_in"]).to(dev)
+    part = torch.zeros(fb.FB_RED_BLOCKS, dtype=torch.float64, device=dev)
+    ctl = torch.zeros(6, dtype=torch.float64, device=dev)
+    fb.call("fb_sumsq_partials", x.data_ptr(), x.numel(), part.data_ptr(), fb.stream_handle())
+    fb.call("fb_step_prepare", part.data_ptr(), 1e-3, 0.1, 0.05, 1.0, ctl.data_ptr(), fb.stream_handle())
+    torch.cuda.synchronize()
+    c = ctl.cpu().numpy()
+    assert np.sqrt(c[3]) == pytest.approx(float(g["clip_raw"]), rel=1e-13)
+    assert c[4] == pytest.approx(1.0 / float(g["clip_raw"]), rel=1e-13)
+    assert ctl.view(torch.int32)[10].item() == 1
+
+
+def _gemm(fb, A, B, a_major, b_major, M, N, K, epi="f32", C_=None, aux=None, aux_out=None, ld_aux=0):
+    if C_ is None:
+        C_ = torch.empty(M, N, dtype=torch.bfloat16 if epi in ("bf16", "gelu", "dgelu") else torch.float32,
+                         device=A.device)
+    fb.call("fb_gemm_bf16", M, N, K, A.data_ptr(), A.stride(0), a_major, B.data_ptr(), B.stride(0), b_major,
+            C_.data_ptr(), C_.stride(0), fb.EPI[epi], fb.ptr(aux), fb.ptr(aux_out), ld_aux, fb.stream_handle())
+    return C_
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 128, 64), (256, 512, 256), (300, 200, 104), (1024, 1536, 512),
+                                   (4096, 6144, 2048), (2048, 32000, 512)])
+@pytest.mark.parametrize("a_major,b_major", [(0, 0), (0, 1), (1, 1), (1, 0)])
+def test_gemm_layouts(fb, M, N, K, a_major, b_major):
+    if (a_major and M % 64) or (b_major and N % 64):
+        pytest.skip("MN-major needs multiples of 64")
+    torch.manual_seed(0)
+    dev = torch.device("cuda")
+    A = torch.randn(M, K, device=dev).to(torch.bfloat16)
+    B = torch.randn(N, K, device=dev).to(torch.bfloat16)
+    Ast = A.t().contiguous() if a_major else A
+    Bst = B.t().contiguous() if b_major else B
+    out = _gemm(fb, Ast, Bst, a_major, b_major, M, N, K)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().t()
+    err = (out - ref).abs().max().item()
+    assert err <= 1e-3 * K ** 0.5 + 1e-2, err
+
+
+def test_gemm_epilogues(fb):
+    torch.manual_seed(1)
+    dev = torch.device("cuda")
+    M, N, K = 512, 768, 384
+    A = torch.randn(M, K, device=dev).to(torch.bfloat16)
+    B = (0.05 * torch.randn(N, K, device=dev)).to(torch.bfloat16)
+    ref = A.float() @ B.float().t()
+    # bf16
+    o = _gemm(fb, A, B, 0, 0, M, N, K, "bf16")
+    torch.testing.assert_close(o.float(), ref, atol=3e-2, rtol=1e-2)
+    # acc_f32
+    base = torch.randn(M, N, device=dev)
+    o = _gemm(fb, A, B, 0, 0, M, N, K, "acc_f32", C_=base.clone())
+    torch.testing.assert_close(o, base + ref, atol=1e-3, rtol=1e-4)
+    # residual (in place)
+    r = base.clone()
+    o = _gemm(fb, A, B, 0, 0, M, N, K, "resid_f32", C_=r, aux=r, ld_aux=N)
+    torch.testing.assert_close(o, base + ref, atol=1e-3, rtol=1e-4)
+    # gelu + pre-activation
+    pre = torch.empty(M, N, dtype=torch.bfloat16, device=dev)
+    o = _gemm(fb, A, B, 0, 0, M, N, K, "gelu", aux_out=pre, ld_aux=N)
+    torch.testing.assert_close(pre.float(), ref, atol=3e-2, rtol=1e-2)
+    torch.testing.assert_close(o.float(), torch.nn.functional.gelu(pre.float()), atol=2e-2, rtol=1e-2)
+    # dgelu
+    o = _gemm(fb, A, B, 0, 0, M, N, K, "dgelu", aux=pre, ld_aux=N)
+    x = pre.float().requires_grad_()
+    torch.nn.functional.gelu(x).backward(ref)
+    torch.testing.assert_close(o.float(), x.grad, atol=3e-2, rtol=2e-2)
+    torch.cuda.synchronize()
