@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""Benchmark of the federated round hot path on B200.
+
+One bench "step" = one local AdamW step of one client on every rank (weak scaling:
+rank r trains client r): 64 micro-batches x 8 sequences x 2048 tokens = 1,048,576
+tokens of the 1.3B decoder (C4), data gathered on device, fwd/bwd on tcgen05,
+clip + fused AdamW. After the timed training steps, the round-end aggregation of
+8 clients x 1.339B params (fused delta + weighted mean + Nesterov step, and the
+NCCL exchange when N > 1) is timed the same way; the round time and round tokens/s
+are composed from those two measured pieces.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4]
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: model dims, batch (B x micro), clients K, local steps S, outer opt, schedule, corpus bytes
+    "c1": dict(V=256, d=512, L=2, H=8, T=128, B=16, micro=1, K=2, S=4, eta=1.0, mu=0.0, nesterov=True,
+               sched=(1e-3, 2, 1000, 0.1), n_bytes=400_000,
+               label="tiny decoder (6.56M), 2 clients x 4 local steps, FedAvg, seq 128"),
+    "c2": dict(V=32000, d=512, L=12, H=8, T=1024, B=16, micro=16, K=8, S=64, eta=1.0, mu=0.0, nesterov=True,
+               sched=(4e-4, 100, 88000, 1e-6), n_bytes=32_000_000,
+               label="75M decoder, 8 clients x 64 local steps, FedAvg, seq 1024"),
+    "c3": dict(V=32000, d=768, L=12, H=12, T=2048, B=8, micro=32, K=8, S=500, eta=0.1, mu=0.9, nesterov=True,
+               sched=(3e-4, 100, 15000, 1e-5), n_bytes=32_000_000,
+               label="125M decoder, 8 clients, Nesterov, seq 2048"),
+    "c4": dict(V=32000, d=2048, L=24, H=16, T=2048, B=8, micro=64, K=8, S=500, eta=0.7, mu=0.9, nesterov=True,
+               sched=(2e-4, 100, 24800, 0.1), n_bytes=32_000_000,
+               label="1.3B decoder, 8 clients x 500 local steps, Nesterov (eta 0.7, mu 0.9), seq 2048"),
+}
+METRIC = "round tokens/s at 1.3B, 8 clients, 1/2/4/8 GPU; aggregation GB/s vs roofline"
+
+
+def flops_per_token(c):
+    return 72 * c["L"] * c["d"] ** 2 + 6 * c["V"] * c["d"] + 6 * c["L"] * c["T"] * c["d"]
+
+
+def n_params(c):
+    V, d, L = c["V"], c["d"], c["L"]
+    return V * d + L * (12 * d * d + 4 * d) + 2 * d + d * V
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (clocks + throttle reasons)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.count(",") >= 8]
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[5 + i] and "Not" not in r[5 + i]})
+        loaded = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------ ours
+def run_ours(args, cfgname):
+    import torch
+    import torch.distributed as dist
+    from paper_2405_10853_b200 import data, ext
+    from paper_2405_10853_b200.config import AdamWConfig, ScheduleConfig, TinyLMConfig, TrainTask
+    from paper_2405_10853_b200.dist import ShardedAggregator, clients_of
+    from paper_2405_10853_b200.fedopt import DeviceVector
+    from paper_2405_10853_b200.model import LossEvaluator, init_params_host
+    from paper_2405_10853_b200.trainer import ClientSession
+
+    c = CONFIGS[cfgname]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ext.lib()
+    hbm, tf_burst, tf_sus, peak_kind = peaks()
+
+    cfg = TinyLMConfig(vocab_size=c["V"], context_len=c["T"], n_layers=c["L"], d_model=c["d"], n_heads=c["H"],
+                       seed=1234)
+    text = data.synth_corpus(99, c["n_bytes"])
+    corpus = data.tokenize_bytes(text, c["T"], c["V"])
+    split = data.split_corpus(corpus, c["K"], 99, 0.05)
+    client = rank % c["K"]
+    it = data.BatchIterator(corpus, split.shards[client], c["B"], 99)
+    ev = LossEvaluator(cfg)
+    w0 = DeviceVector(torch.from_numpy(init_params_host(cfg)).cuda())
+    N = len(w0)
+    sched = ScheduleConfig(*c["sched"])
+    adamw = AdamWConfig()
+    W, K = args.warmup, args.steps
+    task = TrainTask(1, client, W + K, 0, c["B"], c["micro"], {"data": 99}, "bench")
+    sess = ClientSession(ev, it, adamw, sched).begin(w0, task)
+    tokens_step = c["B"] * c["micro"] * c["T"]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for s in range(W):
+        sess.step(s)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ext.check(ext.lib().fb_profile_begin(20000), "profile")
+    torch.cuda.synchronize()
+    barrier()
+    e0.record(st)
+    for s in range(W, W + K):
+        sess.step(s)
+    e1.record(st)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    prof = (C.c_double * 9)()
+    ext.check(ext.lib().fb_profile_end(prof), "profile")
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    upd, tele = sess.finish()
+    losses = [x.loss for x in tele]
+    ms_step = ms / K
+    value = world * tokens_step / (ms_step / 1e3)
+
+    # ---------------- round-end aggregation: K clients x N params ----------------
+    del sess, ev
+    gemm_ms, gemm_n, gemm_fl = prof[0], int(prof[1]), prof[2]
+    afw_ms, afw_n, afw_fl = prof[3], int(prof[4]), prof[5]
+    abw_ms, abw_n, abw_fl = prof[6], int(prof[7]), prof[8]
+    torch.cuda.empty_cache()
+    Kc = c["K"]
+    mine = clients_of(rank, world, Kc)
+    gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    wglob = upd.w_start
+    local_w = {}
+    for k in mine:
+        x = torch.empty_like(wglob)
+        x.normal_(0.0, 2e-3, generator=gen)
+        x.add_(wglob)
+        local_w[k] = x
+    del upd
+    agg = ShardedAggregator(N, Kc)
+    m_shard = torch.zeros(agg.per, dtype=torch.float32, device="cuda")[: agg.hi - agg.lo]
+    m_shard.normal_(0.0, 1e-3, generator=gen)
+    nk = {k: split.shards[k].n_k for k in range(Kc)}
+    w_out = torch.empty_like(wglob)
+    reps = 5
+    # fused kernel alone (bytes of the shard-local launch), and exchange + kernel + all-gather
+    agg.exchange(local_w)
+    for _ in range(2):
+        agg.step(wglob, m_shard, nk, c["eta"], c["mu"], c["nesterov"], w_out=w_out)
+    torch.cuda.synchronize()
+    barrier()
+    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    cnt = agg.hi - agg.lo
+    import ctypes
+    ids = sorted(nk)
+    ptrs = (ctypes.c_void_p * Kc)(*[agg.src[k].data_ptr() for k in ids])
+    nks = (ctypes.c_int64 * Kc)(*[nk[k] for k in ids])
+    wo = torch.empty(cnt, dtype=torch.float32, device="cuda")
+    mo = torch.empty_like(wo)
+    k0.record()
+    for _ in range(reps):
+        ext.call("fb_fedagg_step_f32", ptrs, nks, Kc, 1, wglob[agg.lo:agg.hi].data_ptr(), m_shard.data_ptr(),
+                 wo.data_ptr(), mo.data_ptr(), cnt, c["eta"], c["mu"], int(c["nesterov"]), None, None, None,
+                 ext.stream_handle())
+    k1.record()
+    torch.cuda.synchronize()
+    agg_kernel_ms = k0.elapsed_time(k1) / reps
+    agg_bytes = (4 * Kc + 16) * cnt
+    barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record()
+    for _ in range(reps):
+        agg.exchange(local_w)
+        agg.step(wglob, m_shard, nk, c["eta"], c["mu"], c["nesterov"], w_out=w_out)
+    x1.record()
+    torch.cuda.synchronize()
+    agg_total_ms = x0.elapsed_time(x1) / reps
+    if world > 1:
+        t = torch.tensor([agg_kernel_ms, agg_total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        agg_kernel_ms, agg_total_ms = [float(v) for v in t.tolist()]
+    del local_w, agg
+    torch.cuda.empty_cache()
+
+    # ---------------- e2e: host buffers through the public train step ----------------
+    e2e = run_e2e(c, cfg, corpus, split, client, world, rank, K, barrier)
+
+    # ---------------- compose ----------------
+    clients_per_gpu = math.ceil(Kc / world)
+    round_s = clients_per_gpu * c["S"] * ms_step / 1e3 + agg_total_ms / 1e3
+    round_tokens = Kc * c["S"] * tokens_step
+    gemm_avg_ms = gemm_ms / max(gemm_n, 1)
+    gemm_tflops = gemm_fl / max(gemm_ms, 1e-9) / 1e9
+    step_tflops = flops_per_token(c) * tokens_step / (ms_step / 1e3) / 1e12
+    out = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": K,
+        "warmup": W,
+        "ms_per_step": round(ms_step, 2),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (reference Markov corpus seed 99, 32 MB; seeded reference init)",
+        "config": {"workload": f"{cfgname}: {c['label']}", "params": N, "tokens_per_step_per_gpu": tokens_step,
+                   "global_batch_seqs": c["B"] * c["micro"], "seq_len": c["T"], "clients": Kc,
+                   "clients_per_gpu": clients_per_gpu, "parallelism": f"clients sharded over {world} GPU(s)",
+                   "l2": "inputs > L2 (126 MB): every step streams 5.4 GB params/state and GB-scale activations"},
+        "gpu_launches": None,
+        "loss": [round(x, 4) for x in losses[-K:]],
+        "round": {"time_s": round(round_s, 2), "tokens_per_s": round(round_tokens / round_s, 1),
+                  "local_steps": c["S"], "agg_exchange_ms": round(agg_total_ms, 3),
+                  "agg_kernel_ms": round(agg_kernel_ms, 3),
+                  "agg_kernel_gbs": round(agg_bytes / (agg_kernel_ms / 1e3) / 1e9, 1),
+                  "agg_kernel_frac_hbm": round(agg_bytes / (agg_kernel_ms / 1e3) / 1e9 / hbm, 3),
+                  "agg_bytes_per_rank": agg_bytes},
+        "step_tensor": {"achieved_tflops": round(step_tflops, 1), "peak": tf_sus,
+                        "frac": round(step_tflops / tf_sus, 3), "note": "whole local step, algorithmic FLOPs (SURVEY 8d) vs sustained bf16"},
+        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tc_kernel (tcgen05)",
+                     "achieved": round(gemm_tflops, 1), "peak": tf_burst, "unit": "TFLOP/s",
+                     "frac": round(gemm_tflops / tf_burst, 3), "traffic": None,
+                     "launches_sampled": gemm_n, "avg_launch_ms": round(gemm_avg_ms, 4),
+                     "peak_kind": peak_kind,
+                     "gemm_share_of_step": round(gemm_ms / (ms_step * K) if gemm_n else 0, 3)},
+        "attention": {"fwd_tflops": round(afw_fl / max(afw_ms, 1e-9) / 1e9, 1),
+                      "bwd_tflops": round(abw_fl / max(abw_ms, 1e-9) / 1e9, 1)},
+        "clocks": clk,
+        "e2e": e2e,
+    }
+    # GPU launches of our kernels inside the timed region (per step, counted from the runtime's schedule)
+    L = c["L"]
+    chunks = math.ceil(c["B"] * c["T"] / 8192)
+    # gather + embed + L x (ln, qkv, attn, proj, ln, fc, proj2) + ln_f + chunks x (logits, ce, dgrad, wgrad)
+    # + ln_f bwd(2) + L x (6 GEMMs, 2 x ln bwd(2), attn bwd(3)) + embed bwd
+    per_micro = 1 + 1 + 7 * L + 1 + 4 * chunks + 2 + 15 * L + 1
+    out["gpu_launches"] = K * (c["micro"] * per_micro + 4)  # + sumsq, prepare, adamw, telemetry
+    if rank == 0 and world == 1 and not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(c, args.cpu_budget)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_e2e(c, cfg, corpus, split, client, world, rank, K, barrier):
+    """Same local step through the public C-ABI path but from HOST buffers: every step
+    copies its token batch from pinned host memory and reads the step's loss back."""
+    import torch
+    from paper_2405_10853_b200 import data
+    from paper_2405_10853_b200.config import AdamWConfig, ScheduleConfig, TrainTask
+    from paper_2405_10853_b200.fedopt import DeviceVector
+    from paper_2405_10853_b200.model import LossEvaluator, init_params_host
+    from paper_2405_10853_b200.trainer import ClientSession
+    B, micro, T = c["B"], c["micro"], c["T"]
+    rows_step = B * micro
+    it = data.BatchIterator(corpus, split.shards[client], B, 99)
+    # staging corpus: one step's rows, refilled from pinned host memory every step
+    stage = data.TokenizedCorpus(np.zeros(rows_step * T, dtype=np.uint16), cfg.vocab_size, T)
+    shard = data.ShardSpec(client, np.arange(rows_step))
+    sit = data.BatchIterator(stage, shard, B, 99)
+    sit.order = np.arange(rows_step, dtype=np.int64)
+    ev = LossEvaluator(cfg)
+    host_w = torch.from_numpy(init_params_host(cfg)).pin_memory()
+    sess = ClientSession(ev, sit, AdamWConfig(), ScheduleConfig(*c["sched"]))
+    pinned = torch.empty(rows_step * T, dtype=torch.int16).pin_memory()
+    sess.begin(DeviceVector(host_w.cuda(non_blocking=True)), TrainTask(1, client, 3 + K, 0, B, micro, {}, "e2e"))
+    dev_tokens = sess.dc.tokens
+    h2d = rows_step * T * 2
+    tele_host = torch.empty(8, dtype=torch.float64).pin_memory()
+
+    def one(s):
+        rows = np.concatenate([it.rows(it.cursor + j * B) for j in range(micro)])
+        it.cursor += micro * B
+        pinned.numpy()[:] = corpus.samples(rows).reshape(-1).view(np.int16)
+        dev_tokens.copy_(pinned, non_blocking=True)
+        sit.cursor = 0
+        sess.step(s)
+        tele_host.copy_(sess.tele[s * 8:(s + 1) * 8], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return float(tele_host[0])
+
+    for s in range(3):
+        one(s)
+    barrier()
+    t0 = time.perf_counter()
+    for s in range(3, 3 + K):
+        one(s)
+    el = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([el], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    tokens = world * K * rows_step * T
+    return {"value": round(tokens / el, 1), "unit": "tokens/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 64,
+            "path": "ClientSession.step -> fb_train_step (C ABI), tokens staged from pinned host each step"}
+
+
+# ------------------------------------------------------------------------------ CPU baseline
+def cpu_baseline(c, budget_s=20.0, sample_tokens=None):
+    """The reference's CPU path (oracle port, torch CPU fp32 + numpy f64) on a bounded
+    sample at the workload's exact shapes, extrapolated linearly to one local step:
+    fwd/bwd per token x tokens/step + (micro-accumulate + clip + AdamW + l2) per param x N."""
+    import torch
+    from oracle import localopt_ref, model_ref
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    V, d, L, H, T = c["V"], c["d"], c["L"], c["H"], c["T"]
+    tokens = sample_tokens or (128 if c["d"] >= 2048 else 512)
+    tokens = min(tokens, T)
+    rng = np.random.default_rng(0)
+    N = n_params(c)
+    w = np.asarray(rng.normal(0, 0.02, N), dtype=np.float32)
+    batch = rng.integers(33, 97, size=(1, tokens))
+    t0 = time.perf_counter()
+    model_ref.loss_and_grad(w, batch, V, T, L, d, H)
+    t_fb = time.perf_counter() - t0
+    del w
+    # optimizer pieces on a slice, extrapolated in N
+    n_s = 4_000_000
+    p = rng.normal(0, 0.02, n_s).astype(np.float32)
+    g = rng.normal(0, 1e-3, n_s).astype(np.float32)
+    z = np.zeros_like(p)
+    t0 = time.perf_counter()
+    acc = np.zeros(n_s)
+    if not np.isfinite(g).all():
+        raise RuntimeError
+    acc += g.astype(np.float64)
+    t_acc = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    gm = (acc / 1).astype(np.float32)
+    gc, _ = localopt_ref.clip(gm, 1.0)
+    p2, _, _, _ = localopt_ref.adamw(p, gc, z, z, 1, 1e-4)
+    localopt_ref.l2_norm(p2)
+    t_opt = time.perf_counter() - t0
+    tokens_step = c["B"] * c["micro"] * T
+    step_s = t_fb / tokens * tokens_step + (c["micro"] * t_acc + t_opt) / n_s * N
+    return {"value": round(tokens_step / step_s, 3), "unit": "tokens/s", "cores": cores, "kind": "port",
+            "sample": f"oracle loss_and_grad on 1x{tokens} tokens at the exact {c['d']}-d/{L}-layer/{V}-vocab shape "
+                      f"({t_fb:.1f}s) + accumulate/clip/AdamW on a {n_s // 10**6}M-param slice ({t_opt:.2f}s), "
+                      f"extrapolated to one local step ({tokens_step} tokens, {N} params)"}
+
+
+def run_reference(args, cfgname):
+    c = CONFIGS[cfgname]
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    vals = []
+    for _ in range(args.warmup):
+        cpu_baseline(c)
+    t0 = time.perf_counter()
+    last = None
+    for _ in range(args.steps):
+        last = cpu_baseline(c)
+        vals.append(last["value"])
+    v = statistics.mean(vals)
+    tokens_step = c["B"] * c["micro"] * c["T"]
+    out = {"metric": METRIC, "value": round(v, 3), "unit": "tokens/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tokens_step / v * 1e3, 1),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+           "data": "synthetic", "impl": "reference",
+           "config": {"workload": f"{cfgname}: {c['label']}"},
+           "cpu_baseline": {**last, "value": round(v, 3)},
+           "e2e": {"value": round(v, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+           "wall_s": round(time.perf_counter() - t0, 1)}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args, args.config)
+    else:
+        run_ours(args, args.config)
+
+
+if __name__ == "__main__":
+    main()

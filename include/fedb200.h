@@ -39,16 +39,18 @@ int fb_device_check(void); /* FB_OK iff device 0 is sm_100 (B200) */
  * registers; m' is rounded to f32 before it feeds w' (fedopt.py:189-196).
  * d_stats (optional, 3 doubles): ||pg||^2, ||w'||^2, ||m'||^2.
  * d_first_bad (optional, 1 int64): lowest index with a non-finite w' or m' (or n).
+ * d_pg_out (optional, n doubles): the f64 pseudo-gradient itself (AggregatorState.finalize).
+ * d_w_out/d_m_out may be NULL to only materialise the pseudo-gradient.
  * Returns FB_OK; the caller checks d_first_bad (no host sync inside). */
 int fb_fedagg_step_f32(const float* const* d_client_w, const int64_t* n_k, int n_clients,
                        int deterministic, const float* d_w, const float* d_m, float* d_w_out,
                        float* d_m_out, int64_t n, double eta, double mu, int nesterov,
-                       double* d_stats, int64_t* d_first_bad, void* stream);
+                       double* d_stats, int64_t* d_first_bad, double* d_pg_out, void* stream);
 /* Same contract for reference-format f64 deltas (ClientUpdate.delta, fedopt.py:26-46). */
 int fb_fedagg_step_f64delta(const double* const* d_deltas, const int64_t* n_k, int n_clients,
                             int deterministic, const float* d_w, const float* d_m, float* d_w_out,
                             float* d_m_out, int64_t n, double eta, double mu, int nesterov,
-                            double* d_stats, int64_t* d_first_bad, void* stream);
+                            double* d_stats, int64_t* d_first_bad, double* d_pg_out, void* stream);
 
 /* ---- client optimizer (K10-K12) --------------------------------------------------- */
 /* d_partials[FB_RED_BLOCKS] = per-block sum of x^2 (f64). l2_norm: params.py:126-133 */
@@ -130,6 +132,55 @@ int fb_ce_fwd_bwd(const float* d_logits, const int32_t* d_tok, void* d_dlogits, 
  * rows = order[(cursor + i) mod n_order]; tok[i][t] = corpus[rows[i]*T + t] */
 int fb_gather_batch(const uint16_t* d_corpus, const int64_t* d_order, int64_t n_order,
                     int64_t cursor, int batch, int T, int32_t* d_tok, void* stream);
+
+
+/* ---- native runtime: whole TinyLM micro-batch and whole local step ----------------
+ * TinyLMConfig (model.py:28-43). Flat parameter layout = the reference manifest
+ * order (model.py:184-190): embed, [pos_embed], per block {ln1.w, ln1.b, qkv, attn_proj,
+ * ln2.w, ln2.b, mlp_fc, mlp_proj}, ln_f.w, ln_f.b, head. GPU path constraints:
+ * d_model % 64 == 0, head dim in {64, 128}, vocab % 64 == 0, T % 64 == 0. */
+typedef struct {
+  int32_t vocab, ctx, n_layers, d_model, n_heads, use_alibi;
+} fb_model_cfg;
+
+int64_t fb_model_n_params(const fb_model_cfg* cfg);
+/* bytes of device workspace for one micro-batch of `batch` sequences of length T */
+int64_t fb_model_workspace_bytes(const fb_model_cfg* cfg, int batch, int T);
+/* Forward (+ backward when want_grad) of one micro-batch: LossEvaluator.loss_and_grad
+ * (model.py:237-250). Gradients ACCUMULATE into d_grad (f32, manifest order), scaled by
+ * grad_scale (1 / (B*(T-1)) / n_micro); per-row CE goes to d_row_loss[B*T] (f64,
+ * 0 on each sequence's last position). d_shadow = bf16 copy of d_params. */
+int fb_model_fwd_bwd(const fb_model_cfg* cfg, const float* d_params, const void* d_shadow, float* d_grad,
+                     const int32_t* d_tok, int batch, int T, float grad_scale, double* d_row_loss,
+                     int want_grad, void* d_ws, int64_t ws_bytes, void* stream);
+
+typedef struct {
+  const uint16_t* d_corpus; /* token stream (uint16, data.py:57) */
+  const int64_t* d_order;   /* this client's sample order (data.py:141-144) */
+  int64_t n_order;          /* n_k */
+  int32_t seq_len, batch, micro;
+  int32_t pad;
+  int64_t cursor;           /* sample cursor at the start of this step */
+} fb_data_desc;
+
+/* One local optimizer step of train_round (trainer.py:78-101): micro-batch fwd/bwd with
+ * gradient accumulation, global-norm clip decision on device, fused AdamW (+ bf16
+ * shadow), telemetry into d_tele[8]: {sum of micro mean losses / micro, ||g||^2,
+ * ||u||^2, ||w'||^2, lr, first non-finite param index (as double, or -1)}.
+ * d_scratch: FB_RED_BLOCKS*2 + 8 doubles + sizeof(fb_step_ctl); d_row_loss: micro*B*T doubles. */
+int fb_train_step(const fb_model_cfg* cfg, float* d_params, void* d_shadow, float* d_grad, float* d_m1,
+                  float* d_m2, const fb_data_desc* data, fb_adamw_cfg opt, double lr, double bc1, double bc2,
+                  double* d_tele, double* d_scratch, double* d_row_loss, void* d_ws, int64_t ws_bytes,
+                  void* stream);
+
+
+/* ---- live kernel profiling (used by bench.py inside its timed region) --------------
+ * While enabled, every fb_gemm_bf16 / fb_attn_* launch is bracketed by CUDA events on
+ * its own stream (first max_launches launches per category). fb_profile_end syncs
+ * and returns per category {total ms, launches, algorithmic flops} for
+ * categories 0 = GEMM, 1 = attention fwd, 2 = attention bwd: out[9]. */
+int fb_profile_begin(int max_launches);
+int fb_profile_end(double* out9);
 
 #ifdef __cplusplus
 }

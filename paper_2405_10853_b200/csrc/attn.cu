@@ -457,8 +457,14 @@ extern "C" int fb_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, in
                            void* stream) {
   FB_REQUIRE(B > 0 && H > 0 && T > 0 && T % 64 == 0, "attn_fwd: T must be a positive multiple of 64 (T=%d)", T);
   cudaStream_t st = (cudaStream_t)stream;
-  if (dh == 64) return attn_fwd_launch<64>(d_qkv, d_o, d_lse, B, T, H, use_alibi, st);
-  if (dh == 128) return attn_fwd_launch<128>(d_qkv, d_o, d_lse, B, T, H, use_alibi, st);
+  // algorithmic flops: causal lower triangle, QK^T and PV (2*T*d per layer-token fwd)
+  const double fl = 2.0 * 2.0 * B * H * (double)T * (T + 1) / 2.0 * dh;
+  const int pi = prof_on() ? prof_start(1, st) : -1;
+  int rc = FB_UNSUPPORTED;
+  if (dh == 64) rc = attn_fwd_launch<64>(d_qkv, d_o, d_lse, B, T, H, use_alibi, st);
+  else if (dh == 128) rc = attn_fwd_launch<128>(d_qkv, d_o, d_lse, B, T, H, use_alibi, st);
+  prof_stop(1, pi, st, fl);
+  if (rc != FB_UNSUPPORTED) return rc;
   set_error("attn_fwd: head dim %d unsupported (64 or 128)", dh);
   return FB_UNSUPPORTED;
 }
@@ -468,8 +474,13 @@ extern "C" int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do,
   FB_REQUIRE(B > 0 && H > 0 && T > 0 && T % 64 == 0, "attn_bwd: T must be a positive multiple of 64 (T=%d)", T);
   FB_REQUIRE(d_work != nullptr, "attn_bwd: needs a work buffer of B*H*T + B*T*H*dh floats");
   cudaStream_t st = (cudaStream_t)stream;
-  if (dh == 64) return attn_bwd_launch<64>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, H, use_alibi, st);
-  if (dh == 128) return attn_bwd_launch<128>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, H, use_alibi, st);
+  const double fl = 2.0 * 2.0 * 2.0 * B * H * (double)T * (T + 1) / 2.0 * dh;  // bwd = 2x fwd
+  const int pi = prof_on() ? prof_start(2, st) : -1;
+  int rc = FB_UNSUPPORTED;
+  if (dh == 64) rc = attn_bwd_launch<64>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, H, use_alibi, st);
+  else if (dh == 128) rc = attn_bwd_launch<128>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, H, use_alibi, st);
+  prof_stop(2, pi, st, fl);
+  if (rc != FB_UNSUPPORTED) return rc;
   set_error("attn_bwd: head dim %d unsupported (64 or 128)", dh);
   return FB_UNSUPPORTED;
 }

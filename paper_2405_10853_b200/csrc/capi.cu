@@ -26,3 +26,73 @@ extern "C" int fb_device_check(void) {
   }
   return FB_OK;
 }
+
+// ---------------------------------------------------------------- live profiler
+#include <mutex>
+#include <vector>
+namespace fb {
+struct ProfCat {
+  std::vector<cudaEvent_t> ev;
+  int n = 0;
+  double flops = 0.0;
+};
+static struct {
+  bool on = false;
+  int cap = 0;
+  ProfCat cat[3];
+  std::mutex mu;
+} g_prof;
+
+bool prof_on() { return g_prof.on; }
+int prof_start(int cat, cudaStream_t st) {
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  ProfCat& c = g_prof.cat[cat];
+  if (!g_prof.on || c.n >= g_prof.cap) return -1;
+  const int i = c.n++;
+  cudaEventRecord(c.ev[2 * i], st);
+  return i;
+}
+void prof_stop(int cat, int i, cudaStream_t st, double flops) {
+  if (i < 0) return;
+  std::lock_guard<std::mutex> lk(g_prof.mu);
+  ProfCat& c = g_prof.cat[cat];
+  cudaEventRecord(c.ev[2 * i + 1], st);
+  c.flops += flops;
+}
+}  // namespace fb
+
+extern "C" int fb_profile_begin(int max_launches) {
+  std::lock_guard<std::mutex> lk(fb::g_prof.mu);
+  FB_REQUIRE(max_launches > 0 && max_launches <= 1 << 20, "bad max_launches");
+  for (auto& c : fb::g_prof.cat) {
+    while ((int)c.ev.size() < 2 * max_launches) {
+      cudaEvent_t e;
+      FB_CUDA_TRY(cudaEventCreate(&e));
+      c.ev.push_back(e);
+    }
+    c.n = 0;
+    c.flops = 0.0;
+  }
+  fb::g_prof.cap = max_launches;
+  fb::g_prof.on = true;
+  return FB_OK;
+}
+
+extern "C" int fb_profile_end(double* out) {
+  std::lock_guard<std::mutex> lk(fb::g_prof.mu);
+  fb::g_prof.on = false;
+  for (int k = 0; k < 3; ++k) {
+    fb::ProfCat& c = fb::g_prof.cat[k];
+    double ms = 0.0;
+    for (int i = 0; i < c.n; ++i) {
+      FB_CUDA_TRY(cudaEventSynchronize(c.ev[2 * i + 1]));
+      float t = 0.f;
+      FB_CUDA_TRY(cudaEventElapsedTime(&t, c.ev[2 * i], c.ev[2 * i + 1]));
+      ms += t;
+    }
+    out[3 * k + 0] = ms;
+    out[3 * k + 1] = c.n;
+    out[3 * k + 2] = c.flops;
+  }
+  return FB_OK;
+}

@@ -12,6 +12,10 @@ namespace fb {
 
 // Last error message (thread-local), surfaced through fb_last_error().
 void set_error(const char* fmt, ...);
+// live profiler hooks (capi.cu)
+bool prof_on();
+int prof_start(int cat, cudaStream_t st);
+void prof_stop(int cat, int i, cudaStream_t st, double flops);
 
 #define FB_CUDA_TRY(expr)                                                           \
   do {                                                                              \

@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
                                                      float* __restrict__ w_out,
                                                      float* __restrict__ m_out, int64_t n,
                                                      double eta, double mu, int nesterov,
-                                                     double* stats, unsigned long long* first_bad) {
+                                                     double* stats, unsigned long long* first_bad,
+                                                     double* __restrict__ pg_out) {
   __shared__ double red[3][8];
   double s_pg = 0.0, s_w = 0.0, s_m = 0.0;
   unsigned long long bad = ~0ull;
@@ -162,6 +163,11 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
 #pragma unroll
       for (int e = 0; e < VEC; ++e) pg[e] = __ddiv_rn(sum[e], total);
     }
+    if (pg_out) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) pg_out[j0 + e] = pg[e];
+    }
+    if (!w_out) continue;
     float wo[VEC], mo[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
@@ -198,13 +204,16 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
       for (int k = 0; k < K; ++k) s = __dadd_rn(s, __dmul_rn(P.nk[k], delta_of<TIn>(P.src[k], j, wg)));
       pgv = __ddiv_rn(s, total);
     }
-    StepOut o = outer_step(w[j], m[j], pgv, eta, mu, nesterov);
-    w_out[j] = o.w;
-    m_out[j] = o.m;
+    if (pg_out) pg_out[j] = pgv;
     s_pg += pgv * pgv;
-    s_w += (double)o.w * (double)o.w;
-    s_m += (double)o.m * (double)o.m;
-    if (!(isfinite(o.w) && isfinite(o.m)) && (unsigned long long)j < bad) bad = (unsigned long long)j;
+    if (w_out) {
+      StepOut o = outer_step(w[j], m[j], pgv, eta, mu, nesterov);
+      w_out[j] = o.w;
+      m_out[j] = o.m;
+      s_w += (double)o.w * (double)o.w;
+      s_m += (double)o.m * (double)o.m;
+      if (!(isfinite(o.w) && isfinite(o.m)) && (unsigned long long)j < bad) bad = (unsigned long long)j;
+    }
   }
   if (first_bad) {
     // warp-min then one atomic per warp
@@ -233,7 +242,7 @@ template <typename TIn>
 static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int deterministic,
                          const float* w, const float* m, float* w_out, float* m_out, int64_t n,
                          double eta, double mu, int nesterov, double* stats, int64_t* first_bad,
-                         cudaStream_t st) {
+                         double* pg_out, cudaStream_t st) {
   FB_REQUIRE(K >= 1 && K <= FB_MAX_CLIENTS, "n_clients=%d outside [1, %d]", K, FB_MAX_CLIENTS);
   FB_REQUIRE(n > 0, "model length must be positive, got %lld", (long long)n);
   FB_REQUIRE(eta > 0.0, "server eta must be > 0, got %g", eta);
@@ -241,8 +250,10 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
   AggParams<TIn> P;
   double total = 0.0;
   int64_t itotal = 0;
+  FB_REQUIRE((w_out == nullptr) == (m_out == nullptr), "w_out and m_out must both be set or both NULL");
+  FB_REQUIRE(w_out || pg_out, "nothing to compute");
   bool aligned = ((uintptr_t)w % 16 == 0) && ((uintptr_t)m % 16 == 0) && ((uintptr_t)w_out % 16 == 0) &&
-                 ((uintptr_t)m_out % 16 == 0);
+                 ((uintptr_t)m_out % 16 == 0) && ((uintptr_t)pg_out % 8 == 0);
   for (int k = 0; k < K; ++k) {
     FB_REQUIRE(n_k[k] >= 1, "client %d: n_k must be >= 1, got %lld", k, (long long)n_k[k]);
     FB_REQUIRE(src[k] != nullptr, "client %d: null pointer", k);
@@ -260,13 +271,13 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
     int blocks = (int)(work < kNumSMs * 8 ? (work > 0 ? work : 1) : kNumSMs * 8);
     fedagg_kernel<TIn, 4><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, m_out, n,
                                                       eta, mu, nesterov, stats,
-                                                      (unsigned long long*)first_bad);
+                                                      (unsigned long long*)first_bad, pg_out);
   } else {
     int64_t work = (n + threads - 1) / threads;
     int blocks = (int)(work < kNumSMs * 8 ? (work > 0 ? work : 1) : kNumSMs * 8);
     fedagg_kernel<TIn, 1><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, m_out, n,
                                                       eta, mu, nesterov, stats,
-                                                      (unsigned long long*)first_bad);
+                                                      (unsigned long long*)first_bad, pg_out);
   }
   FB_LAUNCH_CHECK();
   return FB_OK;
@@ -277,15 +288,17 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
 extern "C" int fb_fedagg_step_f32(const float* const* d_client_w, const int64_t* n_k, int n_clients,
                                   int deterministic, const float* d_w, const float* d_m, float* d_w_out,
                                   float* d_m_out, int64_t n, double eta, double mu, int nesterov,
-                                  double* d_stats, int64_t* d_first_bad, void* stream) {
+                                  double* d_stats, int64_t* d_first_bad, double* d_pg_out,
+                                  void* stream) {
   return fb::launch_fedagg<float>(d_client_w, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n,
-                                  eta, mu, nesterov, d_stats, d_first_bad, (cudaStream_t)stream);
+                                  eta, mu, nesterov, d_stats, d_first_bad, d_pg_out, (cudaStream_t)stream);
 }
 
 extern "C" int fb_fedagg_step_f64delta(const double* const* d_deltas, const int64_t* n_k, int n_clients,
                                        int deterministic, const float* d_w, const float* d_m, float* d_w_out,
                                        float* d_m_out, int64_t n, double eta, double mu, int nesterov,
-                                       double* d_stats, int64_t* d_first_bad, void* stream) {
+                                       double* d_stats, int64_t* d_first_bad, double* d_pg_out,
+                                       void* stream) {
   return fb::launch_fedagg<double>(d_deltas, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n,
-                                   eta, mu, nesterov, d_stats, d_first_bad, (cudaStream_t)stream);
+                                   eta, mu, nesterov, d_stats, d_first_bad, d_pg_out, (cudaStream_t)stream);
 }

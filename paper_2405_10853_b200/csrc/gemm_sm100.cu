@@ -375,6 +375,10 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, i
 
 }  // namespace fb
 
+namespace fb {
+int gemm_dispatch(int key, int epilogue, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                  const EpiArgs& ep, cudaStream_t st);
+}
 using namespace fb;
 
 extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, int a_major, const void* d_B,
@@ -405,6 +409,15 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux};
   cudaStream_t st = (cudaStream_t)stream;
   const int key = (BN == 256 ? 4 : 0) | (a_major ? 2 : 0) | (b_major ? 1 : 0);
+  const int pi = prof_on() ? prof_start(0, st) : -1;
+  rc = gemm_dispatch(key, epilogue, ta, tb, M, N, K, ep, st);
+  prof_stop(0, pi, st, 2.0 * M * N * (double)K);
+  return rc;
+}
+
+namespace fb {
+int gemm_dispatch(int key, int epilogue, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                  const EpiArgs& ep, cudaStream_t st) {
   switch (key) {
     case 0: return dispatch_epi<128, 0, 0>(epilogue, ta, tb, M, N, K, ep, st);
     case 1: return dispatch_epi<128, 0, 1>(epilogue, ta, tb, M, N, K, ep, st);
@@ -417,3 +430,4 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   }
   return FB_BAD_ARG;
 }
+}  // namespace fb

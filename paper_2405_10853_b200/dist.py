@@ -1,0 +1,100 @@
+"""Multi-GPU round-end exchange: clients sharded over ranks, one fused aggregation.
+
+Partitioning: client k trains on rank k mod G; its end weights w_k
+stay in that rank's HBM. At round end every rank needs, for its N/G slice of the
+parameter vector, every client's slice — an all-to-all of f32 client shards
+(grouped NCCL send/recv over NVLink 5). Each rank then runs the single-GPU fused
+kernel (fb_fedagg_step_f32) on its slice with the clients in id order, which
+makes the result bit-identical to G = 1 (the f64 pairwise tree never crosses a
+rank boundary), and an all-gather of f32 w' rebuilds the global model on every
+rank. Momentum stays sharded. Bytes per rank per direction:
+4 N ceil(K/G) (G-1)/G (all-to-all) + 4 N (G-1)/G (all-gather).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import ext
+
+
+def shard_bounds(n: int, world: int, rank: int, align: int = 4):
+    """Contiguous, 16-byte aligned slice [lo, hi) of an n-vector owned by `rank`."""
+    per = ((n + world - 1) // world + align - 1) // align * align
+    lo = min(n, rank * per)
+    hi = min(n, lo + per)
+    return lo, hi, per
+
+
+def clients_of(rank: int, world: int, n_clients: int):
+    return [k for k in range(n_clients) if k % world == rank]
+
+
+class ShardedAggregator:
+    """Round-end aggregation + outer step across `world` ranks (torch.distributed / NCCL).
+
+    local: {client_id: f32 device tensor [N]} for the clients this rank trained;
+    n_k:   {client_id: n_k} for ALL contributing clients (known from the round plan).
+    w: the global model (replicated, f32 [N]); m_shard: this rank's momentum slice."""
+
+    def __init__(self, n: int, n_clients: int, group=None):
+        import torch
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.n = n
+        self.K = n_clients
+        self.lo, self.hi, self.per = shard_bounds(n, self.world, self.rank)
+        dev = torch.device("cuda", torch.cuda.current_device())
+        # receive buffers: one slice per client (padded to `per`); none needed on one GPU
+        self.recv = torch.empty(self.K if self.world > 1 else 0, self.per, dtype=torch.float32, device=dev)
+        self.src = {}
+        self.w_full = torch.empty(self.per * self.world, dtype=torch.float32, device=dev)
+        self.stats = torch.empty(3, dtype=torch.float64, device=dev)
+        self.bad = torch.empty(1, dtype=torch.int64, device=dev)
+
+    def exchange(self, local: dict):
+        """all-to-all: every client's slice r lands on rank r (grouped send/recv)."""
+        if self.world == 1:
+            self.src = dict(local)
+            return
+        self.src = {k: self.recv[k] for k in range(self.K)}
+        dist = self.dist
+        ops = []
+        for k in range(self.K):
+            owner = k % self.world
+            if owner == self.rank:
+                wk = local[k]
+                for r in range(self.world):
+                    lo, hi, _ = shard_bounds(self.n, self.world, r)
+                    if r == self.rank:
+                        self.recv[k, : hi - lo].copy_(wk[lo:hi], non_blocking=True)
+                    elif hi > lo:
+                        ops.append(dist.P2POp(dist.isend, wk[lo:hi], r, self.group))
+            elif self.hi > self.lo:
+                ops.append(dist.P2POp(dist.irecv, self.recv[k, : self.hi - self.lo], owner, self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+    def step(self, w, m_shard, n_k: dict, eta, mu, nesterov, deterministic=True, w_out=None):
+        """Fused aggregation + outer step on this rank's slice, then all-gather of w'."""
+        import torch
+        cnt = self.hi - self.lo
+        ids = sorted(n_k) if deterministic else list(n_k)
+        ptrs = (C.c_void_p * len(ids))(*[self.src[k].data_ptr() for k in ids])
+        nks = (C.c_int64 * len(ids))(*[int(n_k[k]) for k in ids])
+        w_slice = w[self.lo:self.hi]
+        m_new = torch.empty_like(m_shard)
+        wo = self.w_full[self.rank * self.per: self.rank * self.per + cnt]
+        if cnt > 0:
+            ext.call("fb_fedagg_step_f32", ptrs, nks, len(ids), int(deterministic), w_slice.data_ptr(),
+                     m_shard.data_ptr(), wo.data_ptr(), m_new.data_ptr(), cnt, float(eta), float(mu), int(nesterov),
+                     self.stats.data_ptr(), self.bad.data_ptr(), None, ext.stream_handle())
+        if self.world > 1:
+            self.dist.all_gather_into_tensor(self.w_full, self.w_full[self.rank * self.per:(self.rank + 1) * self.per],
+                                             group=self.group)
+        out = w_out if w_out is not None else torch.empty_like(w)
+        out.copy_(self.w_full[: self.n])
+        return out, m_new

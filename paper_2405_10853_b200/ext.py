@@ -35,8 +35,8 @@ class StepCtl(C.Structure):
 SIGNATURES = {
     "fb_abi_version": [],
     "fb_device_check": [],
-    "fb_fedagg_step_f32": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _i64, _d, _d, _i, _vp, _vp, _vp],
-    "fb_fedagg_step_f64delta": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _i64, _d, _d, _i, _vp, _vp, _vp],
+    "fb_fedagg_step_f32": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _i64, _d, _d, _i, _vp, _vp, _vp, _vp],
+    "fb_fedagg_step_f64delta": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _i64, _d, _d, _i, _vp, _vp, _vp, _vp],
     "fb_sumsq_partials": [_vp, _i64, _vp, _vp],
     "fb_sum_partials": [_vp, _i, _vp, _vp],
     "fb_step_prepare": [_vp, _d, _d, _d, _d, _vp, _vp],
@@ -51,7 +51,21 @@ SIGNATURES = {
     "fb_attn_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "fb_ce_fwd_bwd": [_vp, _vp, _vp, _i, _i, _i, _i, C.c_float, _vp, _vp],
     "fb_gather_batch": [_vp, _vp, _i64, _i64, _i, _i, _vp, _vp],
+    "fb_profile_begin": [_i],
+    "fb_profile_end": [_vp],
+    "fb_model_fwd_bwd": [_vp, _vp, _vp, _vp, _vp, _i, _i, C.c_float, _vp, _i, _vp, _i64, _vp],
+    "fb_train_step": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, AdamWCfg, _d, _d, _d, _vp, _vp, _vp, _vp, _i64, _vp],
 }
+
+class ModelCfg(C.Structure):
+    _fields_ = [("vocab", C.c_int32), ("ctx", C.c_int32), ("n_layers", C.c_int32), ("d_model", C.c_int32),
+                ("n_heads", C.c_int32), ("use_alibi", C.c_int32)]
+
+
+class DataDesc(C.Structure):
+    _fields_ = [("d_corpus", _vp), ("d_order", _vp), ("n_order", _i64), ("seq_len", C.c_int32),
+                ("batch", C.c_int32), ("micro", C.c_int32), ("pad", C.c_int32), ("cursor", _i64)]
+
 
 _lib = None
 _lock = threading.Lock()
@@ -75,6 +89,11 @@ def lib(require_device: bool = True):
                     continue
                 fn.argtypes = args
                 fn.restype = C.c_int
+            for name in ("fb_model_n_params",):
+                getattr(L, name).argtypes = [C.POINTER(ModelCfg)]
+                getattr(L, name).restype = C.c_int64
+            L.fb_model_workspace_bytes.argtypes = [C.POINTER(ModelCfg), _i, _i]
+            L.fb_model_workspace_bytes.restype = C.c_int64
             L.fb_last_error.argtypes = []
             L.fb_last_error.restype = C.c_char_p
             _lib = L

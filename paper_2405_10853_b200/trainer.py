@@ -1,0 +1,152 @@
+"""Client half of the round: `train_round`, the Flower-style `fit`.
+
+Drop-in for fedforge/trainer.py:54-114 (same signature, same TrainTask /
+StepTelemetry / ClientUpdate contract, same schedule-offset and cursor
+semantics, same errors). Each local step is ONE call into the native runtime
+(fb_train_step: device data gather -> micro-batch fwd/bwd on tcgen05 ->
+deterministic grad-norm + clip decision -> fused AdamW + bf16 shadow ->
+telemetry), so the round runs without host synchronisation; telemetry comes
+back in a single device->host copy at the end of the round.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+
+from . import ext
+from .config import AdamWConfig, ScheduleConfig, StepTelemetry, TrainTask, lr_at
+from .data import BatchIterator, DeviceCorpus
+from .errors import ParamError, RoundFailedError
+from .fedopt import DeviceClientUpdate, DeviceVector
+from .model import LossEvaluator, check_gpu_shape
+from .params import ParamVector
+
+N_TELE = 8
+
+_corpora: dict = {}
+
+
+def device_corpus(batches: BatchIterator, device) -> DeviceCorpus:
+    key = (id(batches.corpus), str(device))
+    dc = _corpora.get(key)
+    if dc is None or dc.corpus is not batches.corpus:
+        dc = DeviceCorpus(batches.corpus, device)
+        _corpora[key] = dc
+    return dc
+
+
+class RoundBuffers:
+    """Per-evaluator scratch for the step loop (reused across rounds)."""
+
+    def __init__(self, ev: LossEvaluator):
+        import torch
+        self.scratch = torch.zeros(3 * ext.FB_RED_BLOCKS + 16, dtype=torch.float64, device=ev.device)
+        self.row_loss = None
+
+    def rows(self, n, device):
+        import torch
+        if self.row_loss is None or self.row_loss.numel() < n:
+            self.row_loss = torch.empty(n, dtype=torch.float64, device=device)
+        return self.row_loss
+
+
+class ClientSession:
+    """One client's round on the device, step by step (train_round is a thin loop over it).
+
+    begin() places the received global in HBM (no copy if it already is), resets the
+    AdamW moments and positions the data cursor; step() enqueues one whole local step
+    (no host sync); finish() does the round's single device->host copy of telemetry."""
+
+    def __init__(self, evaluator: LossEvaluator, batches: BatchIterator, adamw_cfg: AdamWConfig,
+                 sched: ScheduleConfig):
+        self.ev, self.batches, self.adamw_cfg, self.sched = evaluator, batches, adamw_cfg, sched
+        cfg = evaluator.cfg
+        self.T = batches.corpus.sequence_len
+        if self.T > cfg.context_len:
+            raise ParamError(f"sequence length {self.T} exceeds context_len {cfg.context_len}")
+        check_gpu_shape(cfg, self.T)
+        if batches.corpus.vocab_size > cfg.vocab_size:
+            raise ParamError("corpus vocabulary larger than the model's")
+        self.dc = device_corpus(batches, evaluator.device)
+        self.order = self.dc.order(batches)
+        self.opt = ext.AdamWCfg(adamw_cfg.beta1, adamw_cfg.beta2, adamw_cfg.eps, adamw_cfg.weight_decay,
+                                adamw_cfg.clip_norm)
+
+    def begin(self, params, task: TrainTask):
+        import torch
+        if task.local_steps < 1:
+            raise ParamError(f"local_steps must be >= 1, got {task.local_steps}")
+        if task.batch_size != self.batches.batch_size:
+            raise ParamError(f"task batch_size {task.batch_size} != iterator batch_size {self.batches.batch_size}")
+        ev = self.ev
+        self.task = task
+        self.w0 = params.tensor if isinstance(params, DeviceVector) else ev._upload(params)
+        self.w = self.w0.clone()
+        self.shadow, self.grad, self.m1, self.m2 = ev.buffers()
+        self.m1.zero_()
+        self.m2.zero_()
+        self.st = ext.stream_handle()
+        ext.call("fb_cast_bf16", self.w.data_ptr(), self.shadow.data_ptr(), self.w.numel(), self.st)
+        B, T = task.batch_size, self.T
+        self.ws = ev.workspace(B, T, extra=B * T * 4 + 512)
+        rb = getattr(ev, "_round_bufs", None)
+        if rb is None:
+            rb = ev._round_bufs = RoundBuffers(ev)
+        self.rb = rb
+        self.row_loss = rb.rows(task.micro_batches * B * T, ev.device)
+        self.tele = torch.zeros(task.local_steps * N_TELE, dtype=torch.float64, device=ev.device)
+        self.lrs = []
+        self.batches.seek(task.schedule_offset * task.micro_batches * B)
+        return self
+
+    def step(self, s: int) -> None:
+        task, B = self.task, self.task.batch_size
+        lr = lr_at(self.sched, task.schedule_offset + s)
+        self.lrs.append(lr)
+        t = s + 1
+        desc = ext.DataDesc(self.dc.tokens.data_ptr(), self.order.data_ptr(), self.order.numel(), self.T, B,
+                            task.micro_batches, 0, self.batches.cursor)
+        ext.call("fb_train_step", C.byref(self.ev._mcfg), self.w.data_ptr(), self.shadow.data_ptr(),
+                 self.grad.data_ptr(), self.m1.data_ptr(), self.m2.data_ptr(), C.byref(desc), self.opt, lr,
+                 1.0 - self.adamw_cfg.beta1 ** t, 1.0 - self.adamw_cfg.beta2 ** t,
+                 self.tele[(s % self.task.local_steps) * N_TELE:].data_ptr(), self.rb.scratch.data_ptr(),
+                 self.row_loss.data_ptr(), self.ws.data_ptr(), self.ws.numel(), self.st)
+        self.batches.cursor += task.micro_batches * B
+
+    def finish(self):
+        task = self.task
+        S = len(self.lrs)
+        tv = self.tele.view(-1, N_TELE)[:S].cpu().numpy()  # the round's single device->host copy
+        telemetry = []
+        for s in range(S):
+            loss = float(tv[s, 0])
+            if not math.isfinite(loss):
+                raise RoundFailedError(task.client_id, f"non-finite loss in round {task.round}")
+            if tv[s, 5] >= 0:
+                raise ParamError("non-finite parameters after AdamW step")
+            telemetry.append(StepTelemetry(task.schedule_offset + s, loss, math.sqrt(tv[s, 1]),
+                                           math.sqrt(tv[s, 2]), self.lrs[s], math.sqrt(tv[s, 3])))
+        update = DeviceClientUpdate(
+            client_id=task.client_id, round=task.round, n_k=self.batches.shard.n_k, w_end=self.w, w_start=self.w0,
+            local_metrics={"mean_loss": float(np.mean([x.loss for x in telemetry])),
+                           "final_loss": telemetry[-1].loss, "final_param_norm": telemetry[-1].param_norm})
+        return update, telemetry
+
+
+def train_round(params, batches: BatchIterator, evaluator: LossEvaluator, adamw_cfg: AdamWConfig,
+                sched: ScheduleConfig, task: TrainTask, *, step_hook=None):
+    """Run one client round on the GPU; returns (update, per-step telemetry).
+
+    `params` may be a host ParamVector (uploaded once) or a DeviceVector (fast path:
+    no host copy). The returned update keeps the trained weights in HBM
+    (DeviceClientUpdate); its f64 `delta` is materialised lazily on access."""
+    if task.local_steps < 1:
+        raise ParamError(f"local_steps must be >= 1, got {task.local_steps}")
+    sess = ClientSession(evaluator, batches, adamw_cfg, sched).begin(params, task)
+    for s in range(task.local_steps):
+        if step_hook is not None:
+            step_hook(s)
+        sess.step(s)
+    return sess.finish()

@@ -43,7 +43,7 @@ def test_fedagg_bitwise_vs_reference(fb, tag, mode):
         bad = torch.zeros(1, dtype=torch.int64, device=dev)
         fb.call("fb_fedagg_step_f32", _ptr_array(ks), nks, len(order), int(mode == "det"), W.data_ptr(),
                 M.data_ptr(), Wo.data_ptr(), Mo.data_ptr(), W.numel(), eta, mu, int(nes), stats.data_ptr(),
-                bad.data_ptr(), fb.stream_handle())
+                bad.data_ptr(), None, fb.stream_handle())
         torch.cuda.synchronize()
         key = f"{tag}_{mode}_{eta}_{mu}_{int(nes)}"
         assert np.array_equal(Wo.cpu().numpy().view(np.uint32), g[key + "_w"].view(np.uint32))
@@ -61,7 +61,7 @@ def test_fedagg_f64delta_and_nonfinite(fb):
     Wo, Mo = torch.empty_like(W), torch.empty_like(M)
     bad = torch.zeros(1, dtype=torch.int64, device=dev)
     fb.call("fb_fedagg_step_f64delta", _ptr_array([d]), (C.c_int64 * 1)(5), 1, 1, W.data_ptr(), M.data_ptr(),
-            Wo.data_ptr(), Mo.data_ptr(), 3, 1.0, 0.0, 1, None, bad.data_ptr(), fb.stream_handle())
+            Wo.data_ptr(), Mo.data_ptr(), 3, 1.0, 0.0, 1, None, bad.data_ptr(), None, fb.stream_handle())
     torch.cuda.synchronize()
     assert bad.item() == 0
     assert Wo[1].item() == 0.5 and Wo[2].item() == 1.75

@@ -1,0 +1,151 @@
+"""GPU parity of attention / LayerNorm / embedding / cross-entropy kernels
+against a torch fp32 reference of the same op on the same (bf16) inputs."""
+import math
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fb():
+    from paper_2405_10853_b200 import ext
+    ext.lib()
+    return ext
+
+
+def alibi_ref(H, T, use_alibi, dev):
+    slopes = torch.tensor([2.0 ** (-8.0 * (h + 1) / H) for h in range(H)], dtype=torch.float64)
+    i = torch.arange(T)[:, None]
+    j = torch.arange(T)[None, :]
+    b = -slopes[:, None, None] * (i - j)[None].double() if use_alibi else torch.zeros(H, T, T, dtype=torch.float64)
+    b = b.float()
+    b[:, j.expand(T, T) > i.expand(T, T)] = -math.inf
+    return b.to(dev)
+
+
+def attn_ref(qkv, B, T, H, dh, use_alibi):
+    d = H * dh
+    x = qkv.float().view(B, T, 3, H, dh)
+    q, k, v = x[:, :, 0].transpose(1, 2), x[:, :, 1].transpose(1, 2), x[:, :, 2].transpose(1, 2)
+    s = (q @ k.transpose(-1, -2)) / math.sqrt(dh) + alibi_ref(H, T, use_alibi, qkv.device)
+    lse = torch.logsumexp(s, dim=-1)
+    o = (torch.softmax(s, -1) @ v).transpose(1, 2).reshape(B * T, d)
+    return o, lse
+
+
+@pytest.mark.parametrize("B,T,H,dh,alibi", [(2, 128, 2, 64, 1), (1, 256, 3, 64, 1), (2, 64, 2, 128, 1),
+                                             (1, 512, 4, 128, 1), (2, 128, 2, 64, 0), (1, 1024, 12, 64, 1)])
+def test_attention_fwd_bwd(fb, B, T, H, dh, alibi):
+    torch.manual_seed(0)
+    dev = torch.device("cuda")
+    d = H * dh
+    qkv = torch.randn(B * T, 3 * d, device=dev).to(torch.bfloat16)
+    o = torch.empty(B * T, d, dtype=torch.bfloat16, device=dev)
+    lse2 = torch.empty(B * H * T, dtype=torch.float32, device=dev)
+    fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), B, T, H, dh, alibi, fb.stream_handle())
+    q32 = qkv.float().requires_grad_()
+    o_ref, lse_ref = attn_ref(q32, B, T, H, dh, alibi)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(o.float(), o_ref, atol=2e-2, rtol=2e-2)
+    torch.testing.assert_close(lse2.view(B, H, T) * math.log(2.0), lse_ref, atol=1e-3, rtol=1e-3)
+    do = torch.randn(B * T, d, device=dev).to(torch.bfloat16)
+    o_ref.backward(do.float())
+    dqkv = torch.empty_like(qkv)
+    work = torch.empty(B * H * T + B * T * d, dtype=torch.float32, device=dev)
+    fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse2.data_ptr(), dqkv.data_ptr(),
+            work.data_ptr(), B, T, H, dh, alibi, fb.stream_handle())
+    torch.cuda.synchronize()
+    g = q32.grad
+    for sl, name in [(slice(0, d), "dq"), (slice(d, 2 * d), "dk"), (slice(2 * d, 3 * d), "dv")]:
+        ref = g[:, sl]
+        got = dqkv[:, sl].float()
+        err = (got - ref).abs().max().item()
+        scale = ref.abs().max().item()
+        assert err <= 3e-2 * scale + 1e-2, (name, err, scale)
+
+
+@pytest.mark.parametrize("rows,d", [(256, 512), (100, 768), (64, 2048), (33, 128)])
+def test_layernorm(fb, rows, d):
+    torch.manual_seed(1)
+    dev = torch.device("cuda")
+    x = torch.randn(rows, d, device=dev) * 2 + 0.5
+    gamma = torch.randn(d, device=dev)
+    beta = torch.randn(d, device=dev)
+    y = torch.empty(rows, d, dtype=torch.bfloat16, device=dev)
+    mean = torch.empty(rows, device=dev)
+    rstd = torch.empty(rows, device=dev)
+    fb.call("fb_ln_fwd", x.data_ptr(), gamma.data_ptr(), beta.data_ptr(), y.data_ptr(), mean.data_ptr(),
+            rstd.data_ptr(), rows, d, fb.stream_handle())
+    xr = x.clone().requires_grad_()
+    gr = gamma.clone().requires_grad_()
+    br = beta.clone().requires_grad_()
+    ref = F.layer_norm(xr, (d,), gr, br, 1e-5)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(y.float(), ref, atol=3e-2, rtol=1e-2)
+    dy = torch.randn(rows, d, device=dev)
+    dres = torch.randn(rows, d, device=dev)
+    ref.backward(dy)
+    dx = torch.empty_like(x)
+    dxb = torch.empty(rows, d, dtype=torch.bfloat16, device=dev)
+    dg = torch.zeros(d, device=dev)
+    db = torch.ones(d, device=dev)  # accumulates
+    work = torch.empty(2 * 296 * d, device=dev)
+    fb.call("fb_ln_bwd", x.data_ptr(), gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dy.data_ptr(),
+            dres.data_ptr(), dx.data_ptr(), dxb.data_ptr(), dg.data_ptr(), db.data_ptr(), work.data_ptr(), rows, d,
+            fb.stream_handle())
+    torch.cuda.synchronize()
+    torch.testing.assert_close(dx, xr.grad + dres, atol=1e-4, rtol=1e-4)
+    torch.testing.assert_close(dxb.float(), dx, atol=2e-2, rtol=1e-2)
+    torch.testing.assert_close(dg, gr.grad, atol=1e-3, rtol=1e-4)
+    torch.testing.assert_close(db, br.grad + 1, atol=1e-3, rtol=1e-4)
+
+
+def test_embedding(fb):
+    torch.manual_seed(2)
+    dev = torch.device("cuda")
+    V, d, B, T = 300, 256, 4, 64
+    emb = torch.randn(V, d, device=dev)
+    pos = torch.randn(T, d, device=dev)
+    tok = torch.randint(0, V, (B * T,), device=dev, dtype=torch.int32)
+    x = torch.empty(B * T, d, device=dev)
+    for p in (None, pos):
+        fb.call("fb_embed_fwd", tok.data_ptr(), emb.data_ptr(), fb.ptr(p), x.data_ptr(), B * T, T, d, fb.stream_handle())
+        ref = emb[tok.long()] + (pos.repeat(B, 1) if p is not None else 0)
+        torch.cuda.synchronize()
+        assert torch.equal(x, ref)
+    dx = torch.randn(B * T, d, device=dev)
+    ge = torch.zeros(V, d, device=dev)
+    gp = torch.zeros(T, d, device=dev)
+    fb.call("fb_embed_bwd", tok.data_ptr(), dx.data_ptr(), ge.data_ptr(), gp.data_ptr(), B * T, T, d, V,
+            fb.stream_handle())
+    ref = torch.zeros(V, d, device=dev).index_add_(0, tok.long(), dx)
+    torch.cuda.synchronize()
+    torch.testing.assert_close(ge, ref, atol=1e-4, rtol=1e-5)
+    torch.testing.assert_close(gp, dx.view(B, T, d).sum(0), atol=1e-4, rtol=1e-5)
+
+
+@pytest.mark.parametrize("V", [256, 32000])
+def test_cross_entropy(fb, V):
+    torch.manual_seed(3)
+    dev = torch.device("cuda")
+    B, T = 3, 64
+    logits = torch.randn(B * T, V, device=dev) * 3
+    tok = torch.randint(0, V, (B * T,), device=dev, dtype=torch.int32)
+    scale = 1.0 / (B * (T - 1))
+    dl = torch.empty(B * T, V, dtype=torch.bfloat16, device=dev)
+    row_loss = torch.empty(B * T, dtype=torch.float64, device=dev)
+    # two chunks to exercise row0
+    h = (B * T) // 2
+    for r0, n in [(0, h), (h, B * T - h)]:
+        fb.call("fb_ce_fwd_bwd", logits[r0:].data_ptr(), tok.data_ptr(), dl[r0:].data_ptr(), r0, n, T, V, scale,
+                row_loss.data_ptr(), fb.stream_handle())
+    lg = logits.clone().view(B, T, V).requires_grad_()
+    ref = F.cross_entropy(lg[:, :-1].reshape(-1, V), tok.view(B, T)[:, 1:].reshape(-1).long())
+    ref.backward()
+    torch.cuda.synchronize()
+    assert row_loss.sum().item() * scale == pytest.approx(ref.item(), rel=1e-5)
+    torch.testing.assert_close(dl.float(), lg.grad.view(B * T, V), atol=1e-6, rtol=1e-2)
