@@ -110,7 +110,8 @@ int fb_embed_bwd(const int32_t* d_tok, const float* d_dx, float* d_gemb, float* 
 /* LayerNorm eps 1e-5 (model.py:81,84,113): y(bf16) = LN(x), saves mean/rstd */
 int fb_ln_fwd(const float* d_x, const float* d_gamma, const float* d_beta, void* d_y_bf16,
               float* d_mean, float* d_rstd, int rows, int d, void* stream);
-/* dx(f32) = dres(f32, optional) + LN'(dy); optional bf16 copy of dx; dgamma/dbeta += */
+/* dx(f32) = dres(f32, optional) + LN'(dy); optional bf16 copy of dx; dgamma/dbeta +=.
+ * d_work: 2 * 592 * d floats of scratch (per-CTA dgamma/dbeta partials) */
 int fb_ln_bwd(const float* d_x, const float* d_gamma, const float* d_mean, const float* d_rstd,
               const float* d_dy, const float* d_dres, float* d_dx, void* d_dx_bf16,
               float* d_dgamma, float* d_dbeta, float* d_work, int rows, int d, void* stream);

@@ -26,8 +26,8 @@ struct AggParams {
   double nk[FB_MAX_CLIENTS];
 };
 
-constexpr int kStack = 7;  // 2^7 > FB_MAX_CLIENTS
-
+// binary-counter stack of partial sums; D = floor(log2(K)) + 1 levels suffice
+template <int kStack>
 struct TreeAcc {
   double slot[kStack];
   __device__ __forceinline__ void push(double t, int k) {
@@ -92,7 +92,7 @@ __device__ __forceinline__ StepOut outer_step(float w32, float m32, double pg, d
   return o;
 }
 
-template <typename TIn, int VEC>
+template <typename TIn, int VEC, int D>
 __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, int deterministic,
                                                      double inv_total_unused, double total,
                                                      const float* __restrict__ w,
@@ -114,31 +114,67 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
       float4 a = ld_stream_f4(w + j0), b = ld_stream_f4(m + j0);
       wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w;
       mv[0] = b.x; mv[1] = b.y; mv[2] = b.z; mv[3] = b.w;
+    } else if constexpr (VEC == 2) {
+      float2 a = __ldg(reinterpret_cast<const float2*>(w + j0)), b = __ldg(reinterpret_cast<const float2*>(m + j0));
+      wv[0] = a.x; wv[1] = a.y;
+      mv[0] = b.x; mv[1] = b.y;
     } else {
 #pragma unroll
       for (int e = 0; e < VEC; ++e) { wv[e] = w[j0 + e]; mv[e] = m[j0 + e]; }
     }
     double pg[VEC];
-    if (K == 1) {
+    if constexpr (VEC >= 2 && sizeof(TIn) == 4) {
+      // all client loads of a batch are issued before any f64 math (8 vector loads in flight)
+      constexpr int KB = 8;
+      TreeAcc<D> acc[VEC];
+      double sum[VEC];
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) sum[e] = 0.0;
+      for (int k0 = 0; k0 < K; k0 += KB) {
+        float c[KB][VEC];
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+          if (k0 + j < K) {
+            const float* src = reinterpret_cast<const float*>(P.src[k0 + j]) + j0;
+            if constexpr (VEC == 4) {
+              float4 t = ld_stream_f4(src);
+              c[j][0] = t.x; c[j][1] = t.y; c[j][2] = t.z; c[j][3] = t.w;
+            } else {
+              float2 t = __ldg(reinterpret_cast<const float2*>(src));
+              c[j][0] = t.x; c[j][1] = t.y;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < KB; ++j) {
+          if (k0 + j < K) {
+            const int k = k0 + j;
+            const float* cv = c[j];
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              const double dk = __dsub_rn((double)wv[e], (double)cv[e]);
+              if (K == 1) {
+                sum[e] = dk;
+              } else if (deterministic) {
+                acc[e].push(__dmul_rn(P.nk[k], dk), k);
+              } else {
+                sum[e] = __dadd_rn(sum[e], __dmul_rn(P.nk[k], dk));
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < VEC; ++e)
+        pg[e] = (K == 1) ? sum[e] : __ddiv_rn(deterministic ? acc[e].result(K) : sum[e], total);
+    } else if (K == 1) {
 #pragma unroll
       for (int e = 0; e < VEC; ++e) pg[e] = delta_of<TIn>(P.src[0], j0 + e, (double)wv[e]);
     } else if (deterministic) {
-      TreeAcc acc[VEC];
+      TreeAcc<D> acc[VEC];
       for (int k = 0; k < K; ++k) {
-        const TIn* src = P.src[k];
-        double dk[VEC];
-        if constexpr (VEC == 4 && sizeof(TIn) == 4) {
-          float4 c = ld_stream_f4(reinterpret_cast<const float*>(src) + j0);
-          dk[0] = __dsub_rn((double)wv[0], (double)c.x);
-          dk[1] = __dsub_rn((double)wv[1], (double)c.y);
-          dk[2] = __dsub_rn((double)wv[2], (double)c.z);
-          dk[3] = __dsub_rn((double)wv[3], (double)c.w);
-        } else {
 #pragma unroll
-          for (int e = 0; e < VEC; ++e) dk[e] = delta_of<TIn>(src, j0 + e, (double)wv[e]);
-        }
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) acc[e].push(__dmul_rn(P.nk[k], dk[e]), k);
+        for (int e = 0; e < VEC; ++e) acc[e].push(__dmul_rn(P.nk[k], delta_of<TIn>(P.src[k], j0 + e, (double)wv[e])), k);
       }
 #pragma unroll
       for (int e = 0; e < VEC; ++e) pg[e] = __ddiv_rn(acc[e].result(K), total);
@@ -147,18 +183,9 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
 #pragma unroll
       for (int e = 0; e < VEC; ++e) sum[e] = 0.0;
       for (int k = 0; k < K; ++k) {
-        const TIn* src = P.src[k];
-        if constexpr (VEC == 4 && sizeof(TIn) == 4) {
-          float4 c = ld_stream_f4(reinterpret_cast<const float*>(src) + j0);
-          float cv[4] = {c.x, c.y, c.z, c.w};
 #pragma unroll
-          for (int e = 0; e < VEC; ++e)
-            sum[e] = __dadd_rn(sum[e], __dmul_rn(P.nk[k], __dsub_rn((double)wv[e], (double)cv[e])));
-        } else {
-#pragma unroll
-          for (int e = 0; e < VEC; ++e)
-            sum[e] = __dadd_rn(sum[e], __dmul_rn(P.nk[k], delta_of<TIn>(src, j0 + e, (double)wv[e])));
-        }
+        for (int e = 0; e < VEC; ++e)
+          sum[e] = __dadd_rn(sum[e], __dmul_rn(P.nk[k], delta_of<TIn>(P.src[k], j0 + e, (double)wv[e])));
       }
 #pragma unroll
       for (int e = 0; e < VEC; ++e) pg[e] = __ddiv_rn(sum[e], total);
@@ -183,12 +210,15 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
     if constexpr (VEC == 4) {
       st_stream_f4(w_out + j0, make_float4(wo[0], wo[1], wo[2], wo[3]));
       st_stream_f4(m_out + j0, make_float4(mo[0], mo[1], mo[2], mo[3]));
+    } else if constexpr (VEC == 2) {
+      *reinterpret_cast<float2*>(w_out + j0) = make_float2(wo[0], wo[1]);
+      *reinterpret_cast<float2*>(m_out + j0) = make_float2(mo[0], mo[1]);
     } else {
 #pragma unroll
       for (int e = 0; e < VEC; ++e) { w_out[j0 + e] = wo[e]; m_out[j0 + e] = mo[e]; }
     }
   }
-  // scalar tail (only when VEC == 4 and n % 4 != 0)
+  // scalar tail (only when VEC > 1 and n % VEC != 0)
   if (VEC > 1 && blockIdx.x == 0 && threadIdx.x < (n % VEC)) {
     int64_t j = nvec * VEC + threadIdx.x;
     double wg = (double)w[j];
@@ -196,7 +226,7 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
     if (K == 1) {
       pgv = delta_of<TIn>(P.src[0], j, wg);
     } else if (deterministic) {
-      TreeAcc acc;
+      TreeAcc<D> acc;
       for (int k = 0; k < K; ++k) acc.push(__dmul_rn(P.nk[k], delta_of<TIn>(P.src[k], j, wg)), k);
       pgv = __ddiv_rn(acc.result(K), total);
     } else {
@@ -266,19 +296,26 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
   if (stats) FB_CUDA_TRY(cudaMemsetAsync(stats, 0, 3 * sizeof(double), st));
   if (first_bad) FB_CUDA_TRY(cudaMemsetAsync(first_bad, 0x7f, sizeof(int64_t), st));
   const int threads = 256;
+  const int depth = K <= 1 ? 1 : K <= 3 ? 2 : K <= 7 ? 3 : K <= 15 ? 4 : K <= 31 ? 5 : K <= 63 ? 6 : 7;
+#define FB_AGG_LAUNCH(VEC_, D_)                                                                          \
+  do {                                                                                                   \
+    int64_t work = (n / VEC_ + threads - 1) / threads;                                                   \
+    int blocks = (int)(work < kNumSMs * 8 ? (work > 0 ? work : 1) : kNumSMs * 8);                        \
+    fedagg_kernel<TIn, VEC_, D_><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, \
+                                                             m_out, n, eta, mu, nesterov, stats,         \
+                                                             (unsigned long long*)first_bad, pg_out);    \
+  } while (0)
   if (aligned && sizeof(TIn) == 4) {
-    int64_t work = (n / 4 + threads - 1) / threads;
-    int blocks = (int)(work < kNumSMs * 8 ? (work > 0 ? work : 1) : kNumSMs * 8);
-    fedagg_kernel<TIn, 4><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, m_out, n,
-                                                      eta, mu, nesterov, stats,
-                                                      (unsigned long long*)first_bad, pg_out);
+    switch (depth) {
+      case 1: case 2: case 3: FB_AGG_LAUNCH(4, 3); break;
+      case 4: FB_AGG_LAUNCH(4, 4); break;
+      case 5: FB_AGG_LAUNCH(2, 5); break;
+      default: FB_AGG_LAUNCH(2, 7); break;
+    }
   } else {
-    int64_t work = (n + threads - 1) / threads;
-    int blocks = (int)(work < kNumSMs * 8 ? (work > 0 ? work : 1) : kNumSMs * 8);
-    fedagg_kernel<TIn, 1><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, m_out, n,
-                                                      eta, mu, nesterov, stats,
-                                                      (unsigned long long*)first_bad, pg_out);
+    FB_AGG_LAUNCH(1, 7);
   }
+#undef FB_AGG_LAUNCH
   FB_LAUNCH_CHECK();
   return FB_OK;
 }

@@ -107,7 +107,7 @@ static WS carve(const fb_model_cfg& c, int B, int T, Arena& A) {
   w.dqkv = A.take<__nv_bfloat16>(M * 3 * d);
   w.dfc = A.take<__nv_bfloat16>(M * 4 * d);
   w.attn_work = A.take<float>(B * H * T + M * d);
-  w.ln_work = A.take<float>(2 * 296 * d);
+  w.ln_work = A.take<float>(2 * 592 * d);
   return w;
 }
 

@@ -85,89 +85,136 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
 }
 
 // dx = dres + rstd * (g - mean(g) - xhat * mean(g * xhat)),  g = dy * gamma
-// partial dgamma/dbeta per CTA -> work[blockIdx][2][d]
-template <int NJ>
+// One 256-thread CTA walks rows; thread t owns VPT consecutive columns, so the
+// per-column dgamma/dbeta partials stay in a few registers across rows.
+// Partials per CTA -> work[blockIdx][2][d], reduced in fixed order afterwards.
+template <int VPT>
 __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
                                                      const float* __restrict__ mean_in, const float* __restrict__ rstd_in,
                                                      const float* __restrict__ dy, const float* __restrict__ dres,
                                                      float* __restrict__ dx, __nv_bfloat16* __restrict__ dx_bf16,
                                                      float* __restrict__ work, int rows, int d) {
-  extern __shared__ float sh_part[];  // [8 warps][2][d]
-  const int wid = threadIdx.x >> 5;
-  const int lane = threadIdx.x & 31;
-  float pg[NJ], pb[NJ];
+  __shared__ float red[2][8];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int c0 = tid * VPT;
+  const bool vec = (VPT % 4 == 0) && (d % 4 == 0);
+  const float inv_d = 1.0f / d;
+  float gm[VPT], pg[VPT], pb[VPT];
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) { pg[j] = 0.f; pb[j] = 0.f; }
-  for (int row = blockIdx.x * 8 + wid; row < rows; row += gridDim.x * 8) {
-    const float* xr = x + (int64_t)row * d;
-    const float* dyr = dy + (int64_t)row * d;
+  for (int j = 0; j < VPT; ++j) {
+    gm[j] = c0 + j < d ? gamma[c0 + j] : 0.f;
+    pg[j] = 0.f;
+    pb[j] = 0.f;
+  }
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t base = (int64_t)row * d + c0;
+    float xv[VPT], gv[VPT];
+    if (vec && c0 < d) {
+#pragma unroll
+      for (int j = 0; j < VPT; j += 4) {
+        float4 a = *reinterpret_cast<const float4*>(x + base + j);
+        float4 b = *reinterpret_cast<const float4*>(dy + base + j);
+        xv[j] = a.x; xv[j + 1] = a.y; xv[j + 2] = a.z; xv[j + 3] = a.w;
+        gv[j] = b.x; gv[j + 1] = b.y; gv[j + 2] = b.z; gv[j + 3] = b.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        xv[j] = c0 + j < d ? x[base + j] : 0.f;
+        gv[j] = c0 + j < d ? dy[base + j] : 0.f;
+      }
+    }
     const float mu = mean_in[row], rs = rstd_in[row];
-    float xh[NJ], g[NJ];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      const int c = lane + 32 * j;
-      if (c < d) {
-        xh[j] = (xr[c] - mu) * rs;
-        const float dyv = dyr[c];
-        g[j] = dyv * gamma[c];
-        pg[j] += dyv * xh[j];
-        pb[j] += dyv;
-      } else {
-        xh[j] = 0.f;
-        g[j] = 0.f;
-      }
-      s1 += g[j];
-      s2 += g[j] * xh[j];
+    for (int j = 0; j < VPT; ++j) {
+      const float xh = (xv[j] - mu) * rs;
+      pg[j] += gv[j] * xh;
+      pb[j] += gv[j];
+      const float g = gv[j] * gm[j];
+      xv[j] = xh;
+      gv[j] = g;
+      s1 += g;
+      s2 += g * xh;
     }
-    s1 = warp_sum(s1) / d;
-    s2 = warp_sum(s2) / d;
-    float* dxr = dx + (int64_t)row * d;
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) { red[0][wid] = s1; red[1][wid] = s2; }
+    __syncthreads();
+    s1 = 0.f;
+    s2 = 0.f;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      const int c = lane + 32 * j;
-      if (c < d) {
-        float v = rs * (g[j] - s1 - xh[j] * s2);
-        if (dres) v += dres[(int64_t)row * d + c];
-        dxr[c] = v;
-        if (dx_bf16) dx_bf16[(int64_t)row * d + c] = __float2bfloat16_rn(v);
+    for (int i = 0; i < 8; ++i) { s1 += red[0][i]; s2 += red[1][i]; }
+    __syncthreads();
+    s1 *= inv_d;
+    s2 *= inv_d;
+    float o[VPT];
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) o[j] = rs * (gv[j] - s1 - xv[j] * s2);
+    if (vec && c0 < d) {
+#pragma unroll
+      for (int j = 0; j < VPT; j += 4) {
+        float4 v = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
+        if (dres) {
+          float4 r = *reinterpret_cast<const float4*>(dres + base + j);
+          v.x += r.x; v.y += r.y; v.z += r.z; v.w += r.w;
+        }
+        *reinterpret_cast<float4*>(dx + base + j) = v;
+        if (dx_bf16) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(dx_bf16 + base + j) = pk;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < VPT; ++j) {
+        if (c0 + j < d) {
+          float v = o[j] + (dres ? dres[base + j] : 0.f);
+          dx[base + j] = v;
+          if (dx_bf16) dx_bf16[base + j] = __float2bfloat16_rn(v);
+        }
       }
     }
   }
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const int c = lane + 32 * j;
-    if (c < d) {
-      sh_part[(wid * 2 + 0) * d + c] = pg[j];
-      sh_part[(wid * 2 + 1) * d + c] = pb[j];
+  for (int j = 0; j < VPT; ++j) {
+    if (c0 + j < d) {
+      work[((int64_t)blockIdx.x * 2 + 0) * d + c0 + j] = pg[j];
+      work[((int64_t)blockIdx.x * 2 + 1) * d + c0 + j] = pb[j];
     }
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    float a = 0.f, b = 0.f;
-    for (int w = 0; w < 8; ++w) {
-      a += sh_part[(w * 2 + 0) * d + c];
-      b += sh_part[(w * 2 + 1) * d + c];
-    }
-    work[((int64_t)blockIdx.x * 2 + 0) * d + c] = a;
-    work[((int64_t)blockIdx.x * 2 + 1) * d + c] = b;
   }
 }
 
-__global__ void ln_bwd_reduce_kernel(const float* __restrict__ work, int nparts, int d, float* __restrict__ dgamma,
-                                     float* __restrict__ dbeta) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= d) return;
+// 32 columns per CTA; warp w sums partials w, w+8, ... (fixed order), then the 8 warp
+// sums are combined in fixed order: deterministic and 64x more parallel than a column loop.
+__global__ void __launch_bounds__(256) ln_bwd_reduce_kernel(const float* __restrict__ work, int nparts, int d,
+                                                            float* __restrict__ dgamma, float* __restrict__ dbeta) {
+  __shared__ float sg[8][32], sb[8][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int c = blockIdx.x * 32 + lane;
   float a = 0.f, b = 0.f;
-  for (int p = 0; p < nparts; ++p) {
-    a += work[((int64_t)p * 2 + 0) * d + c];
-    b += work[((int64_t)p * 2 + 1) * d + c];
+  if (c < d) {
+    for (int p = w; p < nparts; p += 8) {
+      a += work[((int64_t)p * 2 + 0) * d + c];
+      b += work[((int64_t)p * 2 + 1) * d + c];
+    }
   }
-  dgamma[c] += a;
-  dbeta[c] += b;
+  sg[w][lane] = a;
+  sb[w][lane] = b;
+  __syncthreads();
+  if (w == 0 && c < d) {
+    float ta = 0.f, tb = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) { ta += sg[i][lane]; tb += sb[i][lane]; }
+    dgamma[c] += ta;
+    dbeta[c] += tb;
+  }
 }
 
-constexpr int kLnBwdBlocks = 296;
+constexpr int kLnBwdBlocks = 592;  // 148 SMs x 4
 
 // ------------------------------------------------------------------ cross-entropy
 // One CTA (256 threads) per logits row. Row r of the chunk is position t = (row0+r) % T.
@@ -260,28 +307,19 @@ extern "C" int fb_ln_bwd(const float* d_x, const float* d_gamma, const float* d_
                          float* d_dbeta, float* d_work, int rows, int d, void* stream) {
   FB_REQUIRE(rows > 0 && d > 0 && d <= 4096, "ln_bwd: bad shape rows=%d d=%d", rows, d);
   FB_REQUIRE(d_work != nullptr, "ln_bwd: needs a work buffer of %d floats", 2 * kLnBwdBlocks * d);
-  const int nj = (d + 31) / 32;
+  const int vpt = (d + 255) / 256;
   cudaStream_t st = (cudaStream_t)stream;
-  const int grid = std::min((rows + 7) / 8, kLnBwdBlocks);
-  const size_t shm = (size_t)16 * d * sizeof(float);
-#define CALL_B(N)                                                                                       \
-  do {                                                                                                  \
-    auto k = ln_bwd_kernel<N>;                                                                          \
-    if (shm > 48 * 1024) FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm)); \
-    k<<<grid, 256, shm, st>>>(d_x, d_gamma, d_mean, d_rstd, d_dy, d_dres, d_dx, (__nv_bfloat16*)d_dx_bf16, d_work, rows, d); \
-  } while (0)
-  if (nj <= 1) CALL_B(1);
-  else if (nj <= 2) CALL_B(2);
-  else if (nj <= 4) CALL_B(4);
-  else if (nj <= 8) CALL_B(8);
-  else if (nj <= 16) CALL_B(16);
-  else if (nj <= 24) CALL_B(24);
-  else if (nj <= 32) CALL_B(32);
-  else if (nj <= 64) CALL_B(64);
-  else CALL_B(128);
+  const int grid = std::min(rows, kLnBwdBlocks);
+#define CALL_B(N) ln_bwd_kernel<N><<<grid, 256, 0, st>>>(d_x, d_gamma, d_mean, d_rstd, d_dy, d_dres, d_dx, (__nv_bfloat16*)d_dx_bf16, d_work, rows, d)
+  if (vpt <= 1) CALL_B(1);
+  else if (vpt <= 2) CALL_B(2);
+  else if (vpt <= 3) CALL_B(3);
+  else if (vpt <= 4) CALL_B(4);
+  else if (vpt <= 8) CALL_B(8);
+  else CALL_B(16);
 #undef CALL_B
   FB_LAUNCH_CHECK();
-  ln_bwd_reduce_kernel<<<(d + 255) / 256, 256, 0, st>>>(d_work, grid, d, d_dgamma, d_dbeta);
+  ln_bwd_reduce_kernel<<<(d + 31) / 32, 256, 0, st>>>(d_work, grid, d, d_dgamma, d_dbeta);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }

@@ -93,7 +93,7 @@ def test_layernorm(fb, rows, d):
     dxb = torch.empty(rows, d, dtype=torch.bfloat16, device=dev)
     dg = torch.zeros(d, device=dev)
     db = torch.ones(d, device=dev)  # accumulates
-    work = torch.empty(2 * 296 * d, device=dev)
+    work = torch.empty(2 * 592 * d, device=dev)
     fb.call("fb_ln_bwd", x.data_ptr(), gamma.data_ptr(), mean.data_ptr(), rstd.data_ptr(), dy.data_ptr(),
             dres.data_ptr(), dx.data_ptr(), dxb.data_ptr(), dg.data_ptr(), db.data_ptr(), work.data_ptr(), rows, d,
             fb.stream_handle())
