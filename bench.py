@@ -358,25 +358,33 @@ def run_e2e(c, cfg, corpus, split, client, world, rank, K, barrier):
 
 # ------------------------------------------------------------------------------ CPU baseline
 def cpu_baseline(c, budget_s=20.0, sample_tokens=None):
-    """The reference's CPU path (oracle port, torch CPU fp32 + numpy f64) on a bounded
-    sample at the workload's exact shapes, extrapolated linearly to one local step:
-    fwd/bwd per token x tokens/step + (micro-accumulate + clip + AdamW + l2) per param x N."""
+    """The reference's CPU path (oracle port: torch-CPU fp32 fwd/bwd + numpy f64
+    optimizer, all host cores) on a bounded sample at the workload's exact shapes,
+    extrapolated linearly to one local step:
+      fwd/bwd: a 1-layer and a 2-layer model at the exact width/vocab/context on
+      1 x `tokens` tokens -> per-layer and embedding/head cost -> L layers, per token;
+      optimizer: micro-accumulate / clip / AdamW / l2 on a 4M-param slice, per param."""
     import torch
     from oracle import localopt_ref, model_ref
     cores = os.cpu_count() or 1
     torch.set_num_threads(cores)
     V, d, L, H, T = c["V"], c["d"], c["L"], c["H"], c["T"]
-    tokens = sample_tokens or (128 if c["d"] >= 2048 else 512)
-    tokens = min(tokens, T)
+    tokens = min(sample_tokens or 128, T)
     rng = np.random.default_rng(0)
-    N = n_params(c)
-    w = np.asarray(rng.normal(0, 0.02, N), dtype=np.float32)
     batch = rng.integers(33, 97, size=(1, tokens))
-    t0 = time.perf_counter()
-    model_ref.loss_and_grad(w, batch, V, T, L, d, H)
-    t_fb = time.perf_counter() - t0
-    del w
-    # optimizer pieces on a slice, extrapolated in N
+    times = {}
+    for nl in (1, 2):
+        n = V * d + nl * (12 * d * d + 4 * d) + 2 * d + d * V
+        w = np.asarray(rng.normal(0, 0.02, n), dtype=np.float32)
+        if nl == 1:
+            model_ref.loss_and_grad(w, batch[:, :8], V, T, nl, d, H)  # warm-up: allocator + cached ALiBi buffer
+        t0 = time.perf_counter()
+        model_ref.loss_and_grad(w, batch, V, T, nl, d, H)
+        times[nl] = time.perf_counter() - t0
+        del w
+    per_layer = max(times[2] - times[1], 1e-9)
+    base = max(times[1] - per_layer, 0.0)
+    t_fb = base + L * per_layer
     n_s = 4_000_000
     p = rng.normal(0, 0.02, n_s).astype(np.float32)
     g = rng.normal(0, 1e-3, n_s).astype(np.float32)
@@ -393,12 +401,14 @@ def cpu_baseline(c, budget_s=20.0, sample_tokens=None):
     p2, _, _, _ = localopt_ref.adamw(p, gc, z, z, 1, 1e-4)
     localopt_ref.l2_norm(p2)
     t_opt = time.perf_counter() - t0
+    N = n_params(c)
     tokens_step = c["B"] * c["micro"] * T
     step_s = t_fb / tokens * tokens_step + (c["micro"] * t_acc + t_opt) / n_s * N
     return {"value": round(tokens_step / step_s, 3), "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": f"oracle loss_and_grad on 1x{tokens} tokens at the exact {c['d']}-d/{L}-layer/{V}-vocab shape "
-                      f"({t_fb:.1f}s) + accumulate/clip/AdamW on a {n_s // 10**6}M-param slice ({t_opt:.2f}s), "
-                      f"extrapolated to one local step ({tokens_step} tokens, {N} params)"}
+            "sample": f"oracle loss_and_grad on 1x{tokens} tokens with 1 and 2 layers at the exact d={d}/V={V}/"
+                      f"ctx={T} shape ({times[1]:.1f}s, {times[2]:.1f}s -> {L} layers) + accumulate/clip/AdamW on a "
+                      f"{n_s // 10**6}M-param slice ({t_acc + t_opt:.2f}s), extrapolated to one local step "
+                      f"({tokens_step} tokens, {N} params)"}
 
 
 def run_reference(args, cfgname):

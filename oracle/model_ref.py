@@ -13,6 +13,7 @@ Functional (no nn.Module); autograd supplies the backward.
 """
 from __future__ import annotations
 
+import functools
 import math
 
 import numpy as np
@@ -61,7 +62,9 @@ def slopes(H):
     return np.array([2.0 ** (-8.0 * (h + 1) / H) for h in range(H)])
 
 
+@functools.lru_cache(maxsize=4)
 def attn_bias(H, T, use_alibi=True):
+    """(H, T, T) f32 bias; built once per shape like the reference's registered buffer (model.py:115-121)."""
     i = np.arange(T)[:, None]
     j = np.arange(T)[None, :]
     if use_alibi:

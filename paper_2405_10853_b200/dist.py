@@ -36,7 +36,7 @@ class ShardedAggregator:
     n_k:   {client_id: n_k} for ALL contributing clients (known from the round plan).
     w: the global model (replicated, f32 [N]); m_shard: this rank's momentum slice."""
 
-    def __init__(self, n: int, n_clients: int, group=None):
+    def __init__(self, n: int, n_clients: int, group=None, device=None, kernel=None):
         import torch
         import torch.distributed as dist
         self.dist = dist
@@ -46,7 +46,10 @@ class ShardedAggregator:
         self.n = n
         self.K = n_clients
         self.lo, self.hi, self.per = shard_bounds(n, self.world, self.rank)
-        dev = torch.device("cuda", torch.cuda.current_device())
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        # shard-local aggregation + outer step; the GPU kernel unless a test injects the oracle
+        self.kernel = kernel or fused_kernel
         # receive buffers: one slice per client (padded to `per`); none needed on one GPU
         self.recv = torch.empty(self.K if self.world > 1 else 0, self.per, dtype=torch.float32, device=dev)
         self.src = {}
@@ -83,18 +86,28 @@ class ShardedAggregator:
         import torch
         cnt = self.hi - self.lo
         ids = sorted(n_k) if deterministic else list(n_k)
-        ptrs = (C.c_void_p * len(ids))(*[self.src[k].data_ptr() for k in ids])
-        nks = (C.c_int64 * len(ids))(*[int(n_k[k]) for k in ids])
         w_slice = w[self.lo:self.hi]
         m_new = torch.empty_like(m_shard)
         wo = self.w_full[self.rank * self.per: self.rank * self.per + cnt]
         if cnt > 0:
-            ext.call("fb_fedagg_step_f32", ptrs, nks, len(ids), int(deterministic), w_slice.data_ptr(),
-                     m_shard.data_ptr(), wo.data_ptr(), m_new.data_ptr(), cnt, float(eta), float(mu), int(nesterov),
-                     self.stats.data_ptr(), self.bad.data_ptr(), None, ext.stream_handle())
+            self.kernel([self.src[k][:cnt] for k in ids], [int(n_k[k]) for k in ids], deterministic, w_slice,
+                        m_shard, wo, m_new, eta, mu, nesterov, self)
         if self.world > 1:
-            self.dist.all_gather_into_tensor(self.w_full, self.w_full[self.rank * self.per:(self.rank + 1) * self.per],
-                                             group=self.group)
+            mine = self.w_full[self.rank * self.per:(self.rank + 1) * self.per]
+            if self.dist.get_backend(self.group) == "nccl":
+                self.dist.all_gather_into_tensor(self.w_full, mine, group=self.group)
+            else:
+                parts = list(self.w_full.split(self.per))
+                self.dist.all_gather(parts, mine.clone(), group=self.group)
         out = w_out if w_out is not None else torch.empty_like(w)
         out.copy_(self.w_full[: self.n])
         return out, m_new
+
+
+def fused_kernel(srcs, nks, deterministic, w_slice, m_slice, w_out, m_out, eta, mu, nesterov, agg):
+    """fb_fedagg_step_f32 on one rank's slice (clients already in reduction order)."""
+    ptrs = (C.c_void_p * len(srcs))(*[t.data_ptr() for t in srcs])
+    nk = (C.c_int64 * len(srcs))(*nks)
+    ext.call("fb_fedagg_step_f32", ptrs, nk, len(srcs), int(deterministic), w_slice.data_ptr(), m_slice.data_ptr(),
+             w_out.data_ptr(), m_out.data_ptr(), w_slice.numel(), float(eta), float(mu), int(nesterov),
+             agg.stats.data_ptr(), agg.bad.data_ptr(), None, ext.stream_handle())

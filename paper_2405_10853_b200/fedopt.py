@@ -263,6 +263,7 @@ class AggregatorState:
 
     def _pg_device(self, raw_sum=False):
         t = _torch()
+        ext.lib()
         pg = t.empty(self.model_len, dtype=t.float64, device="cuda")
         srcs = self._launch(None, None, None, None, 1.0, 0.0, False, pg_out=pg)
         t.cuda.current_stream().synchronize()
@@ -305,6 +306,7 @@ def server_step(opt: ServerOptState, w_prev, delta, round_num: Optional[int] = N
     inputs stay in HBM."""
     t = _torch()
     n = len(w_prev)
+    ext.lib()  # no CPU fallback
     if len(opt.momentum) != n or len(delta) != n:
         raise ParamError(f"server_step length mismatch: w={n}, delta={len(delta)}, momentum={len(opt.momentum)}")
     on_device = isinstance(w_prev, DeviceVector)

@@ -166,6 +166,7 @@ class LossEvaluator:
     def _run(self, params, batch, want_grad):
         import torch
         arr = validate_batch(batch, self.cfg)
+        ext.lib()  # raises FedB200Error without the library or a B200: no CPU fallback
         B, T = arr.shape
         check_gpu_shape(self.cfg, T)
         w = self._upload(params)

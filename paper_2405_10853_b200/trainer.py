@@ -62,6 +62,7 @@ class ClientSession:
     def __init__(self, evaluator: LossEvaluator, batches: BatchIterator, adamw_cfg: AdamWConfig,
                  sched: ScheduleConfig):
         self.ev, self.batches, self.adamw_cfg, self.sched = evaluator, batches, adamw_cfg, sched
+        ext.lib()  # no CPU fallback
         cfg = evaluator.cfg
         self.T = batches.corpus.sequence_len
         if self.T > cfg.context_len:

@@ -1,0 +1,157 @@
+"""CPU-side checks: the C-ABI library exports every entry point include/fedb200.h
+declares, the product fails loudly without a B200 (no CPU fallback), and the host
+logic (index contract, init, schedule, validation) matches the reference goldens."""
+import ctypes
+import hashlib
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT, golden
+
+HEADER = os.path.join(ROOT, "include", "fedb200.h")
+
+
+def declared_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"^(?:int|int64_t|const char\*)\s+(fb_\w+)\s*\(", txt, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2405_10853_b200 import ext
+    assert os.path.exists(ext.LIB_PATH), "run __graft_entry__.build() first"
+    L = ctypes.CDLL(ext.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 25
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+    assert L.fb_abi_version() == 1
+    # every declared entry has a ctypes signature in the binding
+    bound = set(ext.SIGNATURES) | {"fb_last_error", "fb_model_n_params", "fb_model_workspace_bytes"}
+    assert set(syms) <= bound, set(syms) - bound
+
+
+def test_model_size_matches_reference_formula():
+    from paper_2405_10853_b200 import ext
+    L = ext.lib(require_device=False)
+    for V, ctx, nl, d, H in [(256, 128, 2, 512, 8), (32000, 2048, 24, 2048, 16), (32000, 2048, 12, 768, 12)]:
+        cfg = ext.ModelCfg(V, ctx, nl, d, H, 1)
+        n = L.fb_model_n_params(ctypes.byref(cfg))
+        assert n == V * d + nl * (12 * d * d + 4 * d) + 2 * d + d * V   # reference tests/test_model.py:132-139
+    assert L.fb_model_n_params(ctypes.byref(ext.ModelCfg(256, 128, 2, 512, 8, 1))) == 6_558_720
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2405_10853_b200 import ext
+    from paper_2405_10853_b200.config import TinyLMConfig
+    from paper_2405_10853_b200.model import LossEvaluator
+    ev = LossEvaluator(TinyLMConfig(vocab_size=256, context_len=64, n_layers=1, d_model=128, n_heads=2), device="cpu")
+    with pytest.raises(ext.FedB200Error, match="B200"):
+        ev.loss(ev.init_params(), np.zeros((1, 64), dtype=np.int64))
+
+
+def test_unsupported_shape_is_loud():
+    from paper_2405_10853_b200.config import TinyLMConfig
+    from paper_2405_10853_b200.errors import UnsupportedShapeError
+    from paper_2405_10853_b200.model import check_gpu_shape
+    with pytest.raises(UnsupportedShapeError):
+        check_gpu_shape(TinyLMConfig(vocab_size=32, context_len=8, n_layers=2, d_model=8, n_heads=2))
+    check_gpu_shape(TinyLMConfig(vocab_size=32000, context_len=2048, n_layers=24, d_model=2048, n_heads=16), 2048)
+
+
+@pytest.mark.parametrize("tag,cfg", [("micro", (32, 8, 2, 8, 2, True, 5)), ("h3", (48, 16, 1, 24, 3, True, 9)),
+                                     ("nopos", (32, 8, 1, 16, 2, False, 4))])
+def test_manifest_and_init_bitwise(tag, cfg):
+    from paper_2405_10853_b200.config import TinyLMConfig
+    from paper_2405_10853_b200.model import init_params_host, manifest_entries
+    g = golden("model.npz")
+    V, ctx, L, d, H, alibi, seed = cfg
+    c = TinyLMConfig(vocab_size=V, context_len=ctx, n_layers=L, d_model=d, n_heads=H, use_alibi=alibi, seed=seed)
+    assert [e.tensor_name for e in manifest_entries(c)] == list(g[f"{tag}_names"])
+    assert np.array_equal(init_params_host(c), g[f"{tag}_init"])
+
+
+def test_c1_init_bitwise():
+    from paper_2405_10853_b200.config import TinyLMConfig
+    from paper_2405_10853_b200.model import init_params_host
+    g = golden("model.npz")
+    p = init_params_host(TinyLMConfig(vocab_size=256, context_len=128, n_layers=2, d_model=512, n_heads=8, seed=1234))
+    assert hashlib.sha256(p.tobytes()).hexdigest() == str(g["c1_init_sha"])
+
+
+def test_index_contract_bitwise():
+    from paper_2405_10853_b200 import data
+    g = golden("data.npz")
+    text = data.synth_corpus(99, 400_000)
+    assert hashlib.sha256(text).hexdigest() == str(g["markov_sha"])
+    corpus = data.tokenize_bytes(text, 128, 256)
+    split = data.split_corpus(corpus, 2, 99, 0.05)
+    assert np.array_equal(split.validation, g["val"])
+    for k in range(2):
+        assert np.array_equal(split.shards[k].indices, g[f"shard{k}"])
+        it = data.BatchIterator(corpus, split.shards[k], 16, 99)
+        assert np.array_equal(it.order, g[f"order{k}"])
+        got = []
+        for off in (0, 4, 37):
+            it.seek(off * 16)
+            for _ in range(3):
+                got.append(it.next_batch()[0])
+        assert np.array_equal(np.stack(got), g[f"batches{k}"])
+    split8 = data.split_corpus(data.tokenize_bytes(text, 1024, 32000), 8, 99, 0.05)
+    assert np.array_equal(np.stack([s.indices for s in split8.shards]), g["c8_shards"])
+
+
+def test_schedule_matches_reference():
+    from paper_2405_10853_b200.config import ScheduleConfig, lr_at
+    for r in json.load(open(os.path.join(GOLDEN, "sched.json"))):
+        s = ScheduleConfig(*r["cfg"])
+        assert [lr_at(s, t) for t in r["steps"]] == r["lr"]
+
+
+def test_config_validation():
+    from paper_2405_10853_b200.config import AdamWConfig, ScheduleConfig, TinyLMConfig, lr_at
+    from paper_2405_10853_b200.errors import ParamError
+    with pytest.raises(ParamError):
+        TinyLMConfig(d_model=10, n_heads=4)
+    with pytest.raises(ParamError):
+        ScheduleConfig(base_lr=1e-3, warmup_steps=100, t_max=100)
+    with pytest.raises(ParamError):
+        AdamWConfig(eps=0)
+    with pytest.raises(ParamError):
+        lr_at(ScheduleConfig(base_lr=1e-3), -1)
+
+
+def test_aggregator_protocol_on_host():
+    from paper_2405_10853_b200.errors import AggregationError, ParamError
+    from paper_2405_10853_b200.fedopt import AggregatorState, ClientUpdate, ServerOptState, client_weight
+    assert client_weight(1000, 8000) == 0.125
+    with pytest.raises(ParamError):
+        client_weight(0, 5)
+    agg = AggregatorState(1, 2)
+    agg.accumulate(ClientUpdate(0, 1, 3, [1.0, 2.0]))
+    with pytest.raises(AggregationError, match="duplicate"):
+        agg.accumulate(ClientUpdate(0, 1, 3, [1.0, 2.0]))
+    with pytest.raises(AggregationError, match="round"):
+        agg.accumulate(ClientUpdate(1, 2, 3, [1.0, 2.0]))
+    with pytest.raises(ParamError):
+        agg.accumulate(ClientUpdate(2, 1, 3, [1.0]))
+    with pytest.raises(ParamError):
+        ClientUpdate(0, 1, 0, [1.0])
+    with pytest.raises(ParamError):
+        ClientUpdate(0, 1, 1, [np.nan])
+    b = AggregatorState(1, 2)
+    b.accumulate(ClientUpdate(5, 1, 1, [0.0, 0.0]))
+    mg = agg.merge(b)
+    assert mg.contributors == {0, 5} and mg.total_weight == 4
+    assert mg.weights() == {0: 0.75, 5: 0.25}
+    with pytest.raises(AggregationError, match="overlap"):
+        mg.merge(b)
+    with pytest.raises(ParamError):
+        ServerOptState.fresh(1, eta=0.0, mu=0.5)
