@@ -406,7 +406,11 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16*
 }
 
 template <int DH>
+int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, int B, int T, int H, int use_alibi, cudaStream_t st);
+
+template <int DH>
 static int attn_fwd_launch(const void* qkv, void* o, float* lse, int B, int T, int H, int use_alibi, cudaStream_t st) {
+  if (T % 128 == 0) return attn_fwd_tc_launch<DH>(qkv, o, lse, B, T, H, use_alibi, st);  // tcgen05 path
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   if (T % 128 == 0) {
     constexpr int NW = 8;
@@ -428,6 +432,10 @@ static int attn_fwd_launch(const void* qkv, void* o, float* lse, int B, int T, i
 }
 
 template <int DH>
+int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const float* Dbuf, float* dq, void* dqkv,
+                       int B, int T, int H, int use_alibi, cudaStream_t st);
+
+template <int DH>
 static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const float* lse, void* dqkv, float* work,
                            int B, int T, int H, int use_alibi, cudaStream_t st) {
   const int d = H * DH;
@@ -437,6 +445,13 @@ static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const
   const int nw = B * T * H;
   attn_bwd_dot_kernel<<<(nw + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dO, Dbuf, B, T, H, DH);
   FB_LAUNCH_CHECK();
+  if (T % 128 == 0) {  // tcgen05 path
+    int rc = attn_bwd_tc_launch<DH>(qkv, dO, lse, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
+    if (rc) return rc;
+    dq_finalize_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq, (__nv_bfloat16*)dqkv, B * T, d);
+    FB_LAUNCH_CHECK();
+    return FB_OK;
+  }
   const int shm = 2 * 64 * DH * 2 + 4 * 64 * DH * 2 + 64 * 64 * 2 + 4 * 64 * 4;
   auto k = attn_bwd_kernel<DH>;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, shm));
