@@ -1,0 +1,70 @@
+"""torchrun --nproc-per-node G tools/multi_gpu_check.py
+Round-end exchange over NCCL (all-to-all of client slices + shard-local fused kernel +
+all-gather) must be bit-identical to the single-GPU fused aggregation. Also reports the
+exchange time (max over ranks) for N params, K clients."""
+import ctypes as C
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2405_10853_b200 import ext  # noqa: E402
+from paper_2405_10853_b200.dist import ShardedAggregator, clients_of  # noqa: E402
+
+N = int(os.environ.get("CHK_N", "70542336"))
+K = int(os.environ.get("CHK_K", "8"))
+local = int(os.environ["LOCAL_RANK"])
+torch.cuda.set_device(local)
+dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+rank, world = dist.get_rank(), dist.get_world_size()
+ext.lib()
+
+
+def client(k):
+    g = torch.Generator(device="cuda").manual_seed(100 + k)
+    return w + torch.empty(N, device="cuda").normal_(0, 2e-3, generator=g)
+
+
+g0 = torch.Generator(device="cuda").manual_seed(7)
+w = torch.empty(N, device="cuda").normal_(0, 0.02, generator=g0)
+m = torch.empty(N, device="cuda").normal_(0, 1e-3, generator=g0)
+nk = {k: 1000 + 7 * k for k in range(K)}
+agg = ShardedAggregator(N, K)
+mine = {k: client(k) for k in clients_of(rank, world, K)}
+for _ in range(2):
+    agg.exchange(mine)
+    w_new, m_shard = agg.step(w, m[agg.lo:agg.hi].contiguous(), nk, 0.7, 0.9, True)
+torch.cuda.synchronize()
+dist.barrier()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+reps = 5
+for _ in range(reps):
+    agg.exchange(mine)
+    w_new, m_shard = agg.step(w, m[agg.lo:agg.hi].contiguous(), nk, 0.7, 0.9, True)
+e1.record()
+torch.cuda.synchronize()
+ms = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
+dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+# single-GPU reference on every rank (all clients regenerated locally)
+allc = [client(k) for k in range(K)]
+ptrs = (C.c_void_p * K)(*[t.data_ptr() for t in allc])
+nks = (C.c_int64 * K)(*[nk[k] for k in range(K)])
+wr, mr = torch.empty_like(w), torch.empty_like(m)
+ext.call("fb_fedagg_step_f32", ptrs, nks, K, 1, w.data_ptr(), m.data_ptr(), wr.data_ptr(), mr.data_ptr(), N, 0.7, 0.9, 1,
+         None, None, None, ext.stream_handle())
+torch.cuda.synchronize()
+ok_w = torch.equal(w_new.view(torch.int32), wr.view(torch.int32))
+ok_m = torch.equal(m_shard.view(torch.int32), mr[agg.lo:agg.hi].view(torch.int32))
+flags = torch.tensor([int(ok_w), int(ok_m)], device="cuda")
+dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+per_rank_bytes = 4 * N * len(mine) * (world - 1) / world + 4 * N * (world - 1) / world
+if rank == 0:
+    print(json.dumps({"world": world, "N": N, "K": K, "bit_identical_w": bool(flags[0]), "bit_identical_m": bool(flags[1]),
+                      "exchange_ms": round(float(ms), 3),
+                      "nvlink_bytes_per_rank_per_dir": int(per_rank_bytes),
+                      "nvlink_gbs_per_rank": round(per_rank_bytes / (float(ms) / 1e3) / 1e9, 1)}), flush=True)
+dist.destroy_process_group()
