@@ -288,8 +288,153 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------
+// 2-SM variant: a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile with
+// tcgen05.mma.cta_group::2 (M = 256). Each CTA stages its 128 rows of A and its 128 of
+// the 256 B rows, so per-SM operand traffic drops from 48 KB to 32 KB per 64-deep
+// k-block and 6 stages fit. The leader CTA (rank 0) issues all MMAs; accumulator rows
+// land in each CTA's own TMEM, and each CTA drains its own 128 rows.
+constexpr int kStages2 = 6;
+constexpr int kStage2Bytes = 2 * BM * BK * 2;  // A half + B half
+constexpr int kSmem2 = kStages2 * kStage2Bytes + 1024 + 1024;
+
+template <int A_MN, int B_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
+    gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
+                         int N, int K, EpiArgs ep) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw_addr = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
+  uint8_t* tiles = smem;
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages2 * kStage2Bytes);
+  uint64_t* empty_bar = full_bar + kStages2;
+  uint64_t* tfull_bar = empty_bar + kStages2;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int num_m = (M + 255) / 256;
+  const int num_n = (N + 255) / 256;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = (K + BK - 1) / BK;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull_bar[b], 1);
+      mbar_init(&tempty_bar[b], 8);  // 4 epilogue warps x 2 CTAs
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_2sm(tmem_slot, 512);
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        const int m0 = (tile % num_m) * 256 + rank * 128;
+        const int n0 = (tile / num_m) * 256 + rank * 128;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = tiles + stage * kStage2Bytes;
+          uint8_t* sb = sa + BM * BK * 2;
+          if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStage2Bytes);
+          const int k0 = kb * BK;
+          if (A_MN) tma_load_3d_2sm(sa, &tmA, &full_bar[stage], 0, k0, m0 / 64);
+          else      tma_load_2d_2sm(sa, &tmA, &full_bar[stage], k0, m0);
+          if (B_MN) tma_load_3d_2sm(sb, &tmB, &full_bar[stage], 0, k0, n0 / 64);
+          else      tma_load_2d_2sm(sb, &tmB, &full_bar[stage], k0, n0);
+          if (++stage == kStages2) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = idesc_bf16_f32(256, 256, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
+        const int buf = it & 1;
+        const uint32_t use = it >> 1;
+        mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * 256;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = smem_u32(tiles + stage * kStage2Bytes);
+            const uint32_t sb = sa + BM * BK * 2;
+#pragma unroll
+            for (int kk = 0; kk < BK / 16; ++kk) {
+              const uint64_t ad = A_MN ? smem_desc_sw128(sa + kk * 2048, BK * 128, 1024)
+                                       : smem_desc_sw128(sa + kk * 32, 16, 1024);
+              const uint64_t bd = B_MN ? smem_desc_sw128(sb + kk * 2048, BK * 128, 1024)
+                                       : smem_desc_sw128(sb + kk * 32, 16, 1024);
+              umma_f16_2sm(d_tmem, ad, bd, idesc, (kb | kk) != 0);
+            }
+            umma_commit_2sm_mc(&empty_bar[stage]);
+          }
+          __syncwarp();
+          if (++stage == kStages2) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) umma_commit_2sm_mc(&tfull_bar[buf]);
+        __syncwarp();
+      }
+    }
+  } else {
+    const int quad = warp & 3;
+    int it = 0;
+    for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
+      const int m0 = (tile % num_m) * 256 + rank * 128;
+      const int n0 = (tile / num_m) * 256;
+      const int buf = it & 1;
+      const uint32_t use = it >> 1;
+      mbar_wait(&tfull_bar[buf], use & 1);
+      tc_fence_after();
+      const int64_t row = m0 + quad * 32 + lane;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * 256;
+#pragma unroll 1
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
+        tmem_ld_wait();
+        if (c == 7) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader(&tempty_bar[buf]);
+        }
+        const int col = n0 + c * 32;
+        if (row < M && col < N) epilogue_chunk<EPI>(ep, row, col, N, r);
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_2sm(tmem_base, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+int g_gemm_2sm = 1;  // fb_gemm_set_2sm() toggles it (A/B tests)
 
 static int get_encoder() {
   if (g_encode) return FB_OK;
@@ -353,6 +498,38 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, in
   return FB_OK;
 }
 
+template <int A_MN, int B_MN, int EPI>
+static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiArgs& ep,
+                          cudaStream_t st) {
+  auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN, EPI>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
+    attr_set = true;
+  }
+  const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  const int clusters = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
+  kern<<<2 * clusters, kGemmThreads, kSmem2, st>>>(ta, tb, M, N, K, ep);
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
+template <int A_MN, int B_MN>
+static int dispatch_epi2(int epi, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
+                         const EpiArgs& ep, cudaStream_t st) {
+  switch (epi) {
+    case FB_EPI_BF16: return launch_gemm2_t<A_MN, B_MN, FB_EPI_BF16>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_F32: return launch_gemm2_t<A_MN, B_MN, FB_EPI_F32>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_ACC_F32: return launch_gemm2_t<A_MN, B_MN, FB_EPI_ACC_F32>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_RESID_F32: return launch_gemm2_t<A_MN, B_MN, FB_EPI_RESID_F32>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_GELU: return launch_gemm2_t<A_MN, B_MN, FB_EPI_GELU>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_DGELU: return launch_gemm2_t<A_MN, B_MN, FB_EPI_DGELU>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_RESID_F32_BF16: return launch_gemm2_t<A_MN, B_MN, FB_EPI_RESID_F32_BF16>(ta, tb, M, N, K, ep, st);
+  }
+  set_error("unknown epilogue %d", epi);
+  return FB_BAD_ARG;
+}
+
 template <int BN, int A_MN, int B_MN>
 static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
                         const EpiArgs& ep, cudaStream_t st) {
@@ -372,6 +549,7 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, i
 }  // namespace fb
 
 namespace fb {
+extern int g_gemm_2sm;
 int gemm_dispatch(int key, int epilogue, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
                   const EpiArgs& ep, cudaStream_t st);
 }
@@ -394,24 +572,36 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   FB_REQUIRE(!need_aux_out || d_aux_out, "gemm: epilogue %d needs aux_out", epilogue);
   int rc = get_encoder();
   if (rc) return rc;
-  // tile width: 256 columns when that still fills the machine, else 128
+  // 2-SM 256x256 tiles when they fill the 74 CTA pairs; else 1-SM 128x256, else 128x128
+  const int tiles2 = ((M + 255) / 256) * ((N + 255) / 256);
+  const bool use2 = g_gemm_2sm && M >= 256 && N >= 256 && tiles2 >= kNumSMs / 2;
   const int tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256);
-  const int BN = (N >= 256 && tiles256 >= kNumSMs) ? 256 : 128;
+  const int BN = (use2 || (N >= 256 && tiles256 >= kNumSMs)) ? 256 : 128;
   CUtensorMap ta, tb;
   rc = a_major ? make_map_mnmajor(&ta, d_A, M, K, lda, BM) : make_map_kmajor(&ta, d_A, M, K, lda, BM);
   if (rc) return rc;
-  rc = b_major ? make_map_mnmajor(&tb, d_B, N, K, ldb, BN) : make_map_kmajor(&tb, d_B, N, K, ldb, BN);
+  const int bbox = use2 ? 128 : BN;  // 2-SM: each CTA stages 128 of the 256 B rows
+  rc = b_major ? make_map_mnmajor(&tb, d_B, N, K, ldb, bbox) : make_map_kmajor(&tb, d_B, N, K, ldb, bbox);
   if (rc) return rc;
   EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux};
   cudaStream_t st = (cudaStream_t)stream;
   const int key = (BN == 256 ? 4 : 0) | (a_major ? 2 : 0) | (b_major ? 1 : 0);
   const int pi = prof_on() ? prof_start(0, st) : -1;
-  rc = gemm_dispatch(key, epilogue, ta, tb, M, N, K, ep, st);
+  if (use2) {
+    const int k2 = (a_major ? 2 : 0) | (b_major ? 1 : 0);
+    rc = k2 == 0 ? dispatch_epi2<0, 0>(epilogue, ta, tb, M, N, K, ep, st)
+       : k2 == 1 ? dispatch_epi2<0, 1>(epilogue, ta, tb, M, N, K, ep, st)
+       : k2 == 2 ? dispatch_epi2<1, 0>(epilogue, ta, tb, M, N, K, ep, st)
+                 : dispatch_epi2<1, 1>(epilogue, ta, tb, M, N, K, ep, st);
+  } else {
+    rc = gemm_dispatch(key, epilogue, ta, tb, M, N, K, ep, st);
+  }
   prof_stop(0, pi, st, 2.0 * M * N * (double)K);
   return rc;
 }
 
 namespace fb {
+extern int g_gemm_2sm;
 int gemm_dispatch(int key, int epilogue, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
                   const EpiArgs& ep, cudaStream_t st) {
   switch (key) {
@@ -427,3 +617,8 @@ int gemm_dispatch(int key, int epilogue, const CUtensorMap& ta, const CUtensorMa
   return FB_BAD_ARG;
 }
 }  // namespace fb
+
+extern "C" int fb_gemm_set_2sm(int enable) {
+  fb::g_gemm_2sm = enable ? 1 : 0;
+  return FB_OK;
+}

@@ -136,10 +136,10 @@ def test_gemm_layouts(fb, M, N, K, a_major, b_major):
     assert err <= 1e-3 * K ** 0.5 + 1e-2, err
 
 
-def test_gemm_epilogues(fb):
+@pytest.mark.parametrize("M,N,K", [(512, 768, 384), (2048, 4096, 512)])
+def test_gemm_epilogues(fb, M, N, K):
     torch.manual_seed(1)
     dev = torch.device("cuda")
-    M, N, K = 512, 768, 384
     A = torch.randn(M, K, device=dev).to(torch.bfloat16)
     B = (0.05 * torch.randn(N, K, device=dev)).to(torch.bfloat16)
     ref = A.float() @ B.float().t()
@@ -165,3 +165,22 @@ def test_gemm_epilogues(fb):
     torch.nn.functional.gelu(x).backward(ref)
     torch.testing.assert_close(o.float(), x.grad, atol=3e-2, rtol=2e-2)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("a_major,b_major", [(0, 0), (0, 1), (1, 1)])
+def test_gemm_2sm_matches_1sm(fb, a_major, b_major):
+    """The cta_group::2 kernel and the 1-SM kernel give the same fp32 results."""
+    torch.manual_seed(5)
+    dev = torch.device("cuda")
+    M, N, K = 4096, 2048, 1024
+    A = torch.randn(M, K, device=dev).to(torch.bfloat16)
+    B = torch.randn(N, K, device=dev).to(torch.bfloat16)
+    Ast = A.t().contiguous() if a_major else A
+    Bst = B.t().contiguous() if b_major else B
+    outs = []
+    for en in (1, 0):
+        fb.call("fb_gemm_set_2sm", en)
+        outs.append(_gemm(fb, Ast, Bst, a_major, b_major, M, N, K))
+    fb.call("fb_gemm_set_2sm", 1)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
