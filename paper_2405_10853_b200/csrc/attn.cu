@@ -410,7 +410,7 @@ int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, int B, int T, int H
 
 template <int DH>
 static int attn_fwd_launch(const void* qkv, void* o, float* lse, int B, int T, int H, int use_alibi, cudaStream_t st) {
-  if (T % 128 == 0) return attn_fwd_tc_launch<DH>(qkv, o, lse, B, T, H, use_alibi, st);  // tcgen05 path
+  if (T % 256 == 0) return attn_fwd_tc_launch<DH>(qkv, o, lse, B, T, H, use_alibi, st);  // tcgen05 path
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
   if (T % 128 == 0) {
     constexpr int NW = 8;

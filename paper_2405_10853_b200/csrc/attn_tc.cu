@@ -30,62 +30,68 @@ __device__ __forceinline__ float ex2(float x) {
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// v2 layout: a CTA owns TWO 128-query tiles (rows q0..q0+255) that ping-pong on the
+// tensor core: while warpgroup 0 turns S0 into P0, the MMA warp runs S1 / PV1 and
+// vice versa. KV tiles are 64 keys, double-buffered.
 template <int DH>
 struct AttnTcCfg {
-  static constexpr int BM = 128, BN = 128;
-  static constexpr int TILE = 128 * DH * 2;  // one 128-row x DH bf16 tile
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = Q_OFF + TILE;          // [2] stages
-  static constexpr int V_OFF = K_OFF + 2 * TILE;      // [2] stages
-  static constexpr int P_OFF = V_OFF + 2 * TILE;      // 128 x 128 bf16
-  static constexpr int BAR_OFF = P_OFF + 128 * 128 * 2;
+  static constexpr int BN = 64;
+  static constexpr int QT = 128 * DH * 2;      // one 128-row Q tile
+  static constexpr int KT = BN * DH * 2;       // one 64-row K (or V) tile
+  static constexpr int PT = 128 * BN * 2;      // one P tile (128 q x 64 keys)
+  static constexpr int Q_OFF = 0;              // [2] Q tiles
+  static constexpr int K_OFF = 2 * QT;         // [2] stages
+  static constexpr int V_OFF = K_OFF + 2 * KT; // [2] stages
+  static constexpr int P_OFF = V_OFF + 2 * KT; // [2] P tiles
+  static constexpr int BAR_OFF = P_OFF + 2 * PT;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
-  static constexpr uint32_t TMEM_COLS = 256;
 };
 
 template <int DH>
-__global__ void __launch_bounds__(192, 1)
-    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tm, __nv_bfloat16* __restrict__ out,
+__global__ void __launch_bounds__(320, 1)
+    attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tm,
+                       __nv_bfloat16* __restrict__ out,
                        float* __restrict__ lse2, int T, int H, float scale_log2, int use_alibi) {
   using Cf = AttnTcCfg<DH>;
+  constexpr int BN = Cf::BN;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cf::BAR_OFF);
   uint64_t* q_full = bar + 0;
-  uint64_t* k_full = bar + 1;   // [2]
-  uint64_t* v_full = bar + 3;   // [2]
-  uint64_t* kv_empty = bar + 5; // [2]
-  uint64_t* s_full = bar + 7;
-  uint64_t* s_empty = bar + 8;
-  uint64_t* p_full = bar + 9;
-  uint64_t* o_full = bar + 10;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  uint64_t* kv_full = bar + 1;   // [2]
+  uint64_t* kv_empty = bar + 3;  // [2]
+  uint64_t* s_full = bar + 5;    // [2] per Q tile
+  uint64_t* s_empty = bar + 7;   // [2]
+  uint64_t* p_full = bar + 9;    // [2]
+  uint64_t* o_full = bar + 11;   // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nq = T / 128;
-  const int qb = nq - 1 - blockIdx.x;  // heavy tiles first
+  const int npair = T / 256;
+  const int pb = npair - 1 - blockIdx.x;  // heavy pairs first
   const int bh = blockIdx.y, b = bh / H, h = bh % H;
   const int d = H * DH;
-  const int row0 = b * T;              // first row of this sequence in [B*T]
-  const int q0 = qb * 128;
-  const int ntiles = qb + 1;
+  const int row0 = b * T;
+  const int q0 = pb * 256;
+  const int nkv = (q0 + 256) / BN;       // KV tiles for tile 1
+  const int nkv0 = (q0 + 128) / BN;      // KV tiles for tile 0
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
+    tma_prefetch(&tmq);
     mbar_init(q_full, 1);
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&v_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&o_full[i], 1);
     }
-    mbar_init(s_full, 1);
-    mbar_init(s_empty, 4);
-    mbar_init(p_full, 4);
-    mbar_init(o_full, 1);
     fence_barrier_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cf::TMEM_COLS);
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -95,124 +101,124 @@ __global__ void __launch_bounds__(192, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer ----------------
-      const int zq = (0 * d + h * DH) / 64, zk = (1 * d + h * DH) / 64, zv = (2 * d + h * DH) / 64;
-      mbar_arrive_expect_tx(q_full, Cf::TILE);
-      tma_load_3d(smem + Cf::Q_OFF, &tm, q_full, 0, row0 + q0, zq);
-      for (int j = 0; j < ntiles; ++j) {
+      const int zq = (h * DH) / 64, zk = (d + h * DH) / 64, zv = (2 * d + h * DH) / 64;
+      mbar_arrive_expect_tx(q_full, 2 * Cf::QT);
+      tma_load_3d(smem + Cf::Q_OFF, &tmq, q_full, 0, row0 + q0, zq);
+      tma_load_3d(smem + Cf::Q_OFF + Cf::QT, &tmq, q_full, 0, row0 + q0 + 128, zq);
+      for (int j = 0; j < nkv; ++j) {
         const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&kv_empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&k_full[s], Cf::TILE);
-        tma_load_3d(smem + Cf::K_OFF + s * Cf::TILE, &tm, &k_full[s], 0, row0 + j * 128, zk);
-        mbar_arrive_expect_tx(&v_full[s], Cf::TILE);
-        tma_load_3d(smem + Cf::V_OFF + s * Cf::TILE, &tm, &v_full[s], 0, row0 + j * 128, zv);
+        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[s], 2 * Cf::KT);
+        tma_load_3d(smem + Cf::K_OFF + s * Cf::KT, &tm, &kv_full[s], 0, row0 + j * BN, zk);
+        tma_load_3d(smem + Cf::V_OFF + s * Cf::KT, &tm, &kv_full[s], 0, row0 + j * BN, zv);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer ----------------
-      constexpr uint32_t idS = idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idS = idesc_bf16_f32(128, BN, 0, 0);
       constexpr uint32_t idO = idesc_bf16_f32(128, DH, 0, 1);
-      const uint32_t tS = tmem, tO = tmem + 128;
-      mbar_wait(q_full, 0);
-      for (int j = 0; j < ntiles; ++j) {
+      // TMEM: S_g at [64 g, 64 g + 64), O_g at [128 + DH g, 128 + DH (g+1))
+      auto issue_s = [&](int g, int j) {
         const int s = j & 1;
-        const uint32_t ph = (j >> 1) & 1;
-        mbar_wait(&k_full[s], ph);
-        mbar_wait(s_empty, (j & 1) ^ 1);
+        mbar_wait(&s_empty[g], (((g ? j : j) & 1)) ^ 1);
         tc_fence_after();
-        const uint32_t kb = sK + s * Cf::TILE;
+        const uint32_t qb = sQ + g * Cf::QT, kb = sK + s * Cf::KT;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-          umma_f16(tS, smem_desc_sw128(sQ + off, 16, 1024), smem_desc_sw128(kb + off, 16, 1024), idS, kk > 0);
+          const uint32_t qoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          const uint32_t koff = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
+          umma_f16(tmem + 64 * g, smem_desc_sw128(qb + qoff, 16, 1024), smem_desc_sw128(kb + koff, 16, 1024), idS,
+                   kk > 0);
         }
-        umma_commit(s_full);
-        mbar_wait(p_full, j & 1);  // P_j written and O rescaled by the softmax warps
-        mbar_wait(&v_full[s], ph);
+        umma_commit(&s_full[g]);
+      };
+      auto issue_pv = [&](int g, int j) {
+        const int s = j & 1;
+        mbar_wait(&p_full[g], j & 1);
         tc_fence_after();
-        const uint32_t vb = sV + s * Cf::TILE;
+        const uint32_t pb_ = sP + g * Cf::PT, vb = sV + s * Cf::KT;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // 128 keys / 16
-          const uint32_t poff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-          umma_f16(tO, smem_desc_sw128(sP + poff, 16, 1024), smem_desc_sw128(vb + kk * 2048, 128 * 128, 1024), idO,
-                   (j | kk) > 0);
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          umma_f16(tmem + 128 + DH * g, smem_desc_sw128(pb_ + kk * 32, 16, 1024),
+                   smem_desc_sw128(vb + kk * 2048, BN * 128, 1024), idO, (j | kk) > 0);
         }
-        umma_commit(o_full);
-        umma_commit(&kv_empty[s]);
+        umma_commit(&o_full[g]);
+      };
+      mbar_wait(q_full, 0);
+      mbar_wait(&kv_full[0], 0);
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < nkv; ++j) {
+        const bool nxt = j + 1 < nkv;
+        if (nxt) mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        if (j < nkv0) issue_pv(0, j);
+        if (nxt && j + 1 < nkv0) issue_s(0, j + 1);
+        issue_pv(1, j);
+        umma_commit(&kv_empty[j & 1]);
+        if (nxt) issue_s(1, j + 1);
       }
     }
   } else {
-    // ---------------- softmax warps 2..5 ----------------
+    // ---------------- softmax warpgroups: warps 2-5 -> Q tile 0, warps 6-9 -> Q tile 1 ----------------
+    const int g = (warp - 2) >> 2;
     const int quad = warp & 3;
-    const int r = quad * 32 + lane;  // row within the tile == TMEM lane
-    const int qi = q0 + r;           // query position
-    const uint32_t tS = tmem + ((uint32_t)(quad * 32) << 16);
-    const uint32_t tO = tS + 128;
+    const int r = quad * 32 + lane;
+    const int qi = q0 + 128 * g + r;
+    const int ntile = g ? nkv : nkv0;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const uint32_t tS = tmem + lane_off + 64 * g;
+    const uint32_t tO = tmem + lane_off + 128 + DH * g;
     const float sl = use_alibi ? exp2f(-8.0f * (float)(h + 1) / (float)H) * 1.4426950408889634f : 0.0f;
+    const uint32_t prow = sP + g * Cf::PT + r * 128;
     float m = -INFINITY, l = 0.f;
-    const uint32_t prow = sP + r * 128;
-    for (int j = 0; j < ntiles; ++j) {
-      const int k0 = j * 128;
-      const bool diag = (j == ntiles - 1);
-      mbar_wait(s_full, j & 1);
+    for (int j = 0; j < ntile; ++j) {
+      const int k0 = j * BN;
+      const bool diag = k0 + BN > qi - r;  // tile reaches this Q tile's diagonal
+      mbar_wait(&s_full[g], j & 1);
       tc_fence_after();
-      // pass 1: row max of the scaled, biased, masked scores
+      uint32_t v[64];
+      tmem_ld_32x32b_x32(tS, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+      tmem_ld_32x32b_x32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+      tmem_ld_wait();
+      // x = S * scale + sl * (k - q): bias base for key k0, step sl per key
+      const float base = sl * (float)(k0 - qi);
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tS + c * 32, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int kj = k0 + c * 32 + i;
-          float x = __uint_as_float(v[i]) * scale_log2 - sl * (float)(qi - kj);
-          if (diag && kj > qi) x = -INFINITY;
-          mx = fmaxf(mx, x);
-        }
+      for (int i = 0; i < 64; ++i) {
+        float x = fmaf(__uint_as_float(v[i]), scale_log2, fmaf(sl, (float)i, base));
+        if (diag && k0 + i > qi) x = -INFINITY;
+        v[i] = __float_as_uint(x);
+        mx = fmaxf(mx, x);
       }
       const float m_new = fmaxf(m, mx);
       const float alpha = ex2(m - m_new);
-      // pass 2: P = exp2(x - m_new) -> bf16 -> swizzled K-major smem tile; row sum
       float rs = 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tS + c * 32, v);
-        tmem_ld_wait();
+      for (int q = 0; q < 8; ++q) {
+        float p[8];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float p[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int kj = k0 + c * 32 + q * 8 + i;
-            const float x = __uint_as_float(v[q * 8 + i]) * scale_log2 - sl * (float)(qi - kj);
-            p[i] = (diag && kj > qi) ? 0.f : ex2(x - m_new);
-            rs += p[i];
-          }
-          const int kc = c * 4 + q;  // 8-key chunk 0..15
-          const uint32_t addr = prow + (kc >> 3) * (128 * 128) + (((kc & 7) ^ (r & 7)) << 4);
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(pack_bf16(p[0], p[1])),
-                       "r"(pack_bf16(p[2], p[3])), "r"(pack_bf16(p[4], p[5])), "r"(pack_bf16(p[6], p[7])));
+        for (int i = 0; i < 8; ++i) {
+          p[i] = ex2(__uint_as_float(v[8 * q + i]) - m_new);
+          rs += p[i];
         }
+        const uint32_t addr = prow + (((q) ^ (r & 7)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(pack_bf16(p[0], p[1])),
+                     "r"(pack_bf16(p[2], p[3])), "r"(pack_bf16(p[4], p[5])), "r"(pack_bf16(p[6], p[7])));
       }
       l = l * alpha + rs;
       m = m_new;
-      // rescale the TMEM accumulator O by alpha once PV_{j-1} has landed (skip when no row moved)
       if (j > 0) {
-        mbar_wait(o_full, (j - 1) & 1);
+        mbar_wait(&o_full[g], (j - 1) & 1);
         tc_fence_after();
         if (__any_sync(0xffffffffu, alpha != 1.0f)) {
 #pragma unroll
           for (int c = 0; c < DH / 32; ++c) {
-            uint32_t v[32];
-            tmem_ld_32x32b_x32(tO + c * 32, v);
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tO + c * 32, o);
             tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * alpha);
-            tmem_st_32x32b_x32(tO + c * 32, v);
+            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st_32x32b_x32(tO + c * 32, o);
           }
           tmem_st_wait();
         }
@@ -221,22 +227,22 @@ __global__ void __launch_bounds__(192, 1)
       fence_async_smem();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(s_empty);
-        mbar_arrive(p_full);
+        mbar_arrive(&s_empty[g]);
+        mbar_arrive(&p_full[g]);
       }
     }
-    mbar_wait(o_full, (ntiles - 1) & 1);
+    mbar_wait(&o_full[g], (ntile - 1) & 1);
     tc_fence_after();
     const float il = 1.0f / l;
     __nv_bfloat16* orow = out + ((int64_t)row0 + qi) * d + h * DH;
 #pragma unroll
     for (int c = 0; c < DH / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld_32x32b_x32(tO + c * 32, v);
+      uint32_t o[32];
+      tmem_ld_32x32b_x32(tO + c * 32, o);
       tmem_ld_wait();
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float* f = reinterpret_cast<const float*>(v) + 8 * q;
+        const float* f = reinterpret_cast<const float*>(o) + 8 * q;
         uint4 pk = make_uint4(pack_bf16(f[0] * il, f[1] * il), pack_bf16(f[2] * il, f[3] * il),
                               pack_bf16(f[4] * il, f[5] * il), pack_bf16(f[6] * il, f[7] * il));
         *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = pk;
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, Cf::TMEM_COLS);
+    tmem_dealloc(tmem, 512);
   }
 }
 
@@ -268,22 +274,24 @@ int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, int B, int T, int H
     g_enc_attn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   const int d = H * DH;
-  CUtensorMap tm;
+  CUtensorMap tmq, tm;
   cuuint64_t dims[3] = {64, (cuuint64_t)B * T, (cuuint64_t)(3 * d / 64)};
   cuuint64_t strides[2] = {(cuuint64_t)3 * d * 2, 128};
-  cuuint32_t box[3] = {64, 128, DH / 64};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = g_enc_attn(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(qkv), dims, strides, box, es,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("attn tensor map encode failed: %d", (int)r);
-    return FB_CUDA_ERROR;
+  for (int which = 0; which < 2; ++which) {
+    cuuint32_t box[3] = {64, (cuuint32_t)(which ? Cf::BN : 128), DH / 64};  // Q: 128 rows, K/V: 64 rows
+    CUresult r = g_enc_attn(which ? &tm : &tmq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(qkv), dims,
+                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("attn tensor map encode failed: %d", (int)r);
+      return FB_CUDA_ERROR;
+    }
   }
   auto k = attn_fwd_tc_kernel<DH>;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  k<<<dim3(T / 128, B * H), 192, Cf::SMEM, st>>>(tm, (__nv_bfloat16*)o, lse, T, H, scale_log2, use_alibi);
+  k<<<dim3(T / 256, B * H), 320, Cf::SMEM, st>>>(tmq, tm, (__nv_bfloat16*)o, lse, T, H, scale_log2, use_alibi);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }
