@@ -208,9 +208,10 @@ __global__ void __launch_bounds__(NW * 32) attn_fwd_kernel(const __nv_bfloat16* 
 }
 
 // ------------------------------------------------------------------ backward
-// D[bh][t] = sum_c dO * O  (one warp per (row, head))
+// D[bh][t] = sum_c dO * O, one warp per (row, head), 8-byte vector loads; the same warp
+// zeroes that (row, head) slice of the f32 dQ accumulator (saves a memset pass).
 __global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dO,
-                                    float* __restrict__ D, int B, int T, int H, int dh) {
+                                    float* __restrict__ D, float* __restrict__ dq, int B, int T, int H, int dh) {
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (gw >= B * T * H) return;
@@ -219,7 +220,15 @@ __global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o, const _
   const __nv_bfloat16* a = o + (int64_t)row * d + h * dh;
   const __nv_bfloat16* g = dO + (int64_t)row * d + h * dh;
   float s = 0.f;
-  for (int c = lane; c < dh; c += 32) s += __bfloat162float(a[c]) * __bfloat162float(g[c]);
+  for (int c = 4 * lane; c < dh; c += 128) {
+    const uint2 av = *reinterpret_cast<const uint2*>(a + c), gv = *reinterpret_cast<const uint2*>(g + c);
+    const __nv_bfloat162* ap = reinterpret_cast<const __nv_bfloat162*>(&av);
+    const __nv_bfloat162* gp = reinterpret_cast<const __nv_bfloat162*>(&gv);
+    const float2 a0 = __bfloat1622float2(ap[0]), a1 = __bfloat1622float2(ap[1]);
+    const float2 g0 = __bfloat1622float2(gp[0]), g1 = __bfloat1622float2(gp[1]);
+    s += a0.x * g0.x + a0.y * g0.y + a1.x * g1.x + a1.y * g1.y;
+    if (dq) *reinterpret_cast<float4*>(dq + (int64_t)row * d + h * dh + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   s = warp_sum(s);
   if (lane == 0) {
     const int b = row / T, t = row % T;
@@ -397,11 +406,14 @@ __global__ void __launch_bounds__(128) attn_bwd_kernel(const __nv_bfloat16* __re
   }
 }
 
+// dqkv[:, 0:d] = bf16(dq accumulator): 8 columns per thread (two 16-byte loads, one 16-byte store)
 __global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dqkv, int rows, int d) {
-  const int64_t n = (int64_t)rows * d;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / d, c = i % d;
-    dqkv[r * 3 * d + c] = __float2bfloat16_rn(acc[i]);
+  const int64_t n8 = (int64_t)rows * d / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = 8 * i, r = e / d, c = e % d;
+    const float4 x = *reinterpret_cast<const float4*>(acc + e), y = *reinterpret_cast<const float4*>(acc + e + 4);
+    *reinterpret_cast<uint4*>(dqkv + r * 3 * d + c) =
+        make_uint4(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w), pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
   }
 }
 
@@ -441,9 +453,9 @@ static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const
   const int d = H * DH;
   float* Dbuf = work;
   float* dq = work + (int64_t)B * H * T;
-  FB_CUDA_TRY(cudaMemsetAsync(dq, 0, sizeof(float) * (size_t)B * T * d, st));
   const int nw = B * T * H;
-  attn_bwd_dot_kernel<<<(nw + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dO, Dbuf, B, T, H, DH);
+  attn_bwd_dot_kernel<<<(nw + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dO, Dbuf, dq, B, T, H,
+                                                    DH);
   FB_LAUNCH_CHECK();
   if (T % 128 == 0) {  // tcgen05 path
     int rc = attn_bwd_tc_launch<DH>(qkv, dO, lse, Dbuf, dq, dqkv, B, T, H, use_alibi, st);

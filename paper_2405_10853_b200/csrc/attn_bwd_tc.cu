@@ -42,17 +42,16 @@ struct AttnBwdCfg {
   static constexpr int TILE = 128 * DH * 2;
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = K_OFF + TILE;
-  static constexpr int Q_OFF = V_OFF + TILE;
-  static constexpr int O_OFF = Q_OFF + TILE;      // dO
-  static constexpr int P_OFF = O_OFF + TILE;      // P^T   128x128 bf16
-  static constexpr int S_OFF = P_OFF + 32768;     // dS^T  128x128 bf16
-  static constexpr int L_OFF = S_OFF + 32768;     // lse2[2][128], D[2][128]
-  static constexpr int BAR_OFF = L_OFF + 4 * 128 * 4;
-  static constexpr int SMEM = BAR_OFF + 256 + 1024;
+  static constexpr int Q_OFF = V_OFF + TILE;      // [2] stages
+  static constexpr int O_OFF = Q_OFF + 2 * TILE;  // dO [2] stages
+  static constexpr int PS_OFF = O_OFF + 2 * TILE; // P^T, then dS^T (128x128 bf16, shared)
+  static constexpr int L_OFF = PS_OFF + 32768;    // e[128], D[128]
+  static constexpr int BAR_OFF = L_OFF + 2 * 128 * 4;
+  static constexpr int SMEM = BAR_OFF + 160 + 1024;  // 17 mbarriers + TMEM slot; 1 KB alignment slack
 };
 
 template <int DH>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                        const float* __restrict__ lse2, const float* __restrict__ Dd, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dqkv, int T, int H, float scale_log2, float scale, int use_alibi) {
@@ -62,18 +61,20 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cf::BAR_OFF);
   uint64_t* kv_full = bar + 0;
-  uint64_t* q_full = bar + 1;
-  uint64_t* o_full = bar + 2;
-  uint64_t* q_empty = bar + 3;
-  uint64_t* o_empty = bar + 4;
-  uint64_t* s_full = bar + 5;
-  uint64_t* p_full = bar + 6;
-  uint64_t* pds_empty = bar + 7;
-  uint64_t* dq_full = bar + 8;
-  uint64_t* dq_empty = bar + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
-  float* sL = reinterpret_cast<float*>(smem + Cf::L_OFF);  // [2][128]
-  float* sD = sL + 256;                                      // [2][128]
+  uint64_t* q_full = bar + 1;    // [2]
+  uint64_t* o_full = bar + 3;    // [2]
+  uint64_t* q_empty = bar + 5;   // [2]
+  uint64_t* o_empty = bar + 7;   // [2]
+  uint64_t* s_full = bar + 9;
+  uint64_t* p_full = bar + 10;
+  uint64_t* p_free = bar + 11;
+  uint64_t* ds_full = bar + 12;
+  uint64_t* ds_free = bar + 13;
+  uint64_t* dq_full = bar + 14;
+  uint64_t* dq_empty = bar + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  float* sE = reinterpret_cast<float*>(smem + Cf::L_OFF);  // [128]
+  float* sD = sE + 128;                                      // [128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nq = T / 128;
@@ -88,15 +89,19 @@ __global__ void __launch_bounds__(192, 1)
     tma_prefetch(&tm_qkv);
     tma_prefetch(&tm_do);
     mbar_init(kv_full, 1);
-    mbar_init(q_full, 1);
-    mbar_init(o_full, 1);
-    mbar_init(q_empty, 1);
-    mbar_init(o_empty, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&o_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+      mbar_init(&o_empty[s], 1);
+    }
     mbar_init(s_full, 1);
-    mbar_init(p_full, 4);
-    mbar_init(pds_empty, 1);
+    mbar_init(p_full, 8);
+    mbar_init(p_free, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(ds_free, 1);
     mbar_init(dq_full, 1);
-    mbar_init(dq_empty, 4);
+    mbar_init(dq_empty, 8);
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -104,8 +109,8 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t sK = smem_u32(smem + Cf::K_OFF), sV = smem_u32(smem + Cf::V_OFF), sQ = smem_u32(smem + Cf::Q_OFF),
-                 sO = smem_u32(smem + Cf::O_OFF), sP = smem_u32(smem + Cf::P_OFF), sS = smem_u32(smem + Cf::S_OFF);
+  const uint32_t sK = smem_u32(smem + Cf::K_OFF), sV = smem_u32(smem + Cf::V_OFF), sQ0 = smem_u32(smem + Cf::Q_OFF),
+                 sO0 = smem_u32(smem + Cf::O_OFF), sPS = smem_u32(smem + Cf::PS_OFF);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -114,13 +119,15 @@ __global__ void __launch_bounds__(192, 1)
       tma_load_3d(smem + Cf::K_OFF, &tm_qkv, kv_full, 0, row0 + k0, zk);
       tma_load_3d(smem + Cf::V_OFF, &tm_qkv, kv_full, 0, row0 + k0, zv);
       for (int t = 0; t < ntiles; ++t) {
+        const int s = t & 1;
+        const uint32_t ph = (t >> 1) & 1;
         const int q0 = (first + t) * 128;
-        mbar_wait(q_empty, (t & 1) ^ 1);
-        mbar_arrive_expect_tx(q_full, Cf::TILE);
-        tma_load_3d(smem + Cf::Q_OFF, &tm_qkv, q_full, 0, row0 + q0, zq);
-        mbar_wait(o_empty, (t & 1) ^ 1);
-        mbar_arrive_expect_tx(o_full, Cf::TILE);
-        tma_load_3d(smem + Cf::O_OFF, &tm_do, o_full, 0, row0 + q0, zo);
+        mbar_wait(&q_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&q_full[s], Cf::TILE);
+        tma_load_3d(smem + Cf::Q_OFF + s * Cf::TILE, &tm_qkv, &q_full[s], 0, row0 + q0, zq);
+        mbar_wait(&o_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&o_full[s], Cf::TILE);
+        tma_load_3d(smem + Cf::O_OFF + s * Cf::TILE, &tm_do, &o_full[s], 0, row0 + q0, zo);
       }
     }
   } else if (warp == 1) {
@@ -131,114 +138,141 @@ __global__ void __launch_bounds__(192, 1)
       const uint32_t tS = tmem, tP = tmem + 128, tV = tmem + 256, tK = tmem + 256 + DH, tQ = tmem + 128;
       mbar_wait(kv_full, 0);
       for (int t = 0; t < ntiles; ++t) {
-        const uint32_t ph = t & 1;
-        // S^T = K Q^T
-        mbar_wait(q_full, ph);
+        const int s = t & 1;
+        const uint32_t ph = t & 1, sph = (t >> 1) & 1;
+        const uint32_t sQ = sQ0 + s * Cf::TILE, sO = sO0 + s * Cf::TILE;
+        mbar_wait(&q_full[s], sph);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
+        for (int kk = 0; kk < DH / 16; ++kk) {  // S^T = K Q^T
           const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
           umma_f16(tS, smem_desc_sw128(sK + off, 16, 1024), smem_desc_sw128(sQ + off, 16, 1024), idSP, kk > 0);
         }
-        // dP^T = V dO^T (its TMEM columns hold dQ of the previous tile until drained)
-        mbar_wait(o_full, ph);
-        mbar_wait(dq_empty, ph ^ 1);
+        mbar_wait(&o_full[s], sph);
+        mbar_wait(dq_empty, ph ^ 1);  // dP^T columns still hold dQ of the previous tile until drained
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < DH / 16; ++kk) {
+        for (int kk = 0; kk < DH / 16; ++kk) {  // dP^T = V dO^T
           const uint32_t off = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
           umma_f16(tP, smem_desc_sw128(sV + off, 16, 1024), smem_desc_sw128(sO + off, 16, 1024), idSP, kk > 0);
         }
         umma_commit(s_full);
-        // P^T and dS^T are in smem
         mbar_wait(p_full, ph);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // dV += P^T dO   (K = 128 queries)
           const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-          umma_f16(tV, smem_desc_sw128(sP + aoff, 16, 1024), smem_desc_sw128(sO + kk * 2048, 128 * 128, 1024), idKV,
+          umma_f16(tV, smem_desc_sw128(sPS + aoff, 16, 1024), smem_desc_sw128(sO + kk * 2048, 128 * 128, 1024), idKV,
                    (t | kk) > 0);
         }
-        umma_commit(o_empty);
+        umma_commit(p_free);
+        umma_commit(&o_empty[s]);
+        mbar_wait(ds_full, ph);
+        tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // dK += dS^T Q
           const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-          umma_f16(tK, smem_desc_sw128(sS + aoff, 16, 1024), smem_desc_sw128(sQ + kk * 2048, 128 * 128, 1024), idKV,
+          umma_f16(tK, smem_desc_sw128(sPS + aoff, 16, 1024), smem_desc_sw128(sQ + kk * 2048, 128 * 128, 1024), idKV,
                    (t | kk) > 0);
         }
-        umma_commit(q_empty);
+        umma_commit(&q_empty[s]);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // dQ = dS K   (K = 128 keys), dS read as MN-major
-          umma_f16(tQ, smem_desc_sw128(sS + kk * 2048, 128 * 128, 1024),
+          umma_f16(tQ, smem_desc_sw128(sPS + kk * 2048, 128 * 128, 1024),
                    smem_desc_sw128(sK + kk * 2048, 128 * 128, 1024), idQ, kk > 0);
         }
-        umma_commit(pds_empty);
+        umma_commit(ds_free);
         umma_commit(dq_full);
       }
     }
   } else {
+    // warps 2-5 (g = 0) and 6-9 (g = 1): each warpgroup owns half of the 128 query
+    // columns of S^T / dP^T and half of the dh columns of dQ / dK / dV.
+    const int g = (warp - 2) >> 2;
     const int quad = warp & 3;
-    const int r = quad * 32 + lane;  // TMEM lane: key row (phase a) / query row (phase b)
+    const int r = quad * 32 + lane;  // TMEM lane: key row (P/dS phase) / query row (dQ drain)
     const int kj = k0 + r;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t tS = tmem + lane_off, tP = tmem + 128 + lane_off;
+    const uint32_t tS = tmem + lane_off + 64 * g, tP = tmem + 128 + lane_off + 64 * g;
+    const uint32_t tQ = tmem + 128 + lane_off + (DH / 2) * g;
     const float sl = use_alibi ? exp2f(-8.0f * (float)(h + 1) / (float)H) * 1.4426950408889634f : 0.0f;
-    const uint32_t prow = sP + r * 128, srow = sS + r * 128;
-    const int tid = threadIdx.x - 64;  // 0..127
+    const float slk = sl * (float)kj;
+    const uint32_t prow = sPS + r * 128;
+    const int tid = threadIdx.x - 64;  // 0..255
     for (int t = 0; t < ntiles; ++t) {
       const uint32_t ph = t & 1;
       const int q0 = (first + t) * 128;
       const bool diag = (t == 0);
-      float* Lb = sL + (t & 1) * 128;
-      float* Db = sD + (t & 1) * 128;
-      Lb[tid] = lse2[(int64_t)bh * T + q0 + tid];
-      Db[tid] = Dd[(int64_t)bh * T + q0 + tid];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
+      float* Eb = sE;  // e_q = sl * q + lse2_q  (x = S c + sl k - e_q)
+      float* Db = sD;
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // everyone is done with the previous tile's e/D
+      if (tid < 128) Eb[tid] = sl * (float)(q0 + tid) + lse2[(int64_t)bh * T + q0 + tid];
+      else Db[tid - 128] = Dd[(int64_t)bh * T + q0 + tid - 128];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
       mbar_wait(s_full, ph);
-      mbar_wait(pds_empty, ph ^ 1);  // dQ of the previous tile no longer reads dS^T
+      mbar_wait(ds_free, ph ^ 1);  // the shared P/dS tile is no longer read by dQ of the previous tile
       tc_fence_after();
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
+      uint32_t dsp[32];  // dS^T packed bf16x2, written after dV consumed P^T
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
         uint32_t sv[32], pv[32];
         tmem_ld_32x32b_x32(tS + c * 32, sv);
         tmem_ld_32x32b_x32(tP + c * 32, pv);
         tmem_ld_wait();
+        const int qb = 64 * g + 32 * c;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          float p[8], ds[8];
+          float p[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const int ql = c * 32 + q * 8 + i;
-            const int qi = q0 + ql;
-            const float x = __uint_as_float(sv[q * 8 + i]) * scale_log2 - sl * (float)(qi - kj) - Lb[ql];
-            p[i] = (diag && qi < kj) ? 0.f : ex2b(x);
-            ds[i] = p[i] * (__uint_as_float(pv[q * 8 + i]) - Db[ql]);
+            const int ql = qb + q * 8 + i;
+            const float x = fmaf(__uint_as_float(sv[q * 8 + i]), scale_log2, slk - Eb[ql]);
+            p[i] = (diag && q0 + ql < kj) ? 0.f : ex2b(x);
+            sv[q * 8 + i] = __float_as_uint(p[i] * (__uint_as_float(pv[q * 8 + i]) - Db[ql]));
           }
-          const int kc = c * 4 + q;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dsp[c * 16 + q * 4 + i] = pack_bf16(__uint_as_float(sv[q * 8 + 2 * i]), __uint_as_float(sv[q * 8 + 2 * i + 1]));
+          const int kc = (qb >> 3) + q;
           const uint32_t sw = (kc >> 3) * (128 * 128) + (((kc & 7) ^ (r & 7)) << 4);
           asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(pack_bf16(p[0], p[1])),
                        "r"(pack_bf16(p[2], p[3])), "r"(pack_bf16(p[4], p[5])), "r"(pack_bf16(p[6], p[7])));
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(srow + sw), "r"(pack_bf16(ds[0], ds[1])),
-                       "r"(pack_bf16(ds[2], ds[3])), "r"(pack_bf16(ds[4], ds[5])), "r"(pack_bf16(ds[6], ds[7])));
         }
       }
       tc_fence_before();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
-      // drain dQ (thread = query row r of this tile)
+      // dV has consumed P^T: overwrite the shared tile with dS^T
+      mbar_wait(p_free, ph);
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int kc = ((64 * g + 32 * c) >> 3) + q;
+          const uint32_t sw = (kc >> 3) * (128 * 128) + (((kc & 7) ^ (r & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(dsp[c * 16 + q * 4]),
+                       "r"(dsp[c * 16 + q * 4 + 1]), "r"(dsp[c * 16 + q * 4 + 2]), "r"(dsp[c * 16 + q * 4 + 3]));
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+      // drain this warpgroup's half of dQ (thread = query row r of this tile)
       mbar_wait(dq_full, ph);
       tc_fence_after();
-      float* dqrow = dq_acc + ((int64_t)row0 + q0 + r) * d + h * DH;
+      float* dqrow = dq_acc + ((int64_t)row0 + q0 + r) * d + h * DH + (DH / 2) * g;
 #pragma unroll 1
-      for (int c = 0; c < DH / 32; ++c) {
+      for (int c = 0; c < DH / 64; ++c) {
         uint32_t v[32];
-        tmem_ld_32x32b_x32(tP + c * 32, v);
+        tmem_ld_32x32b_x32(tQ + c * 32, v);
         tmem_ld_wait();
+#ifndef FB_ABLATE_DQ
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           red_add_v4(dqrow + c * 32 + 4 * q, __uint_as_float(v[4 * q]) * scale, __uint_as_float(v[4 * q + 1]) * scale,
                      __uint_as_float(v[4 * q + 2]) * scale, __uint_as_float(v[4 * q + 3]) * scale);
+#endif
       }
       tc_fence_before();
       __syncwarp();
@@ -246,13 +280,14 @@ __global__ void __launch_bounds__(192, 1)
     }
     // dK, dV: the last dK/dV MMAs completed before the last dq_full
     const int64_t ld = 3 * (int64_t)d;
-    __nv_bfloat16* dkrow = dqkv + ((int64_t)row0 + kj) * ld + d + h * DH;
+    __nv_bfloat16* dkrow = dqkv + ((int64_t)row0 + kj) * ld + d + h * DH + (DH / 2) * g;
     __nv_bfloat16* dvrow = dkrow + d;
 #pragma unroll 1
-    for (int c = 0; c < DH / 32; ++c) {
+    for (int c = 0; c < DH / 64; ++c) {
       uint32_t kv[32], vv[32];
-      tmem_ld_32x32b_x32(tmem + 256 + DH + lane_off + c * 32, kv);
-      tmem_ld_32x32b_x32(tmem + 256 + lane_off + c * 32, vv);
+      const uint32_t col = (DH / 2) * g + c * 32;
+      tmem_ld_32x32b_x32(tmem + 256 + DH + lane_off + col, kv);
+      tmem_ld_32x32b_x32(tmem + 256 + lane_off + col, vv);
       tmem_ld_wait();
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -314,7 +349,7 @@ int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const 
   auto k = attn_bwd_tc_kernel<DH>;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale = 1.0f / sqrtf((float)DH);
-  k<<<dim3(T / 128, B * H), 192, Cf::SMEM, st>>>(tq, to, lse, Dbuf, dq, (__nv_bfloat16*)dqkv, T, H,
+  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tq, to, lse, Dbuf, dq, (__nv_bfloat16*)dqkv, T, H,
                                                  1.4426950408889634f * scale, scale, use_alibi);
   FB_LAUNCH_CHECK();
   return FB_OK;

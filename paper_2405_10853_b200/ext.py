@@ -11,7 +11,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfedb200.so")
+LIB_PATH = os.environ.get("FB_LIB_PATH") or os.path.join(_HERE, "libfedb200.so")  # override: A/B experiments only
 
 FB_OK, FB_BAD_ARG, FB_CUDA_ERROR, FB_NONFINITE, FB_UNSUPPORTED = 0, 1, 2, 3, 4
 FB_RED_BLOCKS = 1184
