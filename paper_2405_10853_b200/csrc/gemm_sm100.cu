@@ -24,7 +24,7 @@ using namespace sm100;
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kGemmThreads = 192;
+constexpr int kGemmThreads = 320;  // TMA warp, MMA warp, 8 epilogue warps (2 per TMEM lane quadrant)
 
 template <int BN>
 struct GemmCfg {
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 4);
+      mbar_init(&tempty_bar[b], 8);
     }
     fence_barrier_init();
   }
@@ -252,8 +252,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       __syncwarp();
     }
   } else {
-    // ---------------- epilogue warps 2..5 ----------------
+    // ---------------- epilogue warps 2..9: quadrant = warp & 3, column half = (warp - 2) >> 2 ----------------
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int half = (warp - 2) >> 2;
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
       const int m0 = (tile % num_m) * BM;
@@ -263,18 +264,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull_bar[buf], use & 1);
       tc_fence_after();
       const int64_t row = m0 + quad * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * BN + half * (BN / 2);
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < BN / 64; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c * 32, r);
         tmem_ld_wait();
-        if (c == BN / 32 - 1) {
+        if (c == BN / 64 - 1) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty_bar[buf]);
         }
-        const int col = n0 + c * 32;
+        const int col = n0 + half * (BN / 2) + c * 32;
         if (row < M && col < N) epilogue_chunk<EPI>(ep, row, col, N, r);
       }
     }
@@ -330,7 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull_bar[b], 1);
-      mbar_init(&tempty_bar[b], 8);  // 4 epilogue warps x 2 CTAs
+      mbar_init(&tempty_bar[b], 16);  // 8 epilogue warps x 2 CTAs
     }
     fence_barrier_init();
   }
@@ -398,22 +399,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     }
   } else {
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
     int it = 0;
     for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
       const int m0 = (tile % num_m) * 256 + rank * 128;
-      const int n0 = (tile / num_m) * 256;
+      const int n0 = (tile / num_m) * 256 + half * 128;
       const int buf = it & 1;
       const uint32_t use = it >> 1;
       mbar_wait(&tfull_bar[buf], use & 1);
       tc_fence_after();
       const int64_t row = m0 + quad * 32 + lane;
-      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * 256;
+      const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * 256 + half * 128;
 #pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c * 32, r);
         tmem_ld_wait();
-        if (c == 7) {
+        if (c == 3) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(&tempty_bar[buf]);
