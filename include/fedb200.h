@@ -46,6 +46,13 @@ int fb_fedagg_step_f32(const float* const* d_client_w, const int64_t* n_k, int n
                        int deterministic, const float* d_w, const float* d_m, float* d_w_out,
                        float* d_m_out, int64_t n, double eta, double mu, int nesterov,
                        double* d_stats, int64_t* d_first_bad, double* d_pg_out, void* stream);
+/* Same fused step plus the round telemetry of compute_round_norms (fedforge/metrics.py:177-215)
+ * as side reductions of the same HBM pass: d_stats[6 + K] = |pg|^2, |w'|^2, |m'|^2, |w|^2,
+ * |sum p_k w_k|^2, |w - sum p_k w_k|^2, then |w_k|^2 per client (p_k = n_k / sum n). */
+int fb_fedagg_round_norms_f32(const float* const* d_client_w, const int64_t* n_k, int n_clients,
+                              int deterministic, const float* d_w, const float* d_m, float* d_w_out,
+                              float* d_m_out, int64_t n, double eta, double mu, int nesterov,
+                              double* d_stats, int64_t* d_first_bad, void* stream);
 /* Same contract for reference-format f64 deltas (ClientUpdate.delta, fedopt.py:26-46). */
 int fb_fedagg_step_f64delta(const double* const* d_deltas, const int64_t* n_k, int n_clients,
                             int deterministic, const float* d_w, const float* d_m, float* d_w_out,

@@ -24,7 +24,12 @@ template <typename TIn>
 struct AggParams {
   const TIn* src[FB_MAX_CLIENTS];
   double nk[FB_MAX_CLIENTS];
+  double pk[FB_MAX_CLIENTS];  // n_k / sum n (f64), for the round-norm telemetry
 };
+
+// stats layout (f64): 0 |pg|^2, 1 |w'|^2, 2 |m'|^2, 3 |w|^2, 4 |sum p_k w_k|^2, 5 |w - sum p_k w_k|^2,
+// 6 + k: |w_k|^2 (only with per-client norms)  -- compute_round_norms, fedforge/metrics.py:177-215
+constexpr int kStatsFixed = 6;
 
 // binary-counter stack of partial sums; D = floor(log2(K)) + 1 levels suffice
 template <int kStack>
@@ -92,8 +97,8 @@ __device__ __forceinline__ StepOut outer_step(float w32, float m32, double pg, d
   return o;
 }
 
-template <typename TIn, int VEC, int D>
-__global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, int deterministic,
+template <typename TIn, int VEC, int D, int STATS>
+__global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K, int deterministic,
                                                      double inv_total_unused, double total,
                                                      const float* __restrict__ w,
                                                      const float* __restrict__ m,
@@ -101,9 +106,14 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
                                                      float* __restrict__ m_out, int64_t n,
                                                      double eta, double mu, int nesterov,
                                                      double* stats, unsigned long long* first_bad,
-                                                     double* __restrict__ pg_out) {
-  __shared__ double red[3][8];
-  double s_pg = 0.0, s_w = 0.0, s_m = 0.0;
+                                                     double* __restrict__ pg_out, int client_norms) {
+  __shared__ double red[kStatsFixed + FB_MAX_CLIENTS][8];
+  double s_pg = 0.0, s_w = 0.0, s_m = 0.0, s_w0 = 0.0, s_avg = 0.0, s_dif = 0.0;
+  const int lane_ = threadIdx.x & 31, wid_ = threadIdx.x >> 5;
+  if (client_norms) {
+    for (int i = threadIdx.x; i < FB_MAX_CLIENTS * 8; i += blockDim.x) red[kStatsFixed + i / 8][i % 8] = 0.0;
+    __syncthreads();
+  }
   unsigned long long bad = ~0ull;
   const int64_t nvec = n / VEC;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
@@ -127,9 +137,9 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
       // all client loads of a batch are issued before any f64 math (8 vector loads in flight)
       constexpr int KB = 8;
       TreeAcc<D> acc[VEC];
-      double sum[VEC];
+      double sum[VEC], avg[VEC];
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) sum[e] = 0.0;
+      for (int e = 0; e < VEC; ++e) { sum[e] = 0.0; avg[e] = 0.0; }
       for (int k0 = 0; k0 < K; k0 += KB) {
         float c[KB][VEC];
 #pragma unroll
@@ -150,6 +160,18 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
           if (k0 + j < K) {
             const int k = k0 + j;
             const float* cv = c[j];
+            if (STATS) {
+              double ck = 0.0;
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) {
+                avg[e] += P.pk[k] * (double)cv[e];
+                ck += (double)cv[e] * (double)cv[e];
+              }
+              if (client_norms) {
+                ck = warp_sum(ck);
+                if (lane_ == 0) red[kStatsFixed + k][wid_] += ck;
+              }
+            }
 #pragma unroll
             for (int e = 0; e < VEC; ++e) {
               const double dk = __dsub_rn((double)wv[e], (double)cv[e]);
@@ -165,8 +187,15 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
         }
       }
 #pragma unroll
-      for (int e = 0; e < VEC; ++e)
+      for (int e = 0; e < VEC; ++e) {
         pg[e] = (K == 1) ? sum[e] : __ddiv_rn(deterministic ? acc[e].result(K) : sum[e], total);
+        if (STATS) {
+          const double w0 = (double)wv[e];
+          s_w0 += w0 * w0;
+          s_avg += avg[e] * avg[e];
+          s_dif += (w0 - avg[e]) * (w0 - avg[e]);
+        }
+      }
     } else if (K == 1) {
 #pragma unroll
       for (int e = 0; e < VEC; ++e) pg[e] = delta_of<TIn>(P.src[0], j0 + e, (double)wv[e]);
@@ -194,16 +223,24 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
 #pragma unroll
       for (int e = 0; e < VEC; ++e) pg_out[j0 + e] = pg[e];
     }
-    if (!w_out) continue;
+    if (!w_out) {
+      if (STATS) {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) s_pg += pg[e] * pg[e];
+      }
+      continue;
+    }
     float wo[VEC], mo[VEC];
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
       StepOut o = outer_step(wv[e], mv[e], pg[e], eta, mu, nesterov);
       wo[e] = o.w;
       mo[e] = o.m;
-      s_pg += pg[e] * pg[e];
-      s_w += (double)o.w * (double)o.w;
-      s_m += (double)o.m * (double)o.m;
+      if (STATS) {
+        s_pg += pg[e] * pg[e];
+        s_w += (double)o.w * (double)o.w;
+        s_m += (double)o.m * (double)o.m;
+      }
       if (!(isfinite(o.w) && isfinite(o.m)) && (unsigned long long)(j0 + e) < bad)
         bad = (unsigned long long)(j0 + e);
     }
@@ -236,6 +273,17 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
     }
     if (pg_out) pg_out[j] = pgv;
     s_pg += pgv * pgv;
+    if (STATS && sizeof(TIn) == 4) {
+      double avg = 0.0;
+      for (int k = 0; k < K; ++k) {
+        const double ck = (double)reinterpret_cast<const float*>(P.src[k])[j];
+        avg += P.pk[k] * ck;
+        if (client_norms) atomicAdd(&red[kStatsFixed + k][wid_], ck * ck);
+      }
+      s_w0 += wg * wg;
+      s_avg += avg * avg;
+      s_dif += (wg - avg) * (wg - avg);
+    }
     if (w_out) {
       StepOut o = outer_step(w[j], m[j], pgv, eta, mu, nesterov);
       w_out[j] = o.w;
@@ -253,17 +301,19 @@ __global__ void __launch_bounds__(256) fedagg_kernel(AggParams<TIn> P, int K, in
     }
     if ((threadIdx.x & 31) == 0 && bad != ~0ull) atomicMin(first_bad, bad);
   }
-  if (stats) {
-    s_pg = warp_sum(s_pg);
-    s_w = warp_sum(s_w);
-    s_m = warp_sum(s_m);
-    int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (lane == 0) { red[0][wid] = s_pg; red[1][wid] = s_w; red[2][wid] = s_m; }
+  if (STATS && stats) {
+    double v[kStatsFixed] = {s_pg, s_w, s_m, s_w0, s_avg, s_dif};
+#pragma unroll
+    for (int i = 0; i < kStatsFixed; ++i) {
+      v[i] = warp_sum(v[i]);
+      if (lane_ == 0) red[i][wid_] = v[i];
+    }
     __syncthreads();
-    if (threadIdx.x < 3) {
+    const int nstat = kStatsFixed + (client_norms ? K : 0);
+    for (int i = threadIdx.x; i < nstat; i += blockDim.x) {
       double t = 0.0;
-      for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[threadIdx.x][i];
-      atomicAdd(stats + threadIdx.x, t);
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[i][w];
+      atomicAdd(stats + i, t);
     }
   }
 }
@@ -272,7 +322,7 @@ template <typename TIn>
 static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int deterministic,
                          const float* w, const float* m, float* w_out, float* m_out, int64_t n,
                          double eta, double mu, int nesterov, double* stats, int64_t* first_bad,
-                         double* pg_out, cudaStream_t st) {
+                         double* pg_out, int stats_mode, cudaStream_t st) {
   FB_REQUIRE(K >= 1 && K <= FB_MAX_CLIENTS, "n_clients=%d outside [1, %d]", K, FB_MAX_CLIENTS);
   FB_REQUIRE(n > 0, "model length must be positive, got %lld", (long long)n);
   FB_REQUIRE(eta > 0.0, "server eta must be > 0, got %g", eta);
@@ -281,7 +331,7 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
   double total = 0.0;
   int64_t itotal = 0;
   FB_REQUIRE((w_out == nullptr) == (m_out == nullptr), "w_out and m_out must both be set or both NULL");
-  FB_REQUIRE(w_out || pg_out, "nothing to compute");
+  FB_REQUIRE(w_out || pg_out || stats, "nothing to compute");
   bool aligned = ((uintptr_t)w % 16 == 0) && ((uintptr_t)m % 16 == 0) && ((uintptr_t)w_out % 16 == 0) &&
                  ((uintptr_t)m_out % 16 == 0) && ((uintptr_t)pg_out % 8 == 0);
   for (int k = 0; k < K; ++k) {
@@ -290,10 +340,13 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
     P.src[k] = src[k];
     P.nk[k] = (double)n_k[k];
     itotal += n_k[k];
+    P.pk[k] = 0.0;
     aligned = aligned && ((uintptr_t)src[k] % 16 == 0);
   }
   total = (double)itotal;
-  if (stats) FB_CUDA_TRY(cudaMemsetAsync(stats, 0, 3 * sizeof(double), st));
+  for (int k = 0; k < K; ++k) P.pk[k] = (double)n_k[k] / total;
+  const int client_norms = (stats_mode & 2) ? 1 : 0;
+  if (stats) FB_CUDA_TRY(cudaMemsetAsync(stats, 0, (kStatsFixed + (client_norms ? K : 0)) * sizeof(double), st));
   if (first_bad) FB_CUDA_TRY(cudaMemsetAsync(first_bad, 0x7f, sizeof(int64_t), st));
   const int threads = 256;
   const int depth = K <= 1 ? 1 : K <= 3 ? 2 : K <= 7 ? 3 : K <= 15 ? 4 : K <= 31 ? 5 : K <= 63 ? 6 : 7;
@@ -301,9 +354,16 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
   do {                                                                                                   \
     int64_t work = (n / VEC_ + threads - 1) / threads;                                                   \
     int blocks = (int)(work < kNumSMs * 8 ? (work > 0 ? work : 1) : kNumSMs * 8);                        \
-    fedagg_kernel<TIn, VEC_, D_><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, \
+    if (stats)                                                                                           \
+      fedagg_kernel<TIn, VEC_, D_, 1><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, \
+                                                               m_out, n, eta, mu, nesterov, stats,         \
+                                                               (unsigned long long*)first_bad, pg_out,     \
+                                                               client_norms);                              \
+    else                                                                                                 \
+    fedagg_kernel<TIn, VEC_, D_, 0><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, \
                                                              m_out, n, eta, mu, nesterov, stats,         \
-                                                             (unsigned long long*)first_bad, pg_out);    \
+                                                             (unsigned long long*)first_bad, pg_out,     \
+                                                             client_norms);                              \
   } while (0)
   if (aligned && sizeof(TIn) == 4) {
     switch (depth) {
@@ -328,7 +388,16 @@ extern "C" int fb_fedagg_step_f32(const float* const* d_client_w, const int64_t*
                                   double* d_stats, int64_t* d_first_bad, double* d_pg_out,
                                   void* stream) {
   return fb::launch_fedagg<float>(d_client_w, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n,
-                                  eta, mu, nesterov, d_stats, d_first_bad, d_pg_out, (cudaStream_t)stream);
+                                  eta, mu, nesterov, d_stats, d_first_bad, d_pg_out, 1, (cudaStream_t)stream);
+}
+
+extern "C" int fb_fedagg_round_norms_f32(const float* const* d_client_w, const int64_t* n_k, int n_clients,
+                                         int deterministic, const float* d_w, const float* d_m, float* d_w_out,
+                                         float* d_m_out, int64_t n, double eta, double mu, int nesterov,
+                                         double* d_stats, int64_t* d_first_bad, void* stream) {
+  FB_REQUIRE(d_stats != nullptr, "fb_fedagg_round_norms_f32 needs d_stats (6 + K doubles)");
+  return fb::launch_fedagg<float>(d_client_w, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n, eta, mu,
+                                  nesterov, d_stats, d_first_bad, nullptr, 3, (cudaStream_t)stream);
 }
 
 extern "C" int fb_fedagg_step_f64delta(const double* const* d_deltas, const int64_t* n_k, int n_clients,
@@ -337,5 +406,5 @@ extern "C" int fb_fedagg_step_f64delta(const double* const* d_deltas, const int6
                                        double* d_stats, int64_t* d_first_bad, double* d_pg_out,
                                        void* stream) {
   return fb::launch_fedagg<double>(d_deltas, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n,
-                                   eta, mu, nesterov, d_stats, d_first_bad, d_pg_out, (cudaStream_t)stream);
+                                   eta, mu, nesterov, d_stats, d_first_bad, d_pg_out, 1, (cudaStream_t)stream);
 }

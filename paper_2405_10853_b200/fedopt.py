@@ -337,3 +337,32 @@ def server_step(opt: ServerOptState, w_prev, delta, round_num: Optional[int] = N
         return DeviceVector(w_out), replace(opt, momentum=DeviceVector(m_out))
     return (ParamVector(w_out.cpu().numpy(), check=False),
             replace(opt, momentum=ParamVector(m_out.cpu().numpy(), check=False)))
+
+
+def server_step_with_norms(opt: ServerOptState, w_prev, agg: AggregatorState, round_num: Optional[int] = None):
+    """Fast path of FederatedRuntime._run_round (cluster.py:511-520): finalize + server_step +
+    compute_round_norms in ONE pass over HBM. Returns (w', opt', RoundNorms)."""
+    from .telemetry import norms_from_stats
+    t = _torch()
+    ext.lib()
+    n = len(w_prev)
+    kind, srcs, w_ref = agg._sources()
+    if kind != "f32":
+        raise ParamError("server_step_with_norms needs device-resident client updates sharing one global")
+    w = _dev(w_prev)
+    m = _dev(opt.momentum)
+    w_out, m_out = t.empty_like(w), t.empty_like(m)
+    ups = agg._ordered()
+    stats = t.zeros(6 + len(ups), dtype=t.float64, device=w.device)
+    bad = t.empty(1, dtype=t.int64, device=w.device)
+    ptrs = (C.c_void_p * len(srcs))(*[s_.data_ptr() for s_ in srcs])
+    nks = (C.c_int64 * len(ups))(*[u.n_k for u in ups])
+    ext.call("fb_fedagg_round_norms_f32", ptrs, nks, len(ups), int(agg.deterministic), w.data_ptr(), m.data_ptr(),
+             w_out.data_ptr(), m_out.data_ptr(), n, float(opt.eta), float(opt.mu), int(opt.nesterov),
+             stats.data_ptr(), bad.data_ptr(), ext.stream_handle())
+    st = stats.cpu().numpy()
+    if int(bad.item()) < n:
+        where = f" in round {round_num}" if round_num is not None else ""
+        raise ParamError(f"non-finite global model after server step{where}")
+    norms = norms_from_stats(st, [u.client_id for u in ups], float(np.sqrt(st[2])))
+    return DeviceVector(w_out), replace(opt, momentum=DeviceVector(m_out)), norms

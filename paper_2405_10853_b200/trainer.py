@@ -151,3 +151,39 @@ def train_round(params, batches: BatchIterator, evaluator: LossEvaluator, adamw_
             step_hook(s)
         sess.step(s)
     return sess.finish()
+
+
+def evaluate_mean_ce(evaluator: LossEvaluator, params, corpus, indices: np.ndarray, batch_size: int,
+                     max_batches: int) -> float:
+    """Server validation (trainer.py:117-135): mean next-token CE over a fixed prefix of the
+    validation set, forward-only on the GPU (one upload of params, batches gathered on device)."""
+    import torch
+    if indices.size == 0:
+        raise ParamError("validation set is empty")
+    ext.lib()
+    w = params.tensor if isinstance(params, DeviceVector) else evaluator._upload(params)
+    shadow, _, _, _ = evaluator.buffers()
+    st = ext.stream_handle()
+    ext.call("fb_cast_bf16", w.data_ptr(), shadow.data_ptr(), w.numel(), st)
+    T = corpus.sequence_len
+    check_gpu_shape(evaluator.cfg, T)
+    dc = DeviceCorpus(corpus, evaluator.device) if not isinstance(corpus, DeviceCorpus) else corpus
+    n = min(indices.size, batch_size * max_batches)
+    order = torch.from_numpy(np.ascontiguousarray(indices[:n], dtype=np.int64)).to(evaluator.device)
+    total, count = 0.0, 0
+    sums = []
+    for start in range(0, n, batch_size):
+        rows = min(batch_size, n - start)
+        ws = evaluator.workspace(rows, T, extra=rows * T * 4 + 512)
+        need = int(ext.lib().fb_model_workspace_bytes(C.byref(evaluator._mcfg), rows, T))
+        tok = ws[((need + 255) // 256) * 256:].view(torch.int32)
+        ext.call("fb_gather_batch", dc.tokens.data_ptr(), order[start:].data_ptr(), rows, 0, rows, T,
+                 tok.data_ptr(), st)
+        rl = torch.empty(rows * T, dtype=torch.float64, device=evaluator.device)
+        ext.call("fb_model_fwd_bwd", C.byref(evaluator._mcfg), w.data_ptr(), shadow.data_ptr(), None, tok.data_ptr(),
+                 rows, T, 1.0, rl.data_ptr(), 0, ws.data_ptr(), need, st)
+        sums.append((rl.sum() / (rows * (T - 1)), rows))
+    for mean_t, rows in sums:  # one sync at the end
+        total += float(mean_t.item()) * rows
+        count += rows
+    return total / count

@@ -202,8 +202,30 @@ def gen_c1():
                         mean_losses=np.array(mean_losses), w_norm=l2_norm(w))
 
 
+def gen_norms_eval():
+    """compute_round_norms (metrics.py:177-215) and evaluate_mean_ce (trainer.py:117-135)."""
+    from fedforge.metrics import compute_round_norms
+    g = np.load(os.path.join(OUT, "agg.npz"))
+    w, m, wk, nk = g["k8_w"], g["k8_m"], g["k8_wk"], g["k8_nk"]
+    deltas = [w.astype(np.float64) - wk[k].astype(np.float64) for k in range(8)]
+    weights = [int(n) / int(nk.sum()) for n in nk]
+    mom = g["k8_det_0.7_0.9_1_m"]
+    rn = compute_round_norms(ParamVector(w), deltas, weights, ParamVector(mom), list(range(8)))
+    cfg = rmodel.TinyLMConfig(vocab_size=256, context_len=128, n_layers=1, d_model=128, n_heads=2, seed=21)
+    ev = rmodel.LossEvaluator(cfg)
+    rng = np.random.default_rng(3)
+    params = (ev.init_params().data + rng.normal(0, 0.05, ev.n_params).astype(np.float32)).astype(np.float32)
+    corpus = rdata.tokenize_bytes(rdata.synth_corpus(99, 60_000, "markov"), 128, 256)
+    split = rdata.split_corpus(corpus, 2, 99, 0.1)
+    ce = rtrain.evaluate_mean_ce(ev, ParamVector(params), corpus, split.validation, 8, 3)
+    np.savez_compressed(os.path.join(OUT, "norms_eval.npz"), global_norm=rn.global_norm,
+                        per_client=np.array([rn.per_client_norms[k] for k in range(8)]),
+                        avg_client_norm=rn.avg_client_norm, momentum_norm=rn.momentum_norm,
+                        pseudograd_norm=rn.pseudograd_norm, eval_params=params, eval_ce=ce)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["agg", "adamw", "sched", "data", "model", "round", "c1"]
+    which = sys.argv[1:] or ["agg", "adamw", "sched", "data", "model", "round", "c1", "norms_eval"]
     for name in which:
         globals()["gen_" + name]()
         print("wrote", name)
