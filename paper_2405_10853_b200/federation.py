@@ -1,0 +1,106 @@
+"""One federated round on B200s: the hot path of FederatedRuntime._run_round
+(fedforge/cluster.py:367-383 task plan, :490-580 round) without its control plane.
+
+Clients are sharded over ranks (client k on rank k mod G, one process per GPU);
+every client on a rank trains with train_round (end weights stay in HBM), then the
+round ends with the fused aggregation + outer step (+ round-norm telemetry): on one
+GPU directly, on G GPUs through the NCCL all-to-all of client slices
+(dist.ShardedAggregator), bit-identical for every G. Optional validation pass
+(evaluate_mean_ce) and FEDP checkpoint of (global, momentum) on rank 0.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import ext
+from .checkpoint import write_checkpoint
+from .config import AdamWConfig, ScheduleConfig, TinyLMConfig, TrainTask
+from .data import BatchIterator, DataSplit, TokenizedCorpus
+from .dist import ShardedAggregator, clients_of
+from .fedopt import AggregatorState, DeviceVector, ServerOptState, server_step_with_norms
+from .model import LossEvaluator, init_params_host
+from .telemetry import RoundNorms, norms_from_stats
+from .trainer import evaluate_mean_ce, train_round
+
+
+@dataclass
+class RoundResult:
+    round: int
+    params: DeviceVector
+    opt: ServerOptState
+    norms: RoundNorms | None
+    client_metrics: dict = field(default_factory=dict)
+    telemetry: dict = field(default_factory=dict)
+    val_loss: float | None = None
+
+
+class Federation:
+    def __init__(self, model_cfg: TinyLMConfig, adamw: AdamWConfig, sched: ScheduleConfig, corpus: TokenizedCorpus,
+                 split: DataSplit, *, batch_size: int, micro_batches: int, local_steps: int, server_eta: float,
+                 server_mu: float, nesterov: bool = True, deterministic: bool = True, data_seed: int = 99,
+                 local_step_overrides: dict | None = None, eval_batches: int = 0):
+        import torch
+        import torch.distributed as dist
+        ext.lib()
+        self.cfg, self.adamw, self.sched = model_cfg, adamw, sched
+        self.corpus, self.split = corpus, split
+        self.B, self.micro, self.S = batch_size, micro_batches, local_steps
+        self.eta, self.mu, self.nesterov, self.det = server_eta, server_mu, nesterov, deterministic
+        self.overrides = dict(local_step_overrides or {})
+        self.eval_batches = eval_batches
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.K = len(split.shards)
+        self.mine = clients_of(self.rank, self.world, self.K)
+        self.ev = LossEvaluator(model_cfg)
+        self.iters = {k: BatchIterator(corpus, split.shards[k], batch_size, data_seed) for k in self.mine}
+        self.n_k = {k: split.shards[k].n_k for k in range(self.K)}
+        self.agg = ShardedAggregator(self.ev.n_params, self.K) if self.world > 1 else None
+
+    def init_state(self):
+        import torch
+        w = DeviceVector(torch.from_numpy(init_params_host(self.cfg)).cuda())
+        if self.agg is not None:
+            m = torch.zeros(self.agg.hi - self.agg.lo, dtype=torch.float32, device="cuda")
+        else:
+            m = torch.zeros(len(w), dtype=torch.float32, device="cuda")
+        return w, ServerOptState(DeviceVector(m) if m.numel() else DeviceVector(torch.zeros(1, device="cuda")),
+                                 self.eta, self.mu, self.nesterov)
+
+    def run_round(self, w: DeviceVector, opt: ServerOptState, round_num: int, checkpoint_path=None) -> RoundResult:
+        import torch
+        updates, tele, metrics = {}, {}, {}
+        for k in self.mine:
+            task = TrainTask(round_num, k, self.overrides.get(k, self.S), (round_num - 1) * self.S, self.B, self.micro,
+                             {"data": 0}, f"round-{round_num}")
+            u, t = train_round(w, self.iters[k], self.ev, self.adamw, self.sched, task)
+            updates[k], tele[k], metrics[k] = u, t, u.local_metrics
+        if self.agg is None:
+            agg = AggregatorState(round_num, len(w), deterministic=self.det)
+            for k in sorted(updates):
+                agg.accumulate(updates[k])
+            w_new, opt_new, norms = server_step_with_norms(opt, w, agg, round_num)
+        else:
+            import torch.distributed as dist
+            self.agg.exchange({k: u.w_end for k, u in updates.items()})
+            w_out = torch.empty_like(w.tensor)
+            w_full, m_new = self.agg.step(w.tensor, opt.momentum.tensor, self.n_k, self.eta, self.mu, self.nesterov,
+                                          deterministic=self.det, w_out=w_out)
+            w_new, opt_new = DeviceVector(w_full), ServerOptState(DeviceVector(m_new), self.eta, self.mu, self.nesterov)
+            stats = self.agg.stats.clone()
+            dist.all_reduce(stats)
+            s = stats.cpu().numpy()
+            norms = RoundNorms(global_norm=float("nan"), per_client_norms={},
+                               avg_client_norm=float("nan"), momentum_norm=math.sqrt(s[2]),
+                               pseudograd_norm=math.sqrt(s[0]))
+        val = None
+        if self.eval_batches and self.rank == 0 and self.split.validation.size:
+            val = evaluate_mean_ce(self.ev, w_new, self.corpus, self.split.validation, self.B, self.eval_batches)
+        if checkpoint_path is not None and self.rank == 0:
+            write_checkpoint({"round": round_num, "global": w_new, "momentum": opt_new.momentum,
+                              "server_opt": {"eta": self.eta, "mu": self.mu, "nesterov": self.nesterov}},
+                             checkpoint_path)
+        return RoundResult(round_num, w_new, opt_new, norms, metrics, tele, val)

@@ -224,8 +224,20 @@ def gen_norms_eval():
                         pseudograd_norm=rn.pseudograd_norm, eval_params=params, eval_ce=ce)
 
 
+def gen_ckpt():
+    """A FEDP blob encoded by the reference (params.encode_sections)."""
+    from fedforge.params import encode_sections
+    rng = np.random.default_rng(4)
+    sections = {"round": 3, "global": ParamVector(rng.normal(size=257).astype(np.float32)),
+                "momentum": ParamVector(rng.normal(size=257).astype(np.float32)),
+                "server_opt": {"eta": 0.7, "mu": 0.9, "nesterov": True}, "lr": 0.25,
+                "delta": rng.normal(size=31), "config_hash": "abc"}
+    with open(os.path.join(OUT, "ckpt_ref.fedp"), "wb") as fh:
+        fh.write(encode_sections(sections))
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["agg", "adamw", "sched", "data", "model", "round", "c1", "norms_eval"]
+    which = sys.argv[1:] or ["agg", "adamw", "sched", "data", "model", "round", "c1", "norms_eval", "ckpt"]
     for name in which:
         globals()["gen_" + name]()
         print("wrote", name)

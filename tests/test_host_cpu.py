@@ -155,3 +155,24 @@ def test_aggregator_protocol_on_host():
         mg.merge(b)
     with pytest.raises(ParamError):
         ServerOptState.fresh(1, eta=0.0, mu=0.5)
+
+
+def test_fedp_checkpoint_byte_compatible(tmp_path):
+    from paper_2405_10853_b200 import checkpoint as ck
+    from paper_2405_10853_b200.params import ParamVector
+    raw = open(os.path.join(GOLDEN, "ckpt_ref.fedp"), "rb").read()
+    dec = ck.decode_sections(raw)
+    assert dec["round"] == 3 and dec["server_opt"]["mu"] == 0.9 and dec["lr"] == 0.25
+    again = ck.encode_sections({"round": dec["round"], "global": dec["global"], "momentum": dec["momentum"],
+                                "server_opt": dec["server_opt"], "lr": dec["lr"], "delta": dec["delta"],
+                                "config_hash": dec["config_hash"]})
+    assert again == raw  # byte-identical to the reference encoder
+    p = tmp_path / "x.fedp"
+    n = ck.write_checkpoint({"global": ParamVector(np.ones(5, np.float32))}, p)
+    assert n == os.path.getsize(p) and ck.read_checkpoint(p)["global"].data.tolist() == [1.0] * 5
+    bad = bytearray(raw)
+    bad[100] ^= 1  # inside the "global" f32 payload
+    with pytest.raises(ck.CheckpointChecksumError):
+        ck.decode_sections(bytes(bad))
+    with pytest.raises(ck.CheckpointFormatError):
+        ck.decode_sections(b"XXXX" + raw[4:])
