@@ -53,7 +53,7 @@ struct AttnBwdCfg {
 template <int DH>
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_tc_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                       const float* __restrict__ lse2, const float* __restrict__ Dd, float* __restrict__ dq_acc,
+                       const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2, const float* __restrict__ Dd, float* __restrict__ dq_acc,
                        __nv_bfloat16* __restrict__ dqkv, int T, int H, float scale_log2, float scale, int use_alibi) {
   using Cf = AttnBwdCfg<DH>;
   extern __shared__ uint8_t smem_raw[];
@@ -258,22 +258,43 @@ __global__ void __launch_bounds__(320, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
-      // drain this warpgroup's half of dQ (thread = query row r of this tile)
+      // drain this warpgroup's half of dQ (thread = query row r of this tile): TMEM -> 128B-swizzled
+      // smem (the P/dS tile is free once dQ_t has completed) -> TMA bulk reduce-add into the f32 dq
+      // accumulator, one 128 x 32 box per chunk (replaces per-thread red.global traffic).
       mbar_wait(dq_full, ph);
       tc_fence_after();
-      float* dqrow = dq_acc + ((int64_t)row0 + q0 + r) * d + h * DH + (DH / 2) * g;
+      const uint32_t stage = sPS + g * 16384;
 #pragma unroll 1
       for (int c = 0; c < DH / 64; ++c) {
         uint32_t v[32];
         tmem_ld_32x32b_x32(tQ + c * 32, v);
         tmem_ld_wait();
-#ifndef FB_ABLATE_DQ
+        if (c > 0) {  // the previous box must have been read out of smem
+          if (quad == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
+        }
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          red_add_v4(dqrow + c * 32 + 4 * q, __uint_as_float(v[4 * q]) * scale, __uint_as_float(v[4 * q + 1]) * scale,
-                     __uint_as_float(v[4 * q + 2]) * scale, __uint_as_float(v[4 * q + 3]) * scale);
-#endif
+        for (int q = 0; q < 8; ++q) {
+          const uint32_t addr = stage + r * 128 + ((q ^ (r & 7)) << 4);
+          asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(__uint_as_float(v[4 * q]) * scale),
+                       "f"(__uint_as_float(v[4 * q + 1]) * scale), "f"(__uint_as_float(v[4 * q + 2]) * scale),
+                       "f"(__uint_as_float(v[4 * q + 3]) * scale));
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
+        if (quad == 0 && lane == 0) {
+          asm volatile(
+              "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                  reinterpret_cast<uint64_t>(&tm_dq)),
+              "r"(stage), "r"(h * DH + (DH / 2) * g + c * 32), "r"(row0 + q0)
+              : "memory");
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
       }
+      // the P/dS tile is reused by the next tile's P: wait until TMA has read the staging box
+      if (quad == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // both staging halves drained before any next-tile P write
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
@@ -346,10 +367,24 @@ int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const 
   if (rc) return rc;
   rc = encode_rows_map(&to, dO, (int64_t)B * T, d, DH / 64);
   if (rc) return rc;
+  CUtensorMap tdq;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)B * T};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 4};
+    cuuint32_t box[2] = {32, 128};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_enc_bwd(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("attn bwd dq tensor map encode failed: %d", (int)r);
+      return FB_CUDA_ERROR;
+    }
+  }
   auto k = attn_bwd_tc_kernel<DH>;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale = 1.0f / sqrtf((float)DH);
-  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tq, to, lse, Dbuf, dq, (__nv_bfloat16*)dqkv, T, H,
+  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tq, to, tdq, lse, Dbuf, dq, (__nv_bfloat16*)dqkv, T, H,
                                                  1.4426950408889634f * scale, scale, use_alibi);
   FB_LAUNCH_CHECK();
   return FB_OK;

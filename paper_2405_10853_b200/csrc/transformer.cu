@@ -46,41 +46,84 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const float* _
 }
 
 // ------------------------------------------------------------------ LayerNorm
-template <int NJ>
+// One 256-thread CTA per row at a time (grid-stride); thread t owns VPT consecutive columns
+// (128-bit loads/stores when VPT % 4 == 0). Two-pass mean / variance in registers.
+template <int VPT>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
                                                      const float* __restrict__ beta, __nv_bfloat16* __restrict__ y,
                                                      float* __restrict__ mean_out, float* __restrict__ rstd_out,
                                                      int rows, int d) {
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (row >= rows) return;
-  const float* xr = x + (int64_t)row * d;
-  float v[NJ];
-  float s = 0.f;
+  __shared__ float red[2][8];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int c0 = tid * VPT;
+  const bool vec = (VPT % 4 == 0) && (d % 4 == 0);
+  float gm[VPT], bt[VPT];
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const int c = lane + 32 * j;
-    v[j] = c < d ? xr[c] : 0.f;
-    s += v[j];
+  for (int j = 0; j < VPT; ++j) {
+    gm[j] = c0 + j < d ? gamma[c0 + j] : 0.f;
+    bt[j] = c0 + j < d ? beta[c0 + j] : 0.f;
   }
-  const float mean = warp_sum(s) / d;
-  float q = 0.f;
+  const float inv_d = 1.0f / d;
+  for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int64_t base = (int64_t)row * d + c0;
+    float v[VPT];
+    if (vec && c0 < d) {
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const int c = lane + 32 * j;
-    const float t = c < d ? v[j] - mean : 0.f;
-    q += t * t;
-  }
-  const float rstd = rsqrtf(warp_sum(q) / d + 1e-5f);
-  __nv_bfloat16* yr = y + (int64_t)row * d;
+      for (int j = 0; j < VPT; j += 4) {
+        const float4 a = *reinterpret_cast<const float4*>(x + base + j);
+        v[j] = a.x; v[j + 1] = a.y; v[j + 2] = a.z; v[j + 3] = a.w;
+      }
+    } else {
 #pragma unroll
-  for (int j = 0; j < NJ; ++j) {
-    const int c = lane + 32 * j;
-    if (c < d) yr[c] = __float2bfloat16_rn((v[j] - mean) * rstd * gamma[c] + beta[c]);
-  }
-  if (lane == 0) {
-    mean_out[row] = mean;
-    rstd_out[row] = rstd;
+      for (int j = 0; j < VPT; ++j) v[j] = c0 + j < d ? x[base + j] : 0.f;
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) s += v[j];
+    s = warp_sum(s);
+    if (lane == 0) red[0][wid] = s;
+    __syncthreads();
+    float mean = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) mean += red[0][i];
+    mean *= inv_d;
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const float t = c0 + j < d ? v[j] - mean : 0.f;
+      q += t * t;
+    }
+    q = warp_sum(q);
+    if (lane == 0) red[1][wid] = q;
+    __syncthreads();
+    float var = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) var += red[1][i];
+    const float rstd = rsqrtf(var * inv_d + 1e-5f);
+    if (tid == 0) {
+      mean_out[row] = mean;
+      rstd_out[row] = rstd;
+    }
+    if (vec && c0 < d) {
+#pragma unroll
+      for (int j = 0; j < VPT; j += 8) {
+        uint4 pk;
+        pk.x = pack_bf16((v[j] - mean) * rstd * gm[j] + bt[j], (v[j + 1] - mean) * rstd * gm[j + 1] + bt[j + 1]);
+        pk.y = pack_bf16((v[j + 2] - mean) * rstd * gm[j + 2] + bt[j + 2], (v[j + 3] - mean) * rstd * gm[j + 3] + bt[j + 3]);
+        if (j + 4 < VPT) {
+          pk.z = pack_bf16((v[j + 4] - mean) * rstd * gm[j + 4] + bt[j + 4], (v[j + 5] - mean) * rstd * gm[j + 5] + bt[j + 5]);
+          pk.w = pack_bf16((v[j + 6] - mean) * rstd * gm[j + 6] + bt[j + 6], (v[j + 7] - mean) * rstd * gm[j + 7] + bt[j + 7]);
+          *reinterpret_cast<uint4*>(y + base + j) = pk;
+        } else {
+          *reinterpret_cast<uint2*>(y + base + j) = make_uint2(pk.x, pk.y);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < VPT; ++j)
+        if (c0 + j < d) y[base + j] = __float2bfloat16_rn((v[j] - mean) * rstd * gm[j] + bt[j]);
+    }
+    __syncthreads();  // red[] reuse by the next row
   }
 }
 
@@ -218,42 +261,78 @@ constexpr int kLnBwdBlocks = 592;  // 148 SMs x 4
 
 // ------------------------------------------------------------------ cross-entropy
 // One CTA (256 threads) per logits row. Row r of the chunk is position t = (row0+r) % T.
+// Pass 1: online max / sum-exp with 128-bit loads; pass 2 (row is L2-resident): bf16 dlogits.
 __global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logits, const int32_t* __restrict__ tok,
                                                  __nv_bfloat16* __restrict__ dlogits, int row0, int T, int V,
                                                  float scale, double* __restrict__ row_loss) {
-  __shared__ float red[8];
+  __shared__ float red_m[8], red_s[8];
   const int r = blockIdx.x;
   const int grow = row0 + r;
   const int t = grow % T;
   const float* lr = logits + (int64_t)r * V;
   __nv_bfloat16* dr = dlogits + (int64_t)r * V;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const bool vec = (V % 8 == 0);
   if (t == T - 1) {  // last position: not scored (logits[:, :-1])
-    for (int c = threadIdx.x; c < V; c += blockDim.x) dr[c] = __float2bfloat16_rn(0.f);
+    if (vec) {
+      for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) *reinterpret_cast<uint4*>(dr + c) = make_uint4(0, 0, 0, 0);
+    } else {
+      for (int c = threadIdx.x; c < V; c += blockDim.x) dr[c] = __float2bfloat16_rn(0.f);
+    }
     if (threadIdx.x == 0) row_loss[grow] = 0.0;
     return;
   }
   const int target = tok[grow + 1];
-  float mx = -INFINITY;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) mx = fmaxf(mx, lr[c]);
-  mx = warp_max(mx);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  float m = -INFINITY, s = 0.f;
+  auto upd = [&](float x) {
+    if (x > m) { s = s * __expf(m - x) + 1.f; m = x; }
+    else s += __expf(x - m);
+  };
+  if (vec) {
+    for (int c = threadIdx.x * 4; c < V; c += blockDim.x * 4) {
+      const float4 a = *reinterpret_cast<const float4*>(lr + c);
+      upd(a.x); upd(a.y); upd(a.z); upd(a.w);
+    }
+  } else {
+    for (int c = threadIdx.x; c < V; c += blockDim.x) upd(lr[c]);
+  }
+  // combine (m, s) pairs: warp then CTA
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    const float mn = fmaxf(m, m2);
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+    m = mn;
+  }
+  if (lane == 0) { red_m[wid] = m; red_s[wid] = s; }
   __syncthreads();
-  mx = red[0];
-  for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red[i]);
-  __syncthreads();
-  float s = 0.f;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) s += __expf(lr[c] - mx);
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  s = 0.f;
-  for (int i = 0; i < 8; ++i) s += red[i];
-  const float lse = mx + logf(s);
-  const float inv = 1.0f / s;
-  for (int c = threadIdx.x; c < V; c += blockDim.x) {
-    float p = __expf(lr[c] - mx) * inv;
-    if (c == target) p -= 1.0f;
-    dr[c] = __float2bfloat16_rn(p * scale);
+  float mx = red_m[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red_m[i]);
+  float sum = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sum += red_s[i] * __expf(red_m[i] - mx);
+  const float lse = mx + logf(sum);
+  const float inv = 1.0f / sum;
+  if (vec) {
+    for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
+      const float4 a = *reinterpret_cast<const float4*>(lr + c), b = *reinterpret_cast<const float4*>(lr + c + 4);
+      float p[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        p[i] = __expf(p[i] - mx) * inv;
+        if (c + i == target) p[i] -= 1.0f;
+        p[i] *= scale;
+      }
+      *reinterpret_cast<uint4*>(dr + c) = make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]),
+                                                     pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
+    }
+  } else {
+    for (int c = threadIdx.x; c < V; c += blockDim.x) {
+      float p = __expf(lr[c] - mx) * inv;
+      if (c == target) p -= 1.0f;
+      dr[c] = __float2bfloat16_rn(p * scale);
+    }
   }
   if (threadIdx.x == 0) row_loss[grow] = (double)(lse - lr[target]);
 }
@@ -284,19 +363,16 @@ extern "C" int fb_embed_bwd(const int32_t* d_tok, const float* d_dx, float* d_ge
 extern "C" int fb_ln_fwd(const float* d_x, const float* d_gamma, const float* d_beta, void* d_y_bf16, float* d_mean,
                          float* d_rstd, int rows, int d, void* stream) {
   FB_REQUIRE(rows > 0 && d > 0 && d <= 4096, "ln_fwd: bad shape rows=%d d=%d", rows, d);
-  const int nj = (d + 31) / 32;
+  const int vpt = (d + 255) / 256;
   cudaStream_t st = (cudaStream_t)stream;
-  const int grid = (rows + 7) / 8;
+  const int grid = std::min(rows, kNumSMs * 8);
 #define CALL_F(N) ln_fwd_kernel<N><<<grid, 256, 0, st>>>(d_x, d_gamma, d_beta, (__nv_bfloat16*)d_y_bf16, d_mean, d_rstd, rows, d)
-  if (nj <= 1) CALL_F(1);
-  else if (nj <= 2) CALL_F(2);
-  else if (nj <= 4) CALL_F(4);
-  else if (nj <= 8) CALL_F(8);
-  else if (nj <= 16) CALL_F(16);
-  else if (nj <= 24) CALL_F(24);
-  else if (nj <= 32) CALL_F(32);
-  else if (nj <= 64) CALL_F(64);
-  else CALL_F(128);
+  if (vpt <= 1) CALL_F(1);
+  else if (vpt <= 2) CALL_F(2);
+  else if (vpt <= 3) CALL_F(3);
+  else if (vpt <= 4) CALL_F(4);
+  else if (vpt <= 8) CALL_F(8);
+  else CALL_F(16);
 #undef CALL_F
   FB_LAUNCH_CHECK();
   return FB_OK;
