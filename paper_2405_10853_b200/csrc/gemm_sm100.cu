@@ -36,6 +36,19 @@ struct GemmCfg {
   static constexpr int TMEM_COLS = 2 * BN;
 };
 
+// Grouped raster: tiles walk GROUP_M m-blocks at a time (m fastest), so the ~148 concurrently
+// resident tiles touch GROUP_M A blocks and a few B blocks that stay L2-resident.
+constexpr int kGroupM = 16;
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
+  const int group_size = kGroupM * num_n;
+  const int g = tile / group_size;
+  const int first_m = g * kGroupM;
+  const int gm = min(num_m - first_m, kGroupM);
+  const int idx = tile - g * group_size;
+  mb = first_m + idx % gm;
+  nb = idx / gm;
+}
+
 struct EpiArgs {
   void* C;
   int64_t ldc;
@@ -199,8 +212,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile % num_m) * BM;
-        const int n0 = (tile / num_m) * BN;
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int m0 = mb * BM;
+        const int n0 = nb * BN;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = tiles + stage * Cfg::STAGE_BYTES;
@@ -257,8 +272,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int half = (warp - 2) >> 2;
     int it = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-      const int m0 = (tile % num_m) * BM;
-      const int n0 = (tile / num_m) * BN;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int m0 = mb * BM;
+      const int n0 = nb * BN;
       const int buf = it & 1;
       const uint32_t use = it >> 1;
       mbar_wait(&tfull_bar[buf], use & 1);
@@ -346,8 +363,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = cluster; tile < num_tiles; tile += nclusters) {
-        const int m0 = (tile % num_m) * 256 + rank * 128;
-        const int n0 = (tile / num_m) * 256 + rank * 128;
+        int mb, nb;
+        tile_coords(tile, num_m, num_n, mb, nb);
+        const int m0 = mb * 256 + rank * 128;
+        const int n0 = nb * 256 + rank * 128;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = tiles + stage * kStage2Bytes;
@@ -402,8 +421,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int half = (warp - 2) >> 2;
     int it = 0;
     for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
-      const int m0 = (tile % num_m) * 256 + rank * 128;
-      const int n0 = (tile / num_m) * 256 + half * 128;
+      int mb, nb;
+      tile_coords(tile, num_m, num_n, mb, nb);
+      const int m0 = mb * 256 + rank * 128;
+      const int n0 = nb * 256 + half * 128;
       const int buf = it & 1;
       const uint32_t use = it >> 1;
       mbar_wait(&tfull_bar[buf], use & 1);
