@@ -42,16 +42,20 @@ struct AttnTcCfg {
   static constexpr int Q_OFF = 0;              // [2] Q tiles
   static constexpr int K_OFF = 2 * QT;         // [2] stages
   static constexpr int V_OFF = K_OFF + 2 * KT; // [2] stages
-  static constexpr int P_OFF = V_OFF + 2 * KT; // [2] P tiles
-  static constexpr int BAR_OFF = P_OFF + 2 * PT;
+  static constexpr int P_OFF = V_OFF + 2 * KT; // [2 Q tiles][2 buffers] P tiles
+  static constexpr int BAR_OFF = P_OFF + 4 * PT;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
 };
 
+// Pipeline (per KV tile j; g = Q tile 0/1, b = j & 1):
+//   MMA:     S_g(j+1) -> TMEM S[g][b^1]   (runs ahead: S is double-buffered)
+//            PV_g(j)  -> TMEM O[g]        (after P_g(j) is in smem buffer [g][b])
+//   softmax: S[g][b] -> P[g][b]; O rescaled only when the row max grows by > 8 (log2)
 template <int DH>
 __global__ void __launch_bounds__(320, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tm,
-                       __nv_bfloat16* __restrict__ out,
-                       float* __restrict__ lse2, int T, int H, float scale_log2, int use_alibi) {
+                       __nv_bfloat16* __restrict__ out, float* __restrict__ lse2, int T, int H, float scale_log2,
+                       int use_alibi) {
   using Cf = AttnTcCfg<DH>;
   constexpr int BN = Cf::BN;
   extern __shared__ uint8_t smem_raw[];
@@ -59,13 +63,15 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cf::BAR_OFF);
   uint64_t* q_full = bar + 0;
-  uint64_t* kv_full = bar + 1;   // [2]
-  uint64_t* kv_empty = bar + 3;  // [2]
-  uint64_t* s_full = bar + 5;    // [2] per Q tile
-  uint64_t* s_empty = bar + 7;   // [2]
-  uint64_t* p_full = bar + 9;    // [2]
-  uint64_t* o_full = bar + 11;   // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 13);
+  uint64_t* k_full = bar + 1;     // [2]
+  uint64_t* k_empty = bar + 3;    // [2]
+  uint64_t* v_full = bar + 5;     // [2]
+  uint64_t* v_empty = bar + 7;    // [2]
+  uint64_t* s_full = bar + 9;     // [g][b]
+  uint64_t* s_empty = bar + 13;   // [g][b]
+  uint64_t* p_full = bar + 17;    // [g][b]
+  uint64_t* pv_done = bar + 21;   // [g][b]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 25);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int npair = T / 256;
@@ -74,20 +80,24 @@ __global__ void __launch_bounds__(320, 1)
   const int d = H * DH;
   const int row0 = b * T;
   const int q0 = pb * 256;
-  const int nkv = (q0 + 256) / BN;       // KV tiles for tile 1
-  const int nkv0 = (q0 + 128) / BN;      // KV tiles for tile 0
+  const int nkv = (q0 + 256) / BN;       // KV tiles for Q tile 1
+  const int nkv0 = (q0 + 128) / BN;      // KV tiles for Q tile 0
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
     tma_prefetch(&tmq);
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&kv_full[i], 1);
-      mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1);
+      mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1);
+      mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 4; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 4);
       mbar_init(&p_full[i], 4);
-      mbar_init(&o_full[i], 1);
+      mbar_init(&pv_done[i], 1);
     }
     fence_barrier_init();
   }
@@ -105,57 +115,70 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive_expect_tx(q_full, 2 * Cf::QT);
       tma_load_3d(smem + Cf::Q_OFF, &tmq, q_full, 0, row0 + q0, zq);
       tma_load_3d(smem + Cf::Q_OFF + Cf::QT, &tmq, q_full, 0, row0 + q0 + 128, zq);
-      for (int j = 0; j < nkv; ++j) {
+      // K runs one tile ahead of V: order K0, K1, V0, K2, V1, ... (K stages free right after the S MMAs)
+      auto load_k = [&](int j) {
         const int s = j & 1;
-        mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[s], 2 * Cf::KT);
-        tma_load_3d(smem + Cf::K_OFF + s * Cf::KT, &tm, &kv_full[s], 0, row0 + j * BN, zk);
-        tma_load_3d(smem + Cf::V_OFF + s * Cf::KT, &tm, &kv_full[s], 0, row0 + j * BN, zv);
+        mbar_wait(&k_empty[s], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[s], Cf::KT);
+        tma_load_3d(smem + Cf::K_OFF + s * Cf::KT, &tm, &k_full[s], 0, row0 + j * BN, zk);
+      };
+      auto load_v = [&](int j) {
+        const int s = j & 1;
+        mbar_wait(&v_empty[s], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[s], Cf::KT);
+        tma_load_3d(smem + Cf::V_OFF + s * Cf::KT, &tm, &v_full[s], 0, row0 + j * BN, zv);
+      };
+      load_k(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) load_k(j + 1);
+        load_v(j);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idS = idesc_bf16_f32(128, BN, 0, 0);
       constexpr uint32_t idO = idesc_bf16_f32(128, DH, 0, 1);
-      // TMEM: S_g at [64 g, 64 g + 64), O_g at [128 + DH g, 128 + DH (g+1))
+      // TMEM: S[g][b] at 64 (2g + b); O[g] at 256 + DH g
       auto issue_s = [&](int g, int j) {
-        const int s = j & 1;
-        mbar_wait(&s_empty[g], (((g ? j : j) & 1)) ^ 1);
+        const int bb = j & 1;
+        mbar_wait(&s_empty[2 * g + bb], ((j >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t qb = sQ + g * Cf::QT, kb = sK + s * Cf::KT;
+        const uint32_t qb = sQ + g * Cf::QT, kb = sK + (j & 1) * Cf::KT;
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {
           const uint32_t qoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
           const uint32_t koff = (kk >> 2) * (BN * 128) + (kk & 3) * 32;
-          umma_f16(tmem + 64 * g, smem_desc_sw128(qb + qoff, 16, 1024), smem_desc_sw128(kb + koff, 16, 1024), idS,
-                   kk > 0);
+          umma_f16(tmem + 64 * (2 * g + bb), smem_desc_sw128(qb + qoff, 16, 1024),
+                   smem_desc_sw128(kb + koff, 16, 1024), idS, kk > 0);
         }
-        umma_commit(&s_full[g]);
+        umma_commit(&s_full[2 * g + bb]);
+      };
+      auto issue_s_both = [&](int j) {  // S(j) for the active Q tiles, then release the K stage
+        mbar_wait(&k_full[j & 1], (j >> 1) & 1);
+        if (j < nkv0) issue_s(0, j);
+        issue_s(1, j);
+        umma_commit(&k_empty[j & 1]);
       };
       auto issue_pv = [&](int g, int j) {
-        const int s = j & 1;
-        mbar_wait(&p_full[g], j & 1);
+        const int bb = j & 1;
+        mbar_wait(&p_full[2 * g + bb], (j >> 1) & 1);
+        mbar_wait(&v_full[j & 1], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t pb_ = sP + g * Cf::PT, vb = sV + s * Cf::KT;
+        const uint32_t pbuf = sP + (2 * g + bb) * Cf::PT, vb = sV + (j & 1) * Cf::KT;
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
-          umma_f16(tmem + 128 + DH * g, smem_desc_sw128(pb_ + kk * 32, 16, 1024),
+          umma_f16(tmem + 256 + DH * g, smem_desc_sw128(pbuf + kk * 32, 16, 1024),
                    smem_desc_sw128(vb + kk * 2048, BN * 128, 1024), idO, (j | kk) > 0);
         }
-        umma_commit(&o_full[g]);
+        umma_commit(&pv_done[2 * g + bb]);
       };
       mbar_wait(q_full, 0);
-      mbar_wait(&kv_full[0], 0);
-      issue_s(0, 0);
-      issue_s(1, 0);
+      issue_s_both(0);
       for (int j = 0; j < nkv; ++j) {
-        const bool nxt = j + 1 < nkv;
-        if (nxt) mbar_wait(&kv_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+        if (j + 1 < nkv) issue_s_both(j + 1);  // run S ahead by one tile
         if (j < nkv0) issue_pv(0, j);
-        if (nxt && j + 1 < nkv0) issue_s(0, j + 1);
         issue_pv(1, j);
-        umma_commit(&kv_empty[j & 1]);
-        if (nxt) issue_s(1, j + 1);
+        umma_commit(&v_empty[j & 1]);
       }
     }
   } else {
@@ -166,72 +189,88 @@ __global__ void __launch_bounds__(320, 1)
     const int qi = q0 + 128 * g + r;
     const int ntile = g ? nkv : nkv0;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t tS = tmem + lane_off + 64 * g;
-    const uint32_t tO = tmem + lane_off + 128 + DH * g;
+    const uint32_t tO = tmem + lane_off + 256 + DH * g;
     const float sl = use_alibi ? exp2f(-8.0f * (float)(h + 1) / (float)H) * 1.4426950408889634f : 0.0f;
-    const uint32_t prow = sP + g * Cf::PT + r * 128;
     float m = -INFINITY, l = 0.f;
     for (int j = 0; j < ntile; ++j) {
       const int k0 = j * BN;
+      const int bb = j & 1;
       const bool diag = k0 + BN > qi - r;  // tile reaches this Q tile's diagonal
-      mbar_wait(&s_full[g], j & 1);
+      const uint32_t tS = tmem + lane_off + 64 * (2 * g + bb);
+      const uint32_t prow = sP + (2 * g + bb) * Cf::PT + r * 128;
+      mbar_wait(&s_full[2 * g + bb], (j >> 1) & 1);
       tc_fence_after();
       uint32_t v[64];
       tmem_ld_32x32b_x32(tS, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
       tmem_ld_32x32b_x32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
       tmem_ld_wait();
-      // x = S * scale + sl * (k - q): bias base for key k0, step sl per key
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[2 * g + bb]);  // S buffer free for S(j+2)
       const float base = sl * (float)(k0 - qi);
-      float mx = -INFINITY;
+      float pm[8];
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        float x = fmaf(__uint_as_float(v[i]), scale_log2, fmaf(sl, (float)i, base));
-        if (diag && k0 + i > qi) x = -INFINITY;
-        v[i] = __float_as_uint(x);
-        mx = fmaxf(mx, x);
+      for (int u = 0; u < 8; ++u) pm[u] = -INFINITY;
+      if (diag) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          float x = fmaf(__uint_as_float(v[i]), scale_log2, fmaf(sl, (float)i, base));
+          x = (k0 + i > qi) ? -INFINITY : x;
+          v[i] = __float_as_uint(x);
+          pm[i & 7] = fmaxf(pm[i & 7], x);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const float x = fmaf(__uint_as_float(v[i]), scale_log2, fmaf(sl, (float)i, base));
+          v[i] = __float_as_uint(x);
+          pm[i & 7] = fmaxf(pm[i & 7], x);
+        }
       }
-      const float m_new = fmaxf(m, mx);
+      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+      // lazy rescale (FA4-style): keep the running max unless it grows by more than 8 (log2 units)
+      const float m_new = (mx > m + 8.0f) ? mx : m;
       const float alpha = ex2(m - m_new);
-      float rs = 0.f;
+      // P buffer [g][bb] was last read by PV(j-2)
+      if (j >= 2) mbar_wait(&pv_done[2 * g + bb], ((j >> 1) & 1) ^ 1);
+      float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         float p[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           p[i] = ex2(__uint_as_float(v[8 * q + i]) - m_new);
-          rs += p[i];
+          ps[i] += p[i];
         }
         const uint32_t addr = prow + (((q) ^ (r & 7)) << 4);
         asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(pack_bf16(p[0], p[1])),
                      "r"(pack_bf16(p[2], p[3])), "r"(pack_bf16(p[4], p[5])), "r"(pack_bf16(p[6], p[7])));
       }
+      const float rs = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
       l = l * alpha + rs;
       m = m_new;
-      if (j > 0) {
-        mbar_wait(&o_full[g], (j - 1) & 1);
+      if (j > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
+        // O must hold exactly PV(0..j-1) before it is rescaled
+        mbar_wait(&pv_done[2 * g + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha != 1.0f)) {
 #pragma unroll
-          for (int c = 0; c < DH / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld_32x32b_x32(tO + c * 32, o);
-            tmem_ld_wait();
+        for (int c = 0; c < DH / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld_32x32b_x32(tO + c * 32, o);
+          tmem_ld_wait();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
-            tmem_st_32x32b_x32(tO + c * 32, o);
-          }
-          tmem_st_wait();
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st_32x32b_x32(tO + c * 32, o);
         }
+        tmem_st_wait();
       }
       tc_fence_before();
       fence_async_smem();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&s_empty[g]);
-        mbar_arrive(&p_full[g]);
-      }
+      if (lane == 0) mbar_arrive(&p_full[2 * g + bb]);
     }
-    mbar_wait(&o_full[g], (ntile - 1) & 1);
+    const int jl = ntile - 1;
+    mbar_wait(&pv_done[2 * g + (jl & 1)], (jl >> 1) & 1);
     tc_fence_after();
     const float il = 1.0f / l;
     __nv_bfloat16* orow = out + ((int64_t)row0 + qi) * d + h * DH;
