@@ -57,6 +57,25 @@ def n_params(c):
     return V * d + L * (12 * d * d + 4 * d) + 2 * d + d * V
 
 
+def ncu_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` capture
+    (profiles/r01_ncu_summary.json, tcgen05 2-SM GEMM, C4 fc fwd + GELU: M=16384 N=8192 K=2048)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_summary.json")) as fh:
+            s = json.load(fh)
+        for k, v in s.items():
+            if k.startswith("gemm2:"):
+                scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+                u = v["units"]
+                rd = float(v["dram__bytes_read.sum"]) * scale.get(u["dram__bytes_read.sum"], 1)
+                wr = float(v["dram__bytes_write.sum"]) * scale.get(u["dram__bytes_write.sum"], 1)
+                alg = (16384 * 2048 + 8192 * 2048) * 2 + 2 * 16384 * 8192 * 2
+                return int(rd + wr), int(alg), k.split(":", 1)[1]
+    except Exception:
+        pass
+    return None, None, None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -243,6 +262,7 @@ def run_ours(args, cfgname):
     e2e = run_e2e(c, cfg, corpus, split, client, world, rank, K, barrier)
 
     # ---------------- compose ----------------
+    traffic, traffic_alg, traffic_kernel = ncu_traffic()
     clients_per_gpu = math.ceil(Kc / world)
     round_s = clients_per_gpu * c["S"] * ms_step / 1e3 + agg_total_ms / 1e3
     round_tokens = Kc * c["S"] * tokens_step
@@ -276,9 +296,11 @@ def run_ours(args, cfgname):
                   "agg_bytes_per_rank": agg_bytes},
         "step_tensor": {"achieved_tflops": round(step_tflops, 1), "peak": tf_sus,
                         "frac": round(step_tflops / tf_sus, 3), "note": "whole local step, algorithmic FLOPs (SURVEY 8d) vs sustained bf16"},
-        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tc_kernel (tcgen05)",
+        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tc{,2}_kernel (tcgen05, all GEMM launches of the step)",
                      "achieved": round(gemm_tflops, 1), "peak": tf_burst, "unit": "TFLOP/s",
-                     "frac": round(gemm_tflops / tf_burst, 3), "traffic": None,
+                     "frac": round(gemm_tflops / tf_burst, 3), "traffic": traffic,
+                     "traffic_note": (f"DRAM read+write bytes per launch of {traffic_kernel} from the committed ncu "
+                                      f"capture; algorithmic operand+output bytes {traffic_alg}") if traffic else None,
                      "launches_sampled": gemm_n, "avg_launch_ms": round(gemm_avg_ms, 4),
                      "peak_kind": peak_kind,
                      "gemm_share_of_step": round(gemm_ms / (ms_step * K) if gemm_n else 0, 3)},
