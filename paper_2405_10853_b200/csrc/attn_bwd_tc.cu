@@ -21,12 +21,25 @@
 //              (x 1/sqrt(dh)) into the f32 dq accumulator with vector reductions.
 //   end        dK (x 1/sqrt(dh)), dV -> bf16 rows of dqkv.
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
 
 namespace fb {
 using namespace sm100;
+
+#ifdef FB_ATTN_TRACE
+__device__ unsigned long long g_attn_trace[4096];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot) do { if (blockIdx.x == 4 && blockIdx.y == 5) g_attn_trace[(slot)] = gtimer(); } while (0)
+#else
+#define TRACE(slot) do {} while (0)
+#endif
 
 __device__ __forceinline__ float ex2b(float x) {
   float y;
@@ -142,6 +155,7 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t ph = t & 1, sph = (t >> 1) & 1;
         const uint32_t sQ = sQ0 + s * Cf::TILE, sO = sO0 + s * Cf::TILE;
         mbar_wait(&q_full[s], sph);
+        TRACE(16 * t + 0);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {  // S^T = K Q^T
@@ -150,6 +164,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         mbar_wait(&o_full[s], sph);
         mbar_wait(dq_empty, ph ^ 1);  // dP^T columns still hold dQ of the previous tile until drained
+        TRACE(16 * t + 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < DH / 16; ++kk) {  // dP^T = V dO^T
@@ -158,6 +173,7 @@ __global__ void __launch_bounds__(320, 1)
         }
         umma_commit(s_full);
         mbar_wait(p_full, ph);
+        TRACE(16 * t + 2);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // dV += P^T dO   (K = 128 queries)
@@ -168,6 +184,7 @@ __global__ void __launch_bounds__(320, 1)
         umma_commit(p_free);
         umma_commit(&o_empty[s]);
         mbar_wait(ds_full, ph);
+        TRACE(16 * t + 3);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // dK += dS^T Q
@@ -209,8 +226,10 @@ __global__ void __launch_bounds__(320, 1)
       if (tid < 128) Eb[tid] = sl * (float)(q0 + tid) + lse2[(int64_t)bh * T + q0 + tid];
       else Db[tid - 128] = Dd[(int64_t)bh * T + q0 + tid - 128];
       asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (warp == 2 && lane == 0) TRACE(16 * t + 4);
       mbar_wait(s_full, ph);
       mbar_wait(ds_free, ph ^ 1);  // the shared P/dS tile is no longer read by dQ of the previous tile
+      if (warp == 2 && lane == 0) TRACE(16 * t + 5);
       tc_fence_after();
       uint32_t dsp[32];  // dS^T packed bf16x2, written after dV consumed P^T
 #pragma unroll
@@ -243,8 +262,10 @@ __global__ void __launch_bounds__(320, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
+      if (warp == 2 && lane == 0) TRACE(16 * t + 6);
       // dV has consumed P^T: overwrite the shared tile with dS^T
       mbar_wait(p_free, ph);
+      if (warp == 2 && lane == 0) TRACE(16 * t + 7);
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
 #pragma unroll
@@ -258,10 +279,12 @@ __global__ void __launch_bounds__(320, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(ds_full);
+      if (warp == 2 && lane == 0) TRACE(16 * t + 8);
       // drain this warpgroup's half of dQ (thread = query row r of this tile): TMEM -> 128B-swizzled
       // smem (the P/dS tile is free once dQ_t has completed) -> TMA bulk reduce-add into the f32 dq
       // accumulator, one 128 x 32 box per chunk (replaces per-thread red.global traffic).
       mbar_wait(dq_full, ph);
+      if (warp == 2 && lane == 0) TRACE(16 * t + 9);
       tc_fence_after();
       const uint32_t stage = sPS + g * 16384;
 #pragma unroll 1
@@ -295,6 +318,7 @@ __global__ void __launch_bounds__(320, 1)
       if (quad == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
       asm volatile("bar.sync 1, 256;" ::: "memory");  // both staging halves drained before any next-tile P write
+      if (warp == 2 && lane == 0) TRACE(16 * t + 10);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
@@ -308,6 +332,273 @@ __global__ void __launch_bounds__(320, 1)
       uint32_t kv[32], vv[32];
       const uint32_t col = (DH / 2) * g + c * 32;
       tmem_ld_32x32b_x32(tmem + 256 + DH + lane_off + col, kv);
+      tmem_ld_32x32b_x32(tmem + 256 + lane_off + col, vv);
+      tmem_ld_wait();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float* fk = reinterpret_cast<const float*>(kv) + 8 * q;
+        const float* fv = reinterpret_cast<const float*>(vv) + 8 * q;
+        *reinterpret_cast<uint4*>(dkrow + c * 32 + 8 * q) =
+            make_uint4(pack_bf16(fk[0] * scale, fk[1] * scale), pack_bf16(fk[2] * scale, fk[3] * scale),
+                       pack_bf16(fk[4] * scale, fk[5] * scale), pack_bf16(fk[6] * scale, fk[7] * scale));
+        *reinterpret_cast<uint4*>(dvrow + c * 32 + 8 * q) = make_uint4(
+            pack_bf16(fv[0], fv[1]), pack_bf16(fv[2], fv[3]), pack_bf16(fv[4], fv[5]), pack_bf16(fv[6], fv[7]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// dh = 128 variant with 64-query tiles and a software pipeline across query tiles:
+//   MMA order per tile t:  [pds_full(t)]  S^T(t+1), dP^T(t+1)  dV(t)  dK(t)  [dq_empty(t-1)] dQ^T(t)
+//   so the elementwise phase of tile t+1 overlaps the dV/dK/dQ MMAs of tile t.
+//   dQ^T = K^T dS^T (M = dh = 128, N = 64 queries, K = 128 keys) has its own TMEM columns;
+//   it is drained by the compute warps of the NEXT tile through a dedicated smem staging
+//   box and ONE TMA bulk reduce-add per tile (dq rows [q0, q0+64) x 128 cols).
+//   TMEM: S^T [0,64)  dP^T [64,128)  dQ^T [128,192)  dV [256,384)  dK [384,512).
+struct AttnBwd64Cfg {
+  static constexpr int DH = 128;
+  static constexpr int KT = 128 * DH * 2;        // K or V tile (128 keys)
+  static constexpr int QT = 64 * DH * 2;         // Q or dO tile (64 queries)
+  static constexpr int PT = 128 * 64 * 2;        // P^T or dS^T tile (128 keys x 64 q)
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = K_OFF + KT;
+  static constexpr int Q_OFF = V_OFF + KT;       // [2]
+  static constexpr int O_OFF = Q_OFF + 2 * QT;   // [2]
+  static constexpr int P_OFF = O_OFF + 2 * QT;   // [2]
+  static constexpr int S_OFF = P_OFF + 2 * PT;   // [2]
+  static constexpr int X_OFF = S_OFF + 2 * PT;   // dQ staging: 64 rows x 128 f32
+  static constexpr int L_OFF = X_OFF + 64 * DH * 4;  // e[64], D[64]
+  static constexpr int BAR_OFF = L_OFF + 2 * 64 * 4;
+  static constexpr int SMEM = BAR_OFF + 192 + 1024;
+};
+
+__global__ void __launch_bounds__(320, 1)
+    attn_bwd_tc64_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
+                         const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
+                         const float* __restrict__ lse2, const float* __restrict__ Dd,
+                         __nv_bfloat16* __restrict__ dqkv, int T, int H, float scale_log2, float scale, int use_alibi) {
+  using Cf = AttnBwd64Cfg;
+  constexpr int DH = Cf::DH;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cf::BAR_OFF);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* q_full = bar + 1;     // [2]
+  uint64_t* o_full = bar + 3;     // [2]
+  uint64_t* q_empty = bar + 5;    // [2]
+  uint64_t* o_empty = bar + 7;    // [2]
+  uint64_t* s_full = bar + 9;
+  uint64_t* pds_full = bar + 10;
+  uint64_t* pds_free = bar + 11;  // [2]
+  uint64_t* dq_full = bar + 13;
+  uint64_t* dq_empty = bar + 14;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  float* sE = reinterpret_cast<float*>(smem + Cf::L_OFF);
+  float* sD = sE + 64;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x;
+  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int d = H * DH;
+  const int row0 = b * T;
+  const int k0 = kb * 128;
+  const int first = 2 * kb, ntiles = T / 64 - 2 * kb;  // causal: query tiles of 64 from the block's diagonal
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_kv);
+    tma_prefetch(&tm_q);
+    tma_prefetch(&tm_do);
+    tma_prefetch(&tm_dq);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&o_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+      mbar_init(&o_empty[s], 1);
+      mbar_init(&pds_free[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(pds_full, 8);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 8);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sK = smem_u32(smem + Cf::K_OFF), sV = smem_u32(smem + Cf::V_OFF), sQ0 = smem_u32(smem + Cf::Q_OFF),
+                 sO0 = smem_u32(smem + Cf::O_OFF), sP0 = smem_u32(smem + Cf::P_OFF), sS0 = smem_u32(smem + Cf::S_OFF),
+                 sX = smem_u32(smem + Cf::X_OFF);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int zq = (h * DH) / 64, zk = (d + h * DH) / 64, zv = (2 * d + h * DH) / 64, zo = (h * DH) / 64;
+      mbar_arrive_expect_tx(kv_full, 2 * Cf::KT);
+      tma_load_3d(smem + Cf::K_OFF, &tm_kv, kv_full, 0, row0 + k0, zk);
+      tma_load_3d(smem + Cf::V_OFF, &tm_kv, kv_full, 0, row0 + k0, zv);
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t & 1;
+        const uint32_t ph = (t >> 1) & 1;
+        const int q0 = (first + t) * 64;
+        mbar_wait(&q_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&q_full[s], Cf::QT);
+        tma_load_3d(smem + Cf::Q_OFF + s * Cf::QT, &tm_q, &q_full[s], 0, row0 + q0, zq);
+        mbar_wait(&o_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&o_full[s], Cf::QT);
+        tma_load_3d(smem + Cf::O_OFF + s * Cf::QT, &tm_do, &o_full[s], 0, row0 + q0, zo);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idSP = idesc_bf16_f32(128, 64, 0, 0);  // S^T, dP^T: M=128 keys, N=64 q, K=dh
+      constexpr uint32_t idKV = idesc_bf16_f32(128, DH, 0, 1);  // dV, dK: K-major A (P^T/dS^T), MN-major B
+      constexpr uint32_t idQ = idesc_bf16_f32(128, 64, 1, 1);   // dQ^T = K^T dS^T: MN-major A and B
+      const uint32_t tS = tmem, tP = tmem + 64, tQ = tmem + 128, tV = tmem + 256, tK = tmem + 384;
+      auto issue_sp = [&](int t) {
+        const int s = t & 1;
+        const uint32_t sph = (t >> 1) & 1;
+        const uint32_t sQ = sQ0 + s * Cf::QT, sO = sO0 + s * Cf::QT;
+        mbar_wait(&q_full[s], sph);
+        mbar_wait(&o_full[s], sph);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          const uint32_t boff = (kk >> 2) * (64 * 128) + (kk & 3) * 32;
+          umma_f16(tS, smem_desc_sw128(sK + aoff, 16, 1024), smem_desc_sw128(sQ + boff, 16, 1024), idSP, kk > 0);
+          umma_f16(tP, smem_desc_sw128(sV + aoff, 16, 1024), smem_desc_sw128(sO + boff, 16, 1024), idSP, kk > 0);
+        }
+        umma_commit(s_full);
+      };
+      mbar_wait(kv_full, 0);
+      issue_sp(0);
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t & 1;
+        const uint32_t ph = t & 1;
+        const uint32_t sQ = sQ0 + s * Cf::QT, sO = sO0 + s * Cf::QT;
+        const uint32_t sP = sP0 + s * Cf::PT, sS = sS0 + s * Cf::PT;
+        mbar_wait(pds_full, ph);  // S^T/dP^T(t) consumed; P^T(t), dS^T(t) in smem
+        if (t + 1 < ntiles) issue_sp(t + 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO   (K = 64 queries)
+          umma_f16(tV, smem_desc_sw128(sP + kk * 32, 16, 1024), smem_desc_sw128(sO + kk * 2048, 64 * 128, 1024), idKV,
+                   (t | kk) > 0);
+        umma_commit(&o_empty[s]);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q
+          umma_f16(tK, smem_desc_sw128(sS + kk * 32, 16, 1024), smem_desc_sw128(sQ + kk * 2048, 64 * 128, 1024), idKV,
+                   (t | kk) > 0);
+        umma_commit(&q_empty[s]);
+        mbar_wait(dq_empty, ph ^ 1);  // dQ^T(t-1) drained
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 keys)
+          umma_f16(tQ, smem_desc_sw128(sK + kk * 2048, 128 * 128, 1024), smem_desc_sw128(sS + kk * 2048, 8192, 1024),
+                   idQ, kk > 0);
+        umma_commit(dq_full);
+        umma_commit(&pds_free[s]);
+      }
+    }
+  } else {
+    // compute warps: g = warpgroup (query-column half), quad = TMEM lane quadrant
+    const int g = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // TMEM lane: key row (elementwise) / dh index (dQ^T drain)
+    const int kj = k0 + r;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const float sl = use_alibi ? exp2f(-8.0f * (float)(h + 1) / (float)H) * 1.4426950408889634f : 0.0f;
+    const float slk = sl * (float)kj;
+    const int tid = threadIdx.x - 64;  // 0..255
+    float* Xs = reinterpret_cast<float*>(smem + Cf::X_OFF);
+    auto drain = [&](int t) {  // dQ^T(t) -> staging [64 q][128 dh] -> TMA reduce-add into dq rows
+      const int q0 = (first + t) * 64;
+      mbar_wait(dq_full, t & 1);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tmem + 128 + lane_off + 32 * g, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+      // the staging box of the previous reduce must have been read by TMA
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+#pragma unroll
+      for (int i = 0; i < 32; ++i) Xs[(32 * g + i) * DH + r] = __uint_as_float(v[i]) * scale;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync 2, 256;" ::: "memory");
+      if (tid == 0) {
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                reinterpret_cast<uint64_t>(&tm_dq)),
+            "r"(sX), "r"(h * DH), "r"(row0 + q0)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    };
+    for (int t = 0; t < ntiles; ++t) {
+      const int s = t & 1;
+      const uint32_t ph = t & 1;
+      const int q0 = (first + t) * 64;
+      const bool diag = (t < 2);
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // everyone is done with the previous e/D
+      if (tid < 64) sE[tid] = sl * (float)(q0 + tid) + lse2[(int64_t)bh * T + q0 + tid];
+      else if (tid < 128) sD[tid - 64] = Dd[(int64_t)bh * T + q0 + tid - 64];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      mbar_wait(s_full, ph);
+      tc_fence_after();
+      uint32_t sv[32], pv[32];
+      tmem_ld_32x32b_x32(tmem + lane_off + 32 * g, sv);
+      tmem_ld_32x32b_x32(tmem + 64 + lane_off + 32 * g, pv);
+      tmem_ld_wait();
+      // P^T / dS^T buffers [s] were last read by the MMAs of tile t-2
+      if (t >= 2) mbar_wait(&pds_free[s], ((t >> 1) & 1) ^ 1);
+      const uint32_t prow = sP0 + s * Cf::PT + r * 128, srow = sS0 + s * Cf::PT + r * 128;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float p[8], ds[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int ql = 32 * g + q * 8 + i;
+          const float x = fmaf(__uint_as_float(sv[q * 8 + i]), scale_log2, slk - sE[ql]);
+          p[i] = (diag && q0 + ql < kj) ? 0.f : ex2b(x);
+          ds[i] = p[i] * (__uint_as_float(pv[q * 8 + i]) - sD[ql]);
+        }
+        const int kc = 4 * g + q;
+        const uint32_t sw = ((kc ^ (r & 7)) << 4);
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(pack_bf16(p[0], p[1])),
+                     "r"(pack_bf16(p[2], p[3])), "r"(pack_bf16(p[4], p[5])), "r"(pack_bf16(p[6], p[7])));
+        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(srow + sw), "r"(pack_bf16(ds[0], ds[1])),
+                     "r"(pack_bf16(ds[2], ds[3])), "r"(pack_bf16(ds[4], ds[5])), "r"(pack_bf16(ds[6], ds[7])));
+      }
+      tc_fence_before();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pds_full);
+      if (t > 0) drain(t - 1);  // overlaps the MMAs of tile t
+    }
+    drain(ntiles - 1);
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // dK, dV (the last dK/dV MMAs completed before the last dq_full)
+    const int64_t ld = 3 * (int64_t)d;
+    __nv_bfloat16* dkrow = dqkv + ((int64_t)row0 + kj) * ld + d + h * DH + (DH / 2) * g;
+    __nv_bfloat16* dvrow = dkrow + d;
+#pragma unroll 1
+    for (int c = 0; c < DH / 64; ++c) {
+      uint32_t kv[32], vv[32];
+      const uint32_t col = (DH / 2) * g + c * 32;
+      tmem_ld_32x32b_x32(tmem + 384 + lane_off + col, kv);
       tmem_ld_32x32b_x32(tmem + 256 + lane_off + col, vv);
       tmem_ld_wait();
 #pragma unroll
@@ -347,6 +638,55 @@ static int encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int c
   return FB_OK;
 }
 
+static int encode_box(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_rows, int box_chunks) {
+  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64)};
+  cuuint64_t strides[2] = {(cuuint64_t)cols * 2, 128};
+  cuuint32_t box[3] = {64, (cuuint32_t)box_rows, (cuuint32_t)box_chunks};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_enc_bwd(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("attn bwd tensor map encode failed: %d", (int)r);
+    return FB_CUDA_ERROR;
+  }
+  return FB_OK;
+}
+
+static int attn_bwd_tc64_launch(const void* qkv, const void* dO, const float* lse, const float* Dbuf, float* dq,
+                                void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
+  using Cf = AttnBwd64Cfg;
+  constexpr int DH = 128;
+  const int d = H * DH;
+  CUtensorMap tkv, tq, to, tdq;
+  int rc = encode_box(&tkv, qkv, (int64_t)B * T, 3 * d, 128, DH / 64);
+  if (rc) return rc;
+  rc = encode_box(&tq, qkv, (int64_t)B * T, 3 * d, 64, DH / 64);
+  if (rc) return rc;
+  rc = encode_box(&to, dO, (int64_t)B * T, d, 64, DH / 64);
+  if (rc) return rc;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)B * T};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 4};
+    cuuint32_t box[2] = {DH, 64};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_enc_bwd(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("attn bwd dq tensor map encode failed: %d", (int)r);
+      return FB_CUDA_ERROR;
+    }
+  }
+  auto k = attn_bwd_tc64_kernel;
+  FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
+  const float scale = 1.0f / sqrtf((float)DH);
+  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tkv, tq, to, tdq, lse, Dbuf, (__nv_bfloat16*)dqkv, T, H,
+                                                 1.4426950408889634f * scale, scale, use_alibi);
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
 template <int DH>
 int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const float* Dbuf, float* dq, void* dqkv,
                        int B, int T, int H, int use_alibi, cudaStream_t st) {
@@ -361,6 +701,7 @@ int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const 
     }
     g_enc_bwd = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
+  if (DH == 128 && !getenv("FB_ATTN_BWD_V1")) return attn_bwd_tc64_launch(qkv, dO, lse, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
   const int d = H * DH;
   CUtensorMap tq, to;
   int rc = encode_rows_map(&tq, qkv, (int64_t)B * T, 3 * d, DH / 64);
@@ -396,3 +737,9 @@ template int attn_bwd_tc_launch<128>(const void*, const void*, const float*, con
                                      int, int, cudaStream_t);
 
 }  // namespace fb
+
+#ifdef FB_ATTN_TRACE
+extern "C" int fb_attn_trace_read(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, fb::g_attn_trace, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : 2;
+}
+#endif

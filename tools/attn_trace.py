@@ -1,0 +1,38 @@
+"""Phase timeline of one attention-bwd CTA (FB_ATTN_TRACE build: tools/libfedb200_trace.so)."""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import torch
+
+os.environ["FB_LIB_PATH"] = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfedb200_trace.so")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2405_10853_b200 import ext  # noqa: E402
+
+L = ext.lib()
+B, T, H, dh = 8, 2048, 16, 128
+d = H * dh
+qkv = torch.randn(B * T, 3 * d, device="cuda").to(torch.bfloat16)
+o = torch.empty(B * T, d, dtype=torch.bfloat16, device="cuda")
+lse = torch.empty(B * H * T, device="cuda")
+do = torch.randn_like(o)
+dqkv = torch.empty_like(qkv)
+work = torch.empty(B * H * T + B * T * d, device="cuda")
+st = ext.stream_handle()
+ext.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T, H, dh, 1, st)
+for _ in range(2):
+    ext.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), dqkv.data_ptr(),
+             work.data_ptr(), B, T, H, dh, 1, st)
+torch.cuda.synchronize()
+buf = (C.c_ulonglong * 4096)()
+L.fb_attn_trace_read.argtypes = [C.c_void_p, C.c_int]
+assert L.fb_attn_trace_read(buf, 4096) == 0
+a = np.array(buf[:16 * 12], dtype=np.int64).reshape(12, 16)
+t0 = a[0, 0]
+names = ["mma:S", "mma:dP", "mma:p_full", "mma:ds_full", "sm:start", "sm:s_full", "sm:P_done", "sm:p_free",
+         "sm:dS_done", "sm:dq_full", "sm:drain_done"]
+for t in range(12):
+    if a[t, 0] == 0:
+        break
+    print(f"tile {t}: " + " ".join(f"{n}={(a[t, i] - t0) / 1000:.2f}" for i, n in enumerate(names)))
