@@ -621,6 +621,294 @@ __global__ void __launch_bounds__(320, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// dh = 64 variant of the pipelined backward: 128-query tiles, dQ = dS K (M = 128 queries,
+// A = the dS^T smem image read MN-major) in its own TMEM columns, two 128 x 32 TMA
+// reduce boxes per tile (one per warpgroup), same cross-tile pipeline as tc64.
+//   TMEM: S^T [0,128)  dP^T [128,256)  dQ [256,320)  dV [320,384)  dK [384,448).
+struct AttnBwdD64Cfg {
+  static constexpr int DH = 64;
+  static constexpr int KT = 128 * DH * 2;        // K or V tile (128 keys)
+  static constexpr int QT = 128 * DH * 2;        // Q or dO tile (128 queries)
+  static constexpr int PT = 128 * 128 * 2;       // P^T or dS^T tile
+  static constexpr int K_OFF = 0;
+  static constexpr int V_OFF = K_OFF + KT;
+  static constexpr int Q_OFF = V_OFF + KT;       // [2]
+  static constexpr int O_OFF = Q_OFF + 2 * QT;   // [2]
+  static constexpr int P_OFF = O_OFF + 2 * QT;   // [2] P^T, then dS^T (shared per buffer)
+  static constexpr int X_OFF = P_OFF + 2 * PT;   // dQ staging: 2 boxes of 128 rows x 32 f32 (swizzled)
+  static constexpr int L_OFF = X_OFF + 128 * DH * 4;
+  static constexpr int BAR_OFF = L_OFF + 2 * 128 * 4;
+  static constexpr int SMEM = BAR_OFF + 192 + 1024;
+};
+
+__global__ void __launch_bounds__(320, 1)
+    attn_bwd_tcd64_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
+                          const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2,
+                          const float* __restrict__ Dd, __nv_bfloat16* __restrict__ dqkv, int T, int H,
+                          float scale_log2, float scale, int use_alibi) {
+  using Cf = AttnBwdD64Cfg;
+  constexpr int DH = Cf::DH;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cf::BAR_OFF);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* q_full = bar + 1;     // [2]
+  uint64_t* o_full = bar + 3;     // [2]
+  uint64_t* q_empty = bar + 5;    // [2]
+  uint64_t* o_empty = bar + 7;    // [2]
+  uint64_t* s_full = bar + 9;
+  uint64_t* p_full = bar + 10;
+  uint64_t* pds_free = bar + 11;  // [2]
+  uint64_t* dq_full = bar + 13;
+  uint64_t* dq_empty = bar + 14;
+  uint64_t* p_free = bar + 15;
+  uint64_t* ds_full = bar + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+  float* sE = reinterpret_cast<float*>(smem + Cf::L_OFF);
+  float* sD = sE + 128;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = blockIdx.x;
+  const int bh = blockIdx.y, b = bh / H, h = bh % H;
+  const int d = H * DH;
+  const int row0 = b * T;
+  const int k0 = kb * 128;
+  const int first = kb, ntiles = T / 128 - kb;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tm_qkv);
+    tma_prefetch(&tm_do);
+    tma_prefetch(&tm_dq);
+    mbar_init(kv_full, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&q_full[s], 1);
+      mbar_init(&o_full[s], 1);
+      mbar_init(&q_empty[s], 1);
+      mbar_init(&o_empty[s], 1);
+      mbar_init(&pds_free[s], 1);
+    }
+    mbar_init(s_full, 1);
+    mbar_init(p_full, 8);
+    mbar_init(p_free, 1);
+    mbar_init(ds_full, 8);
+    mbar_init(dq_full, 1);
+    mbar_init(dq_empty, 8);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sK = smem_u32(smem + Cf::K_OFF), sV = smem_u32(smem + Cf::V_OFF), sQ0 = smem_u32(smem + Cf::Q_OFF),
+                 sO0 = smem_u32(smem + Cf::O_OFF), sP0 = smem_u32(smem + Cf::P_OFF), sX = smem_u32(smem + Cf::X_OFF);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int zq = (h * DH) / 64, zk = (d + h * DH) / 64, zv = (2 * d + h * DH) / 64, zo = (h * DH) / 64;
+      mbar_arrive_expect_tx(kv_full, 2 * Cf::KT);
+      tma_load_3d(smem + Cf::K_OFF, &tm_qkv, kv_full, 0, row0 + k0, zk);
+      tma_load_3d(smem + Cf::V_OFF, &tm_qkv, kv_full, 0, row0 + k0, zv);
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t & 1;
+        const uint32_t ph = (t >> 1) & 1;
+        const int q0 = (first + t) * 128;
+        mbar_wait(&q_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&q_full[s], Cf::QT);
+        tma_load_3d(smem + Cf::Q_OFF + s * Cf::QT, &tm_qkv, &q_full[s], 0, row0 + q0, zq);
+        mbar_wait(&o_empty[s], ph ^ 1);
+        mbar_arrive_expect_tx(&o_full[s], Cf::QT);
+        tma_load_3d(smem + Cf::O_OFF + s * Cf::QT, &tm_do, &o_full[s], 0, row0 + q0, zo);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idSP = idesc_bf16_f32(128, 128, 0, 0);
+      constexpr uint32_t idKV = idesc_bf16_f32(128, DH, 0, 1);
+      constexpr uint32_t idQ = idesc_bf16_f32(128, DH, 1, 1);
+      const uint32_t tS = tmem, tP = tmem + 128, tQ = tmem + 256, tV = tmem + 320, tK = tmem + 384;
+      auto issue_sp = [&](int t) {
+        const int s = t & 1;
+        const uint32_t sph = (t >> 1) & 1;
+        const uint32_t sQ = sQ0 + s * Cf::QT, sO = sO0 + s * Cf::QT;
+        mbar_wait(&q_full[s], sph);
+        mbar_wait(&o_full[s], sph);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < DH / 16; ++kk) {
+          const uint32_t off = (kk & 3) * 32;
+          umma_f16(tS, smem_desc_sw128(sK + off, 16, 1024), smem_desc_sw128(sQ + off, 16, 1024), idSP, kk > 0);
+          umma_f16(tP, smem_desc_sw128(sV + off, 16, 1024), smem_desc_sw128(sO + off, 16, 1024), idSP, kk > 0);
+        }
+        umma_commit(s_full);
+      };
+      mbar_wait(kv_full, 0);
+      issue_sp(0);
+      for (int t = 0; t < ntiles; ++t) {
+        const int s = t & 1;
+        const uint32_t ph = t & 1;
+        const uint32_t sQ = sQ0 + s * Cf::QT, sO = sO0 + s * Cf::QT;
+        const uint32_t sP = sP0 + s * Cf::PT, sS = sP;  // dS^T overwrites P^T after dV
+        mbar_wait(p_full, ph);
+        if (t + 1 < ntiles) issue_sp(t + 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // dV += P^T dO  (K = 128 queries)
+          const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          umma_f16(tV, smem_desc_sw128(sP + aoff, 16, 1024), smem_desc_sw128(sO + kk * 2048, 128 * 128, 1024), idKV,
+                   (t | kk) > 0);
+        }
+        umma_commit(&o_empty[s]);
+        umma_commit(p_free);
+        mbar_wait(ds_full, ph);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {  // dK += dS^T Q
+          const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
+          umma_f16(tK, smem_desc_sw128(sS + aoff, 16, 1024), smem_desc_sw128(sQ + kk * 2048, 128 * 128, 1024), idKV,
+                   (t | kk) > 0);
+        }
+        umma_commit(&q_empty[s]);
+        mbar_wait(dq_empty, ph ^ 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)  // dQ = dS K  (K = 128 keys); dS read as MN-major
+          umma_f16(tQ, smem_desc_sw128(sS + kk * 2048, 128 * 128, 1024), smem_desc_sw128(sK + kk * 2048, 128 * 128, 1024),
+                   idQ, kk > 0);
+        umma_commit(dq_full);
+        umma_commit(&pds_free[s]);
+      }
+    }
+  } else {
+    const int g = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // TMEM lane: key row (elementwise) / query row (dQ drain)
+    const int kj = k0 + r;
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const float sl = use_alibi ? exp2f(-8.0f * (float)(h + 1) / (float)H) * 1.4426950408889634f : 0.0f;
+    const float slk = sl * (float)kj;
+    const int tid = threadIdx.x - 64;
+    const uint32_t xbox = sX + g * 16384;  // this warpgroup's 128 x 32 f32 staging box
+    auto drain = [&](int t) {
+      const int q0 = (first + t) * 128;
+      mbar_wait(dq_full, t & 1);
+      tc_fence_after();
+      uint32_t v[32];
+      tmem_ld_32x32b_x32(tmem + 256 + lane_off + 32 * g, v);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dq_empty);
+      if (quad == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t addr = xbox + r * 128 + ((q ^ (r & 7)) << 4);
+        asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(__uint_as_float(v[4 * q]) * scale),
+                     "f"(__uint_as_float(v[4 * q + 1]) * scale), "f"(__uint_as_float(v[4 * q + 2]) * scale),
+                     "f"(__uint_as_float(v[4 * q + 3]) * scale));
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
+      if (quad == 0 && lane == 0) {
+        asm volatile(
+            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                reinterpret_cast<uint64_t>(&tm_dq)),
+            "r"(xbox), "r"(h * DH + 32 * g), "r"(row0 + q0)
+            : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    };
+    for (int t = 0; t < ntiles; ++t) {
+      const int s = t & 1;
+      const uint32_t ph = t & 1;
+      const int q0 = (first + t) * 128;
+      const bool diag = (t == 0);
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      if (tid < 128) sE[tid] = sl * (float)(q0 + tid) + lse2[(int64_t)bh * T + q0 + tid];
+      else sD[tid - 128] = Dd[(int64_t)bh * T + q0 + tid - 128];
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      mbar_wait(s_full, ph);
+      tc_fence_after();
+      uint32_t sv[2][32], pv[2][32];
+      tmem_ld_32x32b_x32(tmem + lane_off + 64 * g, sv[0]);
+      tmem_ld_32x32b_x32(tmem + lane_off + 64 * g + 32, sv[1]);
+      tmem_ld_32x32b_x32(tmem + 128 + lane_off + 64 * g, pv[0]);
+      tmem_ld_32x32b_x32(tmem + 128 + lane_off + 64 * g + 32, pv[1]);
+      tmem_ld_wait();
+      if (t >= 2) mbar_wait(&pds_free[s], ((t >> 1) & 1) ^ 1);
+      const uint32_t prow = sP0 + s * Cf::PT + r * 128;
+      uint32_t dsp[32];  // dS^T packed bf16x2, written once dV has consumed P^T
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float p[8], ds[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int ql = 64 * g + 32 * c + q * 8 + i;
+            const float x = fmaf(__uint_as_float(sv[c][q * 8 + i]), scale_log2, slk - sE[ql]);
+            p[i] = (diag && q0 + ql < kj) ? 0.f : ex2b(x);
+            ds[i] = p[i] * (__uint_as_float(pv[c][q * 8 + i]) - sD[ql]);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dsp[c * 16 + q * 4 + i] = pack_bf16(ds[2 * i], ds[2 * i + 1]);
+          const int kc = 8 * g + 4 * c + q;  // 8-query chunk 0..15
+          const uint32_t sw = (kc >> 3) * (128 * 128) + (((kc & 7) ^ (r & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(pack_bf16(p[0], p[1])),
+                       "r"(pack_bf16(p[2], p[3])), "r"(pack_bf16(p[4], p[5])), "r"(pack_bf16(p[6], p[7])));
+        }
+      }
+      tc_fence_before();
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full);
+      mbar_wait(p_free, ph);  // dV(t) has read P^T: overwrite with dS^T
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int kc = 8 * g + 4 * c + q;
+          const uint32_t sw = (kc >> 3) * (128 * 128) + (((kc & 7) ^ (r & 7)) << 4);
+          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(dsp[c * 16 + q * 4]),
+                       "r"(dsp[c * 16 + q * 4 + 1]), "r"(dsp[c * 16 + q * 4 + 2]), "r"(dsp[c * 16 + q * 4 + 3]));
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(ds_full);
+      if (t > 0) drain(t - 1);
+    }
+    drain(ntiles - 1);
+    if (quad == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    const int64_t ld = 3 * (int64_t)d;
+    __nv_bfloat16* dkrow = dqkv + ((int64_t)row0 + kj) * ld + d + h * DH + 32 * g;
+    __nv_bfloat16* dvrow = dkrow + d;
+    uint32_t kv[32], vv[32];
+    tmem_ld_32x32b_x32(tmem + 384 + lane_off + 32 * g, kv);
+    tmem_ld_32x32b_x32(tmem + 320 + lane_off + 32 * g, vv);
+    tmem_ld_wait();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float* fk = reinterpret_cast<const float*>(kv) + 8 * q;
+      const float* fv = reinterpret_cast<const float*>(vv) + 8 * q;
+      *reinterpret_cast<uint4*>(dkrow + 8 * q) =
+          make_uint4(pack_bf16(fk[0] * scale, fk[1] * scale), pack_bf16(fk[2] * scale, fk[3] * scale),
+                     pack_bf16(fk[4] * scale, fk[5] * scale), pack_bf16(fk[6] * scale, fk[7] * scale));
+      *reinterpret_cast<uint4*>(dvrow + 8 * q) = make_uint4(pack_bf16(fv[0], fv[1]), pack_bf16(fv[2], fv[3]),
+                                                            pack_bf16(fv[4], fv[5]), pack_bf16(fv[6], fv[7]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 g_enc_bwd = nullptr;
 
 static int encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_chunks) {
@@ -687,6 +975,38 @@ static int attn_bwd_tc64_launch(const void* qkv, const void* dO, const float* ls
   return FB_OK;
 }
 
+static int attn_bwd_tcd64_launch(const void* qkv, const void* dO, const float* lse, const float* Dbuf, float* dq,
+                                 void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
+  using Cf = AttnBwdD64Cfg;
+  constexpr int DH = 64;
+  const int d = H * DH;
+  CUtensorMap tq, to, tdq;
+  int rc = encode_box(&tq, qkv, (int64_t)B * T, 3 * d, 128, 1);
+  if (rc) return rc;
+  rc = encode_box(&to, dO, (int64_t)B * T, d, 128, 1);
+  if (rc) return rc;
+  {
+    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)B * T};
+    cuuint64_t strides[1] = {(cuuint64_t)d * 4};
+    cuuint32_t box[2] = {32, 128};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = g_enc_bwd(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("attn bwd dq tensor map encode failed: %d", (int)r);
+      return FB_CUDA_ERROR;
+    }
+  }
+  auto k = attn_bwd_tcd64_kernel;
+  FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
+  const float scale = 1.0f / sqrtf((float)DH);
+  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tq, to, tdq, lse, Dbuf, (__nv_bfloat16*)dqkv, T, H,
+                                                 1.4426950408889634f * scale, scale, use_alibi);
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
 template <int DH>
 int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const float* Dbuf, float* dq, void* dqkv,
                        int B, int T, int H, int use_alibi, cudaStream_t st) {
@@ -702,6 +1022,7 @@ int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const 
     g_enc_bwd = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   if (DH == 128 && !getenv("FB_ATTN_BWD_V1")) return attn_bwd_tc64_launch(qkv, dO, lse, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
+  if (DH == 64 && !getenv("FB_ATTN_BWD_V1")) return attn_bwd_tcd64_launch(qkv, dO, lse, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
   const int d = H * DH;
   CUtensorMap tq, to;
   int rc = encode_rows_map(&tq, qkv, (int64_t)B * T, 3 * d, DH / 64);
