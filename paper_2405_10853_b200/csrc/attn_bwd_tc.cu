@@ -374,8 +374,8 @@ struct AttnBwd64Cfg {
   static constexpr int P_OFF = O_OFF + 2 * QT;   // [2]
   static constexpr int S_OFF = P_OFF + 2 * PT;   // [2]
   static constexpr int X_OFF = S_OFF + 2 * PT;   // dQ staging: 64 rows x 128 f32
-  static constexpr int L_OFF = X_OFF + 64 * DH * 4;  // e[64], D[64]
-  static constexpr int BAR_OFF = L_OFF + 2 * 64 * 4;
+  static constexpr int L_OFF = X_OFF + 64 * DH * 4;  // e[2][64], D[2][64]
+  static constexpr int BAR_OFF = L_OFF + 4 * 64 * 4;
   static constexpr int SMEM = BAR_OFF + 192 + 1024;
 };
 
@@ -401,8 +401,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* dq_full = bar + 13;
   uint64_t* dq_empty = bar + 14;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-  float* sE = reinterpret_cast<float*>(smem + Cf::L_OFF);
-  float* sD = sE + 64;
+  float* sE0 = reinterpret_cast<float*>(smem + Cf::L_OFF);  // e[2][64] (double-buffered)
+  float* sD0 = sE0 + 128;                                     // D[2][64]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x;
@@ -488,7 +488,9 @@ __global__ void __launch_bounds__(320, 1)
         const uint32_t sQ = sQ0 + s * Cf::QT, sO = sO0 + s * Cf::QT;
         const uint32_t sP = sP0 + s * Cf::PT, sS = sS0 + s * Cf::PT;
         mbar_wait(pds_full, ph);  // S^T/dP^T(t) consumed; P^T(t), dS^T(t) in smem
+        TRACE(16 * t + 0);
         if (t + 1 < ntiles) issue_sp(t + 1);
+        TRACE(16 * t + 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO   (K = 64 queries)
@@ -500,7 +502,9 @@ __global__ void __launch_bounds__(320, 1)
           umma_f16(tK, smem_desc_sw128(sS + kk * 32, 16, 1024), smem_desc_sw128(sQ + kk * 2048, 64 * 128, 1024), idKV,
                    (t | kk) > 0);
         umma_commit(&q_empty[s]);
+        TRACE(16 * t + 2);
         mbar_wait(dq_empty, ph ^ 1);  // dQ^T(t-1) drained
+        TRACE(16 * t + 3);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)  // dQ^T = K^T dS^T   (K = 128 keys)
@@ -547,16 +551,27 @@ __global__ void __launch_bounds__(320, 1)
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
+    // e/D of tile t live in buffer t & 1; tile t+1's are prefetched before drain(t-1), whose
+    // CTA-wide barriers publish them (all readers of that buffer finished tile t-1 earlier)
+    auto load_ed = [&](int t) {
+      const int q0 = (first + t) * 64;
+      float* E = sE0 + (t & 1) * 64;
+      float* Dv = sD0 + (t & 1) * 64;
+      if (tid < 64) E[tid] = sl * (float)(q0 + tid) + lse2[(int64_t)bh * T + q0 + tid];
+      else if (tid < 128) Dv[tid - 64] = Dd[(int64_t)bh * T + q0 + tid - 64];
+    };
+    load_ed(0);
+    asm volatile("bar.sync 1, 256;" ::: "memory");
     for (int t = 0; t < ntiles; ++t) {
       const int s = t & 1;
       const uint32_t ph = t & 1;
       const int q0 = (first + t) * 64;
       const bool diag = (t < 2);
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // everyone is done with the previous e/D
-      if (tid < 64) sE[tid] = sl * (float)(q0 + tid) + lse2[(int64_t)bh * T + q0 + tid];
-      else if (tid < 128) sD[tid - 64] = Dd[(int64_t)bh * T + q0 + tid - 64];
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const float* sE = sE0 + (t & 1) * 64;
+      const float* sD = sD0 + (t & 1) * 64;
+      if (warp == 2 && lane == 0) TRACE(16 * t + 4);
       mbar_wait(s_full, ph);
+      if (warp == 2 && lane == 0) TRACE(16 * t + 5);
       tc_fence_after();
       uint32_t sv[32], pv[32];
       tmem_ld_32x32b_x32(tmem + lane_off + 32 * g, sv);
@@ -568,12 +583,18 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         float p[8], ds[8];
+        const float4 e0 = *reinterpret_cast<const float4*>(sE + 32 * g + q * 8);
+        const float4 e1 = *reinterpret_cast<const float4*>(sE + 32 * g + q * 8 + 4);
+        const float4 d0 = *reinterpret_cast<const float4*>(sD + 32 * g + q * 8);
+        const float4 d1 = *reinterpret_cast<const float4*>(sD + 32 * g + q * 8 + 4);
+        const float ev[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+        const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int ql = 32 * g + q * 8 + i;
-          const float x = fmaf(__uint_as_float(sv[q * 8 + i]), scale_log2, slk - sE[ql]);
+          const float x = fmaf(__uint_as_float(sv[q * 8 + i]), scale_log2, slk - ev[i]);
           p[i] = (diag && q0 + ql < kj) ? 0.f : ex2b(x);
-          ds[i] = p[i] * (__uint_as_float(pv[q * 8 + i]) - sD[ql]);
+          ds[i] = p[i] * (__uint_as_float(pv[q * 8 + i]) - dv[i]);
         }
         const int kc = 4 * g + q;
         const uint32_t sw = ((kc ^ (r & 7)) << 4);
@@ -586,7 +607,11 @@ __global__ void __launch_bounds__(320, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(pds_full);
+      if (warp == 2 && lane == 0) TRACE(16 * t + 6);
+      if (t + 1 < ntiles) load_ed(t + 1);
       if (t > 0) drain(t - 1);  // overlaps the MMAs of tile t
+      else asm volatile("bar.sync 1, 256;" ::: "memory");  // publish e/D(1) on the first tile
+      if (warp == 2 && lane == 0) TRACE(16 * t + 7);
     }
     drain(ntiles - 1);
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
