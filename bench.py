@@ -59,17 +59,17 @@ def n_params(c):
 
 def ncu_traffic():
     """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` capture
-    (profiles/r01_ncu_summary.json, tcgen05 2-SM GEMM, C4 fc fwd + GELU: M=16384 N=8192 K=2048)."""
+    (profiles/r01_ncu_summary.json, tcgen05 2-SM GEMM, C4 qkv fwd: M=16384 N=6144 K=2048, bf16 out)."""
     try:
         with open(os.path.join(ROOT, "profiles", "r01_ncu_summary.json")) as fh:
             s = json.load(fh)
         for k, v in s.items():
-            if k.startswith("gemm2:"):
+            if k.startswith("gemmqkv:"):
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
                 u = v["units"]
                 rd = float(v["dram__bytes_read.sum"]) * scale.get(u["dram__bytes_read.sum"], 1)
                 wr = float(v["dram__bytes_write.sum"]) * scale.get(u["dram__bytes_write.sum"], 1)
-                alg = (16384 * 2048 + 8192 * 2048) * 2 + 2 * 16384 * 8192 * 2
+                alg = (16384 * 2048 + 6144 * 2048) * 2 + 16384 * 6144 * 2
                 return int(rd + wr), int(alg), k.split(":", 1)[1]
     except Exception:
         pass
