@@ -112,6 +112,13 @@ int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, int a_major,
                  const void* d_B, int64_t ldb, int b_major, void* d_C, int64_t ldc, int epilogue,
                  const void* d_aux, void* d_aux_out, int64_t ld_aux, void* stream);
 
+/* Split-K variant for short-M/N, long-K products (weight gradients over many tokens):
+ * ksplit partial f32 products go to d_ws (ksplit*M*N floats) and are reduced in fixed
+ * split order into C (+= for FB_EPI_ACC_F32) — deterministic. ksplit <= 0: auto. */
+int fb_gemm_bf16_splitk(int M, int N, int K, const void* d_A, int64_t lda, int a_major,
+                        const void* d_B, int64_t ldb, int b_major, void* d_C, int64_t ldc, int epilogue,
+                        int ksplit, void* d_ws, int64_t ws_bytes, void* stream);
+
 /* ---- transformer pieces (model.py:75-150, :222-229) --------------------------------- */
 int fb_embed_fwd(const int32_t* d_tok, const float* d_emb, const float* d_pos, float* d_x,
                  int n_tok, int T, int d, void* stream);

@@ -55,7 +55,18 @@ struct EpiArgs {
   const void* aux;
   void* aux_out;
   int64_t ld_aux;
+  int ksplit;            // > 1: work unit u = (split, tile); split s writes C + s * split_stride
+  int64_t split_stride;  // elements
 };
+
+// work unit -> (tile, first k-block, k-block count)
+__device__ __forceinline__ void unit_coords(int u, int num_tiles, int num_kb, int ksplit, int& tile, int& kb0, int& nkb) {
+  tile = u % num_tiles;
+  const int s = u / num_tiles;
+  const int per = (num_kb + ksplit - 1) / ksplit;
+  kb0 = s * per;
+  nkb = min(num_kb, kb0 + per) - kb0;
+}
 
 __device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 __device__ __forceinline__ float gelu_erf_grad(float x) {
@@ -211,12 +222,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       // ---------------- TMA producer ----------------
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < num_tiles * ep.ksplit; u += gridDim.x) {
+        int tile, kb0, nkb;
+        unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
         const int m0 = mb * BM;
         const int n0 = nb * BN;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb0 + nkb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = tiles + stage * Cfg::STAGE_BYTES;
           uint8_t* sb = sa + Cfg::A_BYTES;
@@ -236,13 +249,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < num_tiles * ep.ksplit; u += gridDim.x, ++it) {
+      int tile, kb0, nkb;
+      unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
       const int buf = it & 1;
       const uint32_t use = it >> 1;
       mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + buf * BN;
-      for (int kb = 0; kb < num_kb; ++kb) {
+      for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&full_bar[stage], phase);
         tc_fence_after();
         if (lane == 0) {
@@ -271,7 +286,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int quad = warp & 3;  // TMEM lane quadrant this warp may access
     const int half = (warp - 2) >> 2;
     int it = 0;
-    for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+    for (int u = blockIdx.x; u < num_tiles * ep.ksplit; u += gridDim.x, ++it) {
+      int tile, kb0, nkb;
+      unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
+      EpiArgs eu = ep;
+      eu.C = (char*)ep.C + (u / num_tiles) * ep.split_stride * (EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU ? 2 : 4);
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       const int m0 = mb * BM;
@@ -293,7 +312,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           if (lane == 0) mbar_arrive(&tempty_bar[buf]);
         }
         const int col = n0 + half * (BN / 2) + c * 32;
-        if (row < M && col < N) epilogue_chunk<EPI>(ep, row, col, N, r);
+        if (row < M && col < N) epilogue_chunk<EPI>(eu, row, col, N, r);
       }
     }
   }
@@ -362,12 +381,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      for (int u = cluster; u < num_tiles * ep.ksplit; u += nclusters) {
+        int tile, kb0, nkb;
+        unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
         const int m0 = mb * 256 + rank * 128;
         const int n0 = nb * 256 + rank * 128;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = kb0; kb < kb0 + nkb; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = tiles + stage * kStage2Bytes;
           uint8_t* sb = sa + BM * BK * 2;
@@ -387,13 +408,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
+      for (int u = cluster; u < num_tiles * ep.ksplit; u += nclusters, ++it) {
+        int tile, kb0, nkb;
+        unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
         const int buf = it & 1;
         const uint32_t use = it >> 1;
         mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + buf * 256;
-        for (int kb = 0; kb < num_kb; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           if (lane == 0) {
@@ -420,7 +443,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
     int it = 0;
-    for (int tile = cluster; tile < num_tiles; tile += nclusters, ++it) {
+    for (int u = cluster; u < num_tiles * ep.ksplit; u += nclusters, ++it) {
+      int tile, kb0, nkb;
+      unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
+      EpiArgs eu = ep;
+      eu.C = (char*)ep.C + (u / num_tiles) * ep.split_stride * (EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU ? 2 : 4);
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       const int m0 = mb * 256 + rank * 128;
@@ -442,7 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (lane == 0) mbar_arrive_leader(&tempty_bar[buf]);
         }
         const int col = n0 + c * 32;
-        if (row < M && col < N) epilogue_chunk<EPI>(ep, row, col, N, r);
+        if (row < M && col < N) epilogue_chunk<EPI>(eu, row, col, N, r);
       }
     }
   }
@@ -457,6 +484,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 // ---------------------------------------------------------------------------------------
 // host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static thread_local void* g_split_ws = nullptr;  // split-K workspace for the current call
+static thread_local int g_split_n = 1;
 int g_gemm_2sm = 1;  // fb_gemm_set_2sm() toggles it (A/B tests)
 
 static int get_encoder() {
@@ -514,7 +543,7 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, in
     FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
     attr_set = true;
   }
-  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN) * ep.ksplit;
   const int grid = tiles < kNumSMs ? tiles : kNumSMs;
   kern<<<grid, kGemmThreads, Cfg::SMEM, st>>>(ta, tb, M, N, K, ep);
   FB_LAUNCH_CHECK();
@@ -530,7 +559,7 @@ static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, i
     FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
     attr_set = true;
   }
-  const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  const int tiles = ((M + 255) / 256) * ((N + 255) / 256) * ep.ksplit;
   const int clusters = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
   kern<<<2 * clusters, kGemmThreads, kSmem2, st>>>(ta, tb, M, N, K, ep);
   FB_LAUNCH_CHECK();
@@ -597,8 +626,9 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   if (rc) return rc;
   // 2-SM 256x256 tiles when they fill the 74 CTA pairs; else 1-SM 128x256, else 128x128
   const int tiles2 = ((M + 255) / 256) * ((N + 255) / 256);
-  const bool use2 = g_gemm_2sm && M >= 256 && N >= 256 && tiles2 >= kNumSMs / 2;
-  const int tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256);
+  const int ks = g_split_ws ? g_split_n : 1;
+  const bool use2 = g_gemm_2sm && M >= 256 && N >= 256 && tiles2 * ks >= kNumSMs / 2;
+  const int tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256) * ks;
   const int BN = (use2 || (N >= 256 && tiles256 >= kNumSMs)) ? 256 : 128;
   CUtensorMap ta, tb;
   rc = a_major ? make_map_mnmajor(&ta, d_A, M, K, lda, BM) : make_map_kmajor(&ta, d_A, M, K, lda, BM);
@@ -606,7 +636,13 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   const int bbox = use2 ? 128 : BN;  // 2-SM: each CTA stages 128 of the 256 B rows
   rc = b_major ? make_map_mnmajor(&tb, d_B, N, K, ldb, bbox) : make_map_kmajor(&tb, d_B, N, K, ldb, bbox);
   if (rc) return rc;
-  EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux};
+  EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux, 1, 0};
+  if (g_split_ws) {  // set by fb_gemm_bf16_splitk for this call only
+    ep.ksplit = g_split_n;
+    ep.C = g_split_ws;
+    ep.ldc = N;
+    ep.split_stride = (int64_t)M * N;
+  }
   cudaStream_t st = (cudaStream_t)stream;
   const int key = (BN == 256 ? 4 : 0) | (a_major ? 2 : 0) | (b_major ? 1 : 0);
   const int pi = prof_on() ? prof_start(0, st) : -1;
@@ -643,5 +679,56 @@ int gemm_dispatch(int key, int epilogue, const CUtensorMap& ta, const CUtensorMa
 
 extern "C" int fb_gemm_set_2sm(int enable) {
   fb::g_gemm_2sm = enable ? 1 : 0;
+  return FB_OK;
+}
+
+namespace fb {
+// C[m][n] (+)= sum_s W[s][m][n] in fixed split order (deterministic)
+__global__ void splitk_reduce_kernel(const float* __restrict__ W, int S, int64_t MN, int N, float* __restrict__ C,
+                                     int64_t ldc, int accumulate) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < MN / 4; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = 4 * i, m = e / N, n = e % N;
+    float4 acc = *reinterpret_cast<const float4*>(W + e);
+    for (int s = 1; s < S; ++s) {
+      const float4 v = *reinterpret_cast<const float4*>(W + s * MN + e);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    float4* c = reinterpret_cast<float4*>(C + m * ldc + n);
+    if (accumulate) {
+      const float4 o = *c;
+      acc.x += o.x; acc.y += o.y; acc.z += o.z; acc.w += o.w;
+    }
+    *c = acc;
+  }
+}
+}  // namespace fb
+
+// Split-K GEMM for short-M/N, long-K products (weight gradients over many tokens):
+// ksplit partial f32 products into d_ws (ksplit * M * N floats), then a fixed-order
+// reduction into C (f32; += when epilogue == FB_EPI_ACC_F32). ksplit <= 0 picks a split
+// that fills the 148 SMs.
+extern "C" int fb_gemm_bf16_splitk(int M, int N, int K, const void* d_A, int64_t lda, int a_major, const void* d_B,
+                                   int64_t ldb, int b_major, void* d_C, int64_t ldc, int epilogue, int ksplit,
+                                   void* d_ws, int64_t ws_bytes, void* stream) {
+  FB_REQUIRE(epilogue == FB_EPI_F32 || epilogue == FB_EPI_ACC_F32, "split-K supports the f32 / acc_f32 epilogues");
+  FB_REQUIRE(N % 4 == 0 && ldc % 4 == 0, "split-K needs N and ldc multiples of 4");
+  const int tiles2 = ((M + 255) / 256) * ((N + 255) / 256);
+  const int num_kb = (K + BK - 1) / BK;
+  if (ksplit <= 0) {
+    ksplit = 1;
+    while (tiles2 * ksplit < kNumSMs / 2 && num_kb / (ksplit + 1) >= 16) ++ksplit;
+  }
+  if (ksplit <= 1) return fb_gemm_bf16(M, N, K, d_A, lda, a_major, d_B, ldb, b_major, d_C, ldc, epilogue, nullptr,
+                                       nullptr, 0, stream);
+  FB_REQUIRE(d_ws && ws_bytes >= (int64_t)ksplit * M * N * 4, "split-K workspace too small (%d splits)", ksplit);
+  g_split_ws = d_ws;
+  g_split_n = ksplit;
+  int rc = fb_gemm_bf16(M, N, K, d_A, lda, a_major, d_B, ldb, b_major, d_ws, N, FB_EPI_F32, nullptr, nullptr, 0, stream);
+  g_split_ws = nullptr;
+  g_split_n = 1;
+  if (rc) return rc;
+  fb::splitk_reduce_kernel<<<fb::kNumSMs * 4, 256, 0, (cudaStream_t)stream>>>(
+      (const float*)d_ws, ksplit, (int64_t)M * N, N, (float*)d_C, ldc, epilogue == FB_EPI_ACC_F32);
+  FB_LAUNCH_CHECK();
   return FB_OK;
 }

@@ -66,9 +66,13 @@ struct Acts {  // per-layer saved activations
   __nv_bfloat16 *ln1, *qkv, *ao, *ln2, *pre, *act;
 };
 
+// split-K partials of the weight-gradient GEMMs: auto-split stops once the 74 CTA pairs are
+// busy, so splits * M * N <= (74 + tiles) * 256 * 256 < 16 M floats for every shape
+constexpr int64_t kSplitKFloats = 16ll << 20;
+
 struct WS {
   std::vector<Acts> L;
-  float *x_out, *meanf, *rstdf, *logits, *dx, *dln, *attn_work, *ln_work;
+  float *x_out, *meanf, *rstdf, *logits, *dx, *dln, *attn_work, *ln_work, *splitk;
   __nv_bfloat16 *lnf, *dlogits, *dxb, *dao, *dqkv, *dfc;
   int chunk;
 };
@@ -108,6 +112,7 @@ static WS carve(const fb_model_cfg& c, int B, int T, Arena& A) {
   w.dfc = A.take<__nv_bfloat16>(M * 4 * d);
   w.attn_work = A.take<float>(B * H * T + M * d);
   w.ln_work = A.take<float>(2 * 592 * d);
+  w.splitk = A.take<float>(kSplitKFloats);
   return w;
 }
 
@@ -134,6 +139,8 @@ using namespace fb;
 
 extern "C" int fb_gemm_bf16(int, int, int, const void*, int64_t, int, const void*, int64_t, int, void*, int64_t, int,
                             const void*, void*, int64_t, void*);
+extern "C" int fb_gemm_bf16_splitk(int, int, int, const void*, int64_t, int, const void*, int64_t, int, void*, int64_t,
+                                   int, int, void*, int64_t, void*);
 
 #define TRY(x)            \
   do {                    \
@@ -196,6 +203,11 @@ extern "C" int fb_model_fwd_bwd(const fb_model_cfg* cfgp, const float* P, const 
   }
   if (!want_grad) return FB_OK;
 
+  auto wgrad = [&](int Mg, int Ng, const __nv_bfloat16* A, int64_t lda, const __nv_bfloat16* Bm, int64_t ldb,
+                   float* Cg) {
+    return fb_gemm_bf16_splitk(Mg, Ng, M, A, lda, 1, Bm, ldb, 1, Cg, Ng, FB_EPI_ACC_F32, 0, w.splitk,
+                               kSplitKFloats * 4, st);
+  };
   // ---------------- backward ----------------
   TRY(fb_ln_bwd(w.x_out, P + Lo.lnf_w, w.meanf, w.rstdf, w.dln, nullptr, w.dx, w.dxb, G + Lo.lnf_w, G + Lo.lnf_b,
                 w.ln_work, M, d, st));
@@ -205,19 +217,17 @@ extern "C" int fb_model_fwd_bwd(const fb_model_cfg* cfgp, const float* P, const 
     // MLP: x_next = x_mid + proj2(gelu(fc(ln2(x_mid))))
     TRY(fb_gemm_bf16(M, 4 * d, d, w.dxb, d, 0, S + b.proj2, 4 * d, 1, w.dfc, 4 * d, FB_EPI_DGELU, a.pre, nullptr,
                      4 * d, st));
-    TRY(fb_gemm_bf16(d, 4 * d, M, w.dxb, d, 1, a.act, 4 * d, 1, G + b.proj2, 4 * d, FB_EPI_ACC_F32, nullptr, nullptr,
-                     0, st));
+    TRY(wgrad(d, 4 * d, w.dxb, d, a.act, 4 * d, G + b.proj2));
     TRY(fb_gemm_bf16(M, d, 4 * d, w.dfc, 4 * d, 0, S + b.fc, d, 1, w.dln, d, FB_EPI_F32, nullptr, nullptr, 0, st));
-    TRY(fb_gemm_bf16(4 * d, d, M, w.dfc, 4 * d, 1, a.ln2, d, 1, G + b.fc, d, FB_EPI_ACC_F32, nullptr, nullptr, 0, st));
+    TRY(wgrad(4 * d, d, w.dfc, 4 * d, a.ln2, d, G + b.fc));
     TRY(fb_ln_bwd(a.x_mid, P + b.ln2_w, a.mean2, a.rstd2, w.dln, w.dx, w.dx, w.dxb, G + b.ln2_w, G + b.ln2_b,
                   w.ln_work, M, d, st));
     // attention: x_mid = x_in + proj(attn(ln1(x_in)))
     TRY(fb_gemm_bf16(M, d, d, w.dxb, d, 0, S + b.proj, d, 1, w.dao, d, FB_EPI_BF16, nullptr, nullptr, 0, st));
-    TRY(fb_gemm_bf16(d, d, M, w.dxb, d, 1, a.ao, d, 1, G + b.proj, d, FB_EPI_ACC_F32, nullptr, nullptr, 0, st));
+    TRY(wgrad(d, d, w.dxb, d, a.ao, d, G + b.proj));
     TRY(fb_attn_bwd(a.qkv, a.ao, w.dao, a.lse, w.dqkv, w.attn_work, B, T, H, dh, c.use_alibi, st));
     TRY(fb_gemm_bf16(M, d, 3 * d, w.dqkv, 3 * d, 0, S + b.qkv, d, 1, w.dln, d, FB_EPI_F32, nullptr, nullptr, 0, st));
-    TRY(fb_gemm_bf16(3 * d, d, M, w.dqkv, 3 * d, 1, a.ln1, d, 1, G + b.qkv, d, FB_EPI_ACC_F32, nullptr, nullptr, 0,
-                     st));
+    TRY(wgrad(3 * d, d, w.dqkv, 3 * d, a.ln1, d, G + b.qkv));
     TRY(fb_ln_bwd(a.x_in, P + b.ln1_w, a.mean1, a.rstd1, w.dln, w.dx, w.dx, w.dxb, G + b.ln1_w, G + b.ln1_b,
                   w.ln_work, M, d, st));
   }

@@ -44,6 +44,7 @@ SIGNATURES = {
     "fb_adamw_step": [_vp, _vp, _vp, _vp, _vp, _i64, AdamWCfg, _vp, _vp, _vp, _vp, _vp],
     "fb_cast_bf16": [_vp, _vp, _i64, _vp],
     "fb_gemm_bf16": [_i, _i, _i, _vp, _i64, _i, _vp, _i64, _i, _vp, _i64, _i, _vp, _vp, _i64, _vp],
+    "fb_gemm_bf16_splitk": [_i, _i, _i, _vp, _i64, _i, _vp, _i64, _i, _vp, _i64, _i, _i, _vp, _i64, _vp],
     "fb_embed_fwd": [_vp, _vp, _vp, _vp, _i, _i, _i, _vp],
     "fb_embed_bwd": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp],
     "fb_ln_fwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp],

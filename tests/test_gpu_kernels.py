@@ -184,3 +184,25 @@ def test_gemm_2sm_matches_1sm(fb, a_major, b_major):
     fb.call("fb_gemm_set_2sm", 1)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("M,N,K,ks", [(1536, 512, 16384, 0), (2048, 2048, 16384, 2), (512, 512, 4096, 5), (384, 1024, 3000, 0)])
+def test_gemm_splitk_wgrad(fb, M, N, K, ks):
+    """Split-K weight gradient (MN-major A and B, f32 accumulate) == one-pass GEMM within fp32 reassociation."""
+    torch.manual_seed(6)
+    dev = torch.device("cuda")
+    dY = torch.randn(K, M, device=dev).to(torch.bfloat16)   # [tokens][M] -> A MN-major
+    X = torch.randn(K, N, device=dev).to(torch.bfloat16)    # [tokens][N] -> B MN-major
+    base = torch.randn(M, N, device=dev)
+    C1 = base.clone()
+    ws = torch.empty(32 << 20, dtype=torch.float32, device=dev)
+    fb.call("fb_gemm_bf16_splitk", M, N, K, dY.data_ptr(), M, 1, X.data_ptr(), N, 1, C1.data_ptr(), N,
+            fb.EPI["acc_f32"], ks, ws.data_ptr(), ws.numel() * 4, fb.stream_handle())
+    ref = base + dY.float().t() @ X.float()
+    torch.cuda.synchronize()
+    torch.testing.assert_close(C1, ref, atol=2e-3 * K ** 0.5, rtol=1e-4)
+    C2 = base.clone()  # deterministic: same result twice
+    fb.call("fb_gemm_bf16_splitk", M, N, K, dY.data_ptr(), M, 1, X.data_ptr(), N, 1, C2.data_ptr(), N,
+            fb.EPI["acc_f32"], ks, ws.data_ptr(), ws.numel() * 4, fb.stream_handle())
+    torch.cuda.synchronize()
+    assert torch.equal(C1, C2)

@@ -15,6 +15,7 @@ shapes = [  # name, M, N, K, a_major, b_major, epi
     ("proj2_fwd_resid", Mt, 2048, 8192, 0, 0, "resid_f32"), ("proj2_dgrad_dgelu", Mt, 8192, 2048, 0, 1, "dgelu"),
     ("fc_dgrad", Mt, 2048, 8192, 0, 1, "f32"), ("qkv_wgrad", 6144, 2048, Mt, 1, 1, "acc_f32"),
     ("proj_wgrad", 2048, 2048, Mt, 1, 1, "acc_f32"), ("head_fwd", 8192, 32000, 2048, 0, 0, "f32"),
+    ("c2_qkv_wgrad", 1536, 512, Mt, 1, 1, "acc_f32"), ("c2_proj_wgrad", 512, 512, Mt, 1, 1, "acc_f32"),
 ]
 for name, M, N, K, am, bm, epi in shapes:
     A = torch.randn((K, M) if am else (M, K), device="cuda").to(torch.bfloat16)
@@ -38,4 +39,17 @@ for name, M, N, K, am, bm, epi in shapes:
         ms = e0.elapsed_time(e1) / 10
         res["tflops_2sm" if en else "tflops_1sm"] = round(2.0 * M * N * K / ms / 1e9, 1)
     ext.call("fb_gemm_set_2sm", 1)
+    if epi == "acc_f32":
+        ws = torch.empty(16 << 20, dtype=torch.float32, device="cuda")
+        f = lambda: ext.call("fb_gemm_bf16_splitk", M, N, K, A.data_ptr(), A.stride(0), am, B.data_ptr(), B.stride(0),
+                             bm, C.data_ptr(), N, ext.EPI[epi], 0, ws.data_ptr(), ws.numel() * 4, ext.stream_handle())
+        for _ in range(3):
+            f()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            f()
+        e1.record()
+        torch.cuda.synchronize()
+        res["tflops_splitk_auto"] = round(2.0 * M * N * K / (e0.elapsed_time(e1) / 10) / 1e9, 1)
     print(json.dumps(res), flush=True)
