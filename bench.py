@@ -76,6 +76,30 @@ def ncu_traffic():
     return None, None, None
 
 
+def splitk_splits(M, N, K):
+    """Mirror of fb_gemm_bf16_splitk's auto split (csrc/gemm_sm100.cu)."""
+    tiles2 = ((M + 255) // 256) * ((N + 255) // 256)
+    num_kb = (K + 63) // 64
+    s = 1
+    while tiles2 * s < 74 and num_kb // (s + 1) >= 16:
+        s += 1
+    return s
+
+
+def launches_per_step(c):
+    """Kernel launches of our library per local step (fb_train_step), from the runtime's schedule."""
+    L, d, M = c["L"], c["d"], c["B"] * c["T"]
+    chunks = math.ceil(M / 8192)
+    # forward: gather + embed + L x (ln, qkv, attn, proj, ln, fc, proj2) + ln_f + chunks x (logits, ce, dgrad, wgrad)
+    fwd = 1 + 1 + 7 * L + 1 + 4 * chunks
+    # backward: ln_f bwd(2) + L x (dgelu, wgrad, dgrad, wgrad, ln bwd(2), dgrad, wgrad, attn bwd(3), dgrad, wgrad,
+    # ln bwd(2)) + split-K reduction launches + embed bwd
+    wg = [(d, 4 * d), (4 * d, d), (d, d), (3 * d, d)]
+    red = sum(1 for (mm, nn) in wg if splitk_splits(mm, nn, M) > 1)
+    bwd = 2 + L * (15 + red) + 1
+    return c["micro"] * (fwd + bwd) + 4  # + sumsq, step_prepare, adamw, telemetry
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -310,12 +334,7 @@ def run_ours(args, cfgname):
         "e2e": e2e,
     }
     # GPU launches of our kernels inside the timed region (per step, counted from the runtime's schedule)
-    L = c["L"]
-    chunks = math.ceil(c["B"] * c["T"] / 8192)
-    # gather + embed + L x (ln, qkv, attn, proj, ln, fc, proj2) + ln_f + chunks x (logits, ce, dgrad, wgrad)
-    # + ln_f bwd(2) + L x (6 GEMMs, 2 x ln bwd(2), attn bwd(3)) + embed bwd
-    per_micro = 1 + 1 + 7 * L + 1 + 4 * chunks + 2 + 15 * L + 1
-    out["gpu_launches"] = K * (c["micro"] * per_micro + 4)  # + sumsq, prepare, adamw, telemetry
+    out["gpu_launches"] = launches_per_step(c) * K
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(c, args.cpu_budget)
     if rank == 0:
