@@ -338,7 +338,7 @@ def run_ours(args, cfgname):
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(c, args.cpu_budget)
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     if world > 1:
         dist.destroy_process_group()
 
@@ -474,7 +474,30 @@ def run_reference(args, cfgname):
            "cpu_baseline": {**last, "value": round(v, 3)},
            "e2e": {"value": round(v, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "wall_s": round(time.perf_counter() - t0, 1)}
-    print(json.dumps(out), flush=True)
+    emit(out)
+
+
+class _StdoutToStderr:
+    """Route fd 1 to stderr while the benchmark runs (NCCL / library banners), so rank 0's
+    stdout carries exactly one JSON line."""
+
+    def __enter__(self):
+        sys.stdout.flush()
+        self.saved = os.dup(1)
+        os.dup2(2, 1)
+        return self
+
+    def __exit__(self, *exc):
+        sys.stdout.flush()
+        os.dup2(self.saved, 1)
+        os.close(self.saved)
+
+
+_result_lines = []
+
+
+def emit(obj):
+    _result_lines.append(json.dumps(obj))
 
 
 def main():
@@ -487,10 +510,13 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
-    if args.impl == "reference":
-        run_reference(args, args.config)
-    else:
-        run_ours(args, args.config)
+    with _StdoutToStderr():
+        if args.impl == "reference":
+            run_reference(args, args.config)
+        else:
+            run_ours(args, args.config)
+    for line in _result_lines:
+        print(line, flush=True)
 
 
 if __name__ == "__main__":
