@@ -1,20 +1,21 @@
 // Causal ALiBi attention FORWARD on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
 //
 // Reference: fedforge/model.py:92-98 (scores/sqrt(dh) + alibi bias, softmax, PV) with
-// slope_h = 2^(-8(h+1)/H) (model.py:46-50). Output/lse contract identical to
-// attn_fwd_kernel in attn.cu (o [B*T][d] bf16, lse2 [B][H][T] base-2).
+// slope_h = 2^(-8(h+1)/H) (model.py:46-50). Outputs: o [B*T][d] bf16 and
+// lse2 [B][H][T] (base-2 log-sum-exp, consumed by the backward).
 //
-// CTA = 128 query rows of one (b, h); KV tiles of 128 keys, causal (tiles 0..qb).
-//   warp 0     TMA producer: Q once, K/V double-buffered. One 3-D tensor map
-//              {64, B*T, 3d/64} over the qkv buffer serves Q, K and V: the smem image
-//              [dh/64][128 rows][64] is a K-major operand for Q and K and an MN-major
-//              operand for V, so no transposes are ever materialised.
-//   warp 1     TMEM owner + single-thread tcgen05.mma issuer:
-//              S = Q K^T  (M=128, N=128, K=dh)       -> TMEM cols [0,128)
-//              O_j = P V  (M=128, N=dh,  K=128 keys)  -> TMEM cols [128, 128+dh)
-//   warps 2-5  softmax: thread = query row = TMEM lane. Two passes over S in TMEM
-//              (row max, then exp2 + row sum + bf16 P into a 128B-swizzled K-major smem
-//              tile), then O_acc = O_acc * alpha + O_j in registers.
+// CTA = a PAIR of 128-row query tiles of one (b, h) (ping-pong; the last pair holds one
+// tile when T % 256 == 128), KV tiles of 64 keys, causal. Heaviest pairs launch first.
+//   warp 0     TMA producer: Q once, K and V double-buffered with separate barriers, K
+//              loaded ahead of V. One 3-D tensor map {64, B*T, 3d/64} serves K and V:
+//              the smem image [dh/64][rows][64] is K-major for K and MN-major for V, so
+//              no transposes are ever materialised.
+//   warp 1     TMEM owner + single-thread tcgen05.mma issuer. S = Q K^T for both Q tiles
+//              is issued one KV tile ahead into double-buffered TMEM columns, then
+//              O_g += P_g V (accumulated in TMEM).
+//   warps 2-5 (Q tile 0), 6-9 (Q tile 1): softmax, thread = query row = TMEM lane.
+//              exp2 with the ALiBi bias folded into one FFMA, bf16 P into a 128B-swizzled
+//              K-major smem tile, lazy (threshold 8, log2 units) in-TMEM rescale of O.
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -74,14 +75,15 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 25);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int npair = T / 256;
+  const int npair = (T + 255) / 256;
   const int pb = npair - 1 - blockIdx.x;  // heavy pairs first
   const int bh = blockIdx.y, b = bh / H, h = bh % H;
   const int d = H * DH;
   const int row0 = b * T;
   const int q0 = pb * 256;
-  const int nkv = (q0 + 256) / BN;       // KV tiles for Q tile 1
+  const bool has1 = q0 + 256 <= T;        // T % 256 == 128: the last pair has only Q tile 0
   const int nkv0 = (q0 + 128) / BN;      // KV tiles for Q tile 0
+  const int nkv = has1 ? (q0 + 256) / BN : nkv0;  // KV tiles for the whole pair
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm);
@@ -112,9 +114,9 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 0) {
     if (lane == 0) {
       const int zq = (h * DH) / 64, zk = (d + h * DH) / 64, zv = (2 * d + h * DH) / 64;
-      mbar_arrive_expect_tx(q_full, 2 * Cf::QT);
+      mbar_arrive_expect_tx(q_full, (has1 ? 2 : 1) * Cf::QT);
       tma_load_3d(smem + Cf::Q_OFF, &tmq, q_full, 0, row0 + q0, zq);
-      tma_load_3d(smem + Cf::Q_OFF + Cf::QT, &tmq, q_full, 0, row0 + q0 + 128, zq);
+      if (has1) tma_load_3d(smem + Cf::Q_OFF + Cf::QT, &tmq, q_full, 0, row0 + q0 + 128, zq);
       // K runs one tile ahead of V: order K0, K1, V0, K2, V1, ... (K stages free right after the S MMAs)
       auto load_k = [&](int j) {
         const int s = j & 1;
@@ -156,7 +158,7 @@ __global__ void __launch_bounds__(320, 1)
       auto issue_s_both = [&](int j) {  // S(j) for the active Q tiles, then release the K stage
         mbar_wait(&k_full[j & 1], (j >> 1) & 1);
         if (j < nkv0) issue_s(0, j);
-        issue_s(1, j);
+        if (has1) issue_s(1, j);
         umma_commit(&k_empty[j & 1]);
       };
       auto issue_pv = [&](int g, int j) {
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(320, 1)
       for (int j = 0; j < nkv; ++j) {
         if (j + 1 < nkv) issue_s_both(j + 1);  // run S ahead by one tile
         if (j < nkv0) issue_pv(0, j);
-        issue_pv(1, j);
+        if (has1) issue_pv(1, j);
         umma_commit(&v_empty[j & 1]);
       }
     }
@@ -187,7 +189,7 @@ __global__ void __launch_bounds__(320, 1)
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const int qi = q0 + 128 * g + r;
-    const int ntile = g ? nkv : nkv0;
+    const int ntile = g ? (has1 ? nkv : 0) : nkv0;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t tO = tmem + lane_off + 256 + DH * g;
     const float sl = use_alibi ? exp2f(-8.0f * (float)(h + 1) / (float)H) * 1.4426950408889634f : 0.0f;
@@ -269,25 +271,27 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[2 * g + bb]);
     }
-    const int jl = ntile - 1;
-    mbar_wait(&pv_done[2 * g + (jl & 1)], (jl >> 1) & 1);
-    tc_fence_after();
-    const float il = 1.0f / l;
-    __nv_bfloat16* orow = out + ((int64_t)row0 + qi) * d + h * DH;
+    if (ntile > 0) {  // warps of an absent second Q tile (T % 256 == 128) have nothing to write
+      const int jl = ntile - 1;
+      mbar_wait(&pv_done[2 * g + (jl & 1)], (jl >> 1) & 1);
+      tc_fence_after();
+      const float il = 1.0f / l;
+      __nv_bfloat16* orow = out + ((int64_t)row0 + qi) * d + h * DH;
 #pragma unroll
-    for (int c = 0; c < DH / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld_32x32b_x32(tO + c * 32, o);
-      tmem_ld_wait();
+      for (int c = 0; c < DH / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tO + c * 32, o);
+        tmem_ld_wait();
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float* f = reinterpret_cast<const float*>(o) + 8 * q;
-        uint4 pk = make_uint4(pack_bf16(f[0] * il, f[1] * il), pack_bf16(f[2] * il, f[3] * il),
-                              pack_bf16(f[4] * il, f[5] * il), pack_bf16(f[6] * il, f[7] * il));
-        *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = pk;
+        for (int q = 0; q < 4; ++q) {
+          const float* f = reinterpret_cast<const float*>(o) + 8 * q;
+          uint4 pk = make_uint4(pack_bf16(f[0] * il, f[1] * il), pack_bf16(f[2] * il, f[3] * il),
+                                pack_bf16(f[4] * il, f[5] * il), pack_bf16(f[6] * il, f[7] * il));
+          *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = pk;
+        }
       }
+      lse2[(int64_t)bh * T + qi] = m + log2f(l);
     }
-    lse2[(int64_t)bh * T + qi] = m + log2f(l);
   }
   tc_fence_before();
   __syncthreads();
@@ -330,7 +334,7 @@ int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, int B, int T, int H
   auto k = attn_fwd_tc_kernel<DH>;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  k<<<dim3(T / 256, B * H), 320, Cf::SMEM, st>>>(tmq, tm, (__nv_bfloat16*)o, lse, T, H, scale_log2, use_alibi);
+  k<<<dim3((T + 255) / 256, B * H), 320, Cf::SMEM, st>>>(tmq, tm, (__nv_bfloat16*)o, lse, T, H, scale_log2, use_alibi);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }

@@ -126,8 +126,8 @@ static int check_cfg(const fb_model_cfg& c, int B, int T) {
     return FB_UNSUPPORTED;
   }
   FB_REQUIRE(B > 0 && T >= 2 && T <= c.ctx, "sequence length %d outside [2, context_len=%d]", T, c.ctx);
-  if (T % 64) {
-    set_error("GPU path needs T %% 64 == 0 (T=%d)", T);
+  if (T % 128) {
+    set_error("GPU path needs T %% 128 == 0 (T=%d)", T);
     return FB_UNSUPPORTED;
   }
   return FB_OK;

@@ -80,8 +80,8 @@ def check_gpu_shape(cfg: TinyLMConfig, T: int | None = None) -> None:
         why.append(f"head dim {dh} not in {{64, 128}}")
     if cfg.vocab_size % 64:
         why.append(f"vocab_size={cfg.vocab_size} not a multiple of 64")
-    if T is not None and T % 64:
-        why.append(f"sequence length {T} not a multiple of 64")
+    if T is not None and T % 128:
+        why.append(f"sequence length {T} not a multiple of 128")
     if why:
         raise UnsupportedShapeError("sm_100a kernels do not implement this shape: " + "; ".join(why))
 

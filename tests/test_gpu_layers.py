@@ -37,8 +37,9 @@ def attn_ref(qkv, B, T, H, dh, use_alibi):
     return o, lse
 
 
-@pytest.mark.parametrize("B,T,H,dh,alibi", [(2, 128, 2, 64, 1), (1, 256, 3, 64, 1), (2, 64, 2, 128, 1),
-                                             (1, 512, 4, 128, 1), (2, 128, 2, 64, 0), (1, 1024, 12, 64, 1)])
+@pytest.mark.parametrize("B,T,H,dh,alibi", [(2, 128, 2, 64, 1), (1, 256, 3, 64, 1), (2, 128, 2, 128, 1),
+                                             (1, 512, 4, 128, 1), (2, 128, 2, 64, 0), (1, 1024, 12, 64, 1),
+                                             (1, 384, 2, 128, 1), (2, 640, 3, 64, 0)])
 def test_attention_fwd_bwd(fb, B, T, H, dh, alibi):
     torch.manual_seed(0)
     dev = torch.device("cuda")

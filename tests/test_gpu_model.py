@@ -18,8 +18,8 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("V,ctx,L,d,H,alibi,B,T", [(256, 128, 2, 128, 2, True, 2, 128),
-                                                   (320, 128, 1, 256, 2, True, 2, 64),
-                                                   (256, 64, 2, 192, 3, False, 3, 64),
+                                                   (320, 128, 1, 256, 2, True, 2, 128),
+                                                   (256, 384, 2, 192, 3, False, 1, 384),
                                                    (512, 256, 1, 768, 12, True, 1, 256)])
 def test_loss_and_grad_vs_oracle(V, ctx, L, d, H, alibi, B, T):
     from paper_2405_10853_b200.config import TinyLMConfig
@@ -48,9 +48,9 @@ def test_loss_and_grad_vs_oracle(V, ctx, L, d, H, alibi, B, T):
 def test_untrained_loss_is_log_vocab():
     from paper_2405_10853_b200.config import TinyLMConfig
     from paper_2405_10853_b200.model import LossEvaluator
-    cfg = TinyLMConfig(vocab_size=256, context_len=64, n_layers=2, d_model=128, n_heads=2)
+    cfg = TinyLMConfig(vocab_size=256, context_len=128, n_layers=2, d_model=128, n_heads=2)
     ev = LossEvaluator(cfg)
-    loss = ev.loss(ev.init_params(), np.random.default_rng(0).integers(0, 256, size=(4, 64)))
+    loss = ev.loss(ev.init_params(), np.random.default_rng(0).integers(0, 256, size=(4, 128)))
     assert loss == pytest.approx(math.log(256), abs=1e-3)
 
 
@@ -58,8 +58,8 @@ def test_token_range_error():
     from paper_2405_10853_b200.config import TinyLMConfig
     from paper_2405_10853_b200.errors import TokenRangeError
     from paper_2405_10853_b200.model import LossEvaluator
-    ev = LossEvaluator(TinyLMConfig(vocab_size=64, context_len=64, n_layers=1, d_model=64, n_heads=1))
-    b = np.zeros((2, 64), dtype=np.int64)
+    ev = LossEvaluator(TinyLMConfig(vocab_size=64, context_len=128, n_layers=1, d_model=64, n_heads=1))
+    b = np.zeros((2, 128), dtype=np.int64)
     b[1, 3] = 64
     with pytest.raises(TokenRangeError, match=r"row 1, position 3"):
         ev.loss(ev.init_params(), b)

@@ -52,9 +52,9 @@ def test_no_cpu_fallback():
     from paper_2405_10853_b200 import ext
     from paper_2405_10853_b200.config import TinyLMConfig
     from paper_2405_10853_b200.model import LossEvaluator
-    ev = LossEvaluator(TinyLMConfig(vocab_size=256, context_len=64, n_layers=1, d_model=128, n_heads=2), device="cpu")
+    ev = LossEvaluator(TinyLMConfig(vocab_size=256, context_len=128, n_layers=1, d_model=128, n_heads=2), device="cpu")
     with pytest.raises(ext.FedB200Error, match="B200"):
-        ev.loss(ev.init_params(), np.zeros((1, 64), dtype=np.int64))
+        ev.loss(ev.init_params(), np.zeros((1, 128), dtype=np.int64))
 
 
 def test_unsupported_shape_is_loud():
