@@ -68,13 +68,42 @@ __device__ __forceinline__ void unit_coords(int u, int num_tiles, int num_kb, in
   nkb = min(num_kb, kb0 + per) - kb0;
 }
 
-__device__ __forceinline__ float gelu_erf(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
-__device__ __forceinline__ float gelu_erf_grad(float x) {
-  const float cdf = 0.5f * (1.0f + erff(x * 0.70710678118654752f));
-  const float pdf = 0.39894228040143268f * __expf(-0.5f * x * x);
-  return cdf + x * pdf;
+// Exact-erf GELU (reference: F.gelu, fedforge/model.py:101) on the FMA pipe.
+// Phi(x) = 1 - h (x >= 0) or h (x < 0), h = erfc(|x|/sqrt2)/2 from the Chebyshev-fitted
+// erfc of Numerical Recipes (relative error < 1.2e-7 everywhere, i.e. float-exact):
+//   erfc(z) = t exp(-z^2 + P(t)), t = 1 / (1 + z/2)
+// with log2(e) and the 1/2 folded into P's coefficients so exp is one ex2. About half the
+// instructions of erff(), which mattered: the GELU GEMM runs at the power cap.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float norm_cdf(float x) {
+  const float t = rcp_approx(fmaf(fabsf(x), 0.353553391f, 1.0f));  // 1 / (1 + |x| / (2 sqrt2))
+  float q = 0.246517298f;
+  q = fmaf(q, t, -1.18611495f);
+  q = fmaf(q, t, 2.14747446f);
+  q = fmaf(q, t, -1.63775315f);
+  q = fmaf(q, t, 0.402321582f);
+  q = fmaf(q, t, -0.26875686f);
+  q = fmaf(q, t, 0.139630057f);
+  q = fmaf(q, t, 0.539700616f);
+  q = fmaf(q, t, 1.4427292f);
+  q = fmaf(q, t, -2.82574822f);                          // log2(e) * c0 - 1  (the 1/2)
+  const float h = t * ex2_approx(fmaf(x * x, -0.72134752f, q));  // - z^2 log2(e), z^2 = x^2 / 2
+  return x >= 0.f ? 1.0f - h : h;
+}
+__device__ __forceinline__ float gelu_erf(float x) { return x * norm_cdf(x); }
+__device__ __forceinline__ float gelu_erf_grad(float x) {
+  // Phi(x) + x phi(x), phi(x) = exp(-x^2/2) / sqrt(2 pi)
+  return fmaf(x, ex2_approx(fmaf(x * x, -0.72134752f, -1.32574806f)), norm_cdf(x));
+}
 
 // Process 32 consecutive columns [col, col+32) of one row held in registers.
 template <int EPI>
@@ -325,6 +354,115 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 }
 
 // ---------------------------------------------------------------------------------------
+// TMA-store epilogue (2-SM kernel). Each epilogue warp owns a 4 KB staging tile in smem:
+// its 32 TMEM lanes (= 32 output rows) x one 32-column chunk, written with 16-byte
+// st.shared in the swizzle the output tensor map uses (f32: 128 B rows, SWIZZLE_128B;
+// bf16: 64 B rows, SWIZZLE_64B -> conflict-free), then ONE cp.async.bulk.tensor store per
+// chunk and output. The TMA engine writes whole lines and clips the M / N tails, so the
+// warps never issue per-row global stores. The previous chunk's store drains (read side)
+// while the next chunk is pulled from TMEM and computed.
+constexpr int kStageEpi = 4096;
+
+__device__ __forceinline__ void stg_put_f32(uint8_t* stg, int r, int j, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(stg + r * 128 + ((j ^ (r & 7)) << 4)) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ void stg_put_bf16(uint8_t* stg, int r, int j, const float* f) {
+  *reinterpret_cast<uint4*>(stg + r * 64 + ((j ^ ((r >> 1) & 3)) << 4)) =
+      make_uint4(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]), pack_bf16(f[6], f[7]));
+}
+
+struct EpiMaps {
+  CUtensorMap C;    // {N, M, splits} box {32, 32, 1}
+  CUtensorMap Aux;  // bf16 second output (GELU pre-activation, RESID_F32_BF16 copy), {N, M, 1}
+};
+
+// One 32-column chunk of one warp: lane = row (row0 + lane), r[] = TMEM accumulator values.
+template <int EPI>
+__device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& e, const EpiMaps& mp, uint8_t* stg, int lane,
+                                                   int64_t row, int row0, int col, int split, int M, int N,
+                                                   const uint32_t (&r)[32]) {
+  float v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+  const bool in = row < M;
+  const bool full = col + 32 <= N;
+  // ---- inputs (per-row reads; the M / N tails read nothing) ----
+  if constexpr (EPI == FB_EPI_ACC_F32 || EPI == FB_EPI_RESID_F32 || EPI == FB_EPI_RESID_F32_BF16) {
+    const float* R = EPI == FB_EPI_ACC_F32 ? reinterpret_cast<const float*>(e.C) + row * e.ldc + col
+                                           : reinterpret_cast<const float*>(e.aux) + row * e.ld_aux + col;
+    if (in && full) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 c = *reinterpret_cast<const float4*>(R + 4 * q);
+        v[4 * q] += c.x; v[4 * q + 1] += c.y; v[4 * q + 2] += c.z; v[4 * q + 3] += c.w;
+      }
+    } else if (in) {
+      _Pragma("unroll") for (int i = 0; i < 32; ++i) if (col + i < N) v[i] += R[i];
+    }
+  }
+  uint32_t pre[16];  // GELU: bf16 pre-activation pairs (stored as aux_out; gelu sees the rounded value)
+  if constexpr (EPI == FB_EPI_GELU) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      pre[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
+      v[2 * i] = gelu_erf(__uint_as_float(pre[i] << 16));
+      v[2 * i + 1] = gelu_erf(__uint_as_float(pre[i] & 0xFFFF0000u));
+    }
+  } else if constexpr (EPI == FB_EPI_DGELU) {
+    const __nv_bfloat16* P = reinterpret_cast<const __nv_bfloat16*>(e.aux) + row * e.ld_aux + col;
+    if (in && full) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 pk = *reinterpret_cast<const uint4*>(P + 8 * q);
+        const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&pk);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[8 * q + i] *= gelu_erf_grad(__bfloat162float(pb[i]));
+      }
+    } else {
+      _Pragma("unroll") for (int i = 0; i < 32; ++i) v[i] = (in && col + i < N) ? v[i] * gelu_erf_grad(__bfloat162float(P[i])) : 0.f;
+    }
+  }
+  // ---- staging (the previous chunk's bulk store must have read the tile) ----
+  if (lane == 0) bulk_wait_read<0>();
+  __syncwarp();
+  constexpr bool kBf16Out = EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU;
+  if constexpr (kBf16Out) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) stg_put_bf16(stg, lane, j, v + 8 * j);
+    if constexpr (EPI == FB_EPI_GELU) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<uint4*>(stg + 2048 + lane * 64 + ((j ^ ((lane >> 1) & 3)) << 4)) =
+            make_uint4(pre[4 * j], pre[4 * j + 1], pre[4 * j + 2], pre[4 * j + 3]);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) stg_put_f32(stg, lane, j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  }
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_3d(&mp.C, stg, col, row0, split);
+#ifndef FB_EXP_NO_AUX
+    if constexpr (EPI == FB_EPI_GELU) tma_store_3d(&mp.Aux, stg + 2048, col, row0, 0);
+#endif
+    bulk_commit();
+  }
+  if constexpr (EPI == FB_EPI_RESID_F32_BF16) {  // second output reuses the tile once the f32 store read it
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) stg_put_bf16(stg, lane, j, v + 8 * j);
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(&mp.Aux, stg, col, row0, 0);
+      bulk_commit();
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // 2-SM variant: a CTA pair (cluster of 2 on one TPC) computes a 256 x 256 tile with
 // tcgen05.mma.cta_group::2 (M = 256). Each CTA stages its 128 rows of A and its 128 of
 // the 256 B rows, so per-SM operand traffic drops from 48 KB to 32 KB per 64-deep
@@ -332,17 +470,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // land in each CTA's own TMEM, and each CTA drains its own 128 rows.
 constexpr int kStages2 = 6;
 constexpr int kStage2Bytes = 2 * BM * BK * 2;  // A half + B half
-constexpr int kSmem2 = kStages2 * kStage2Bytes + 1024 + 1024;
+constexpr int kSmem2 = kStages2 * kStage2Bytes + 8 * 4096 + 1024 + 1024;  // tiles, epilogue staging, barriers, align
 
 template <int A_MN, int B_MN, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     gemm_bf16_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M,
-                         int N, int K, EpiArgs ep) {
+                         int N, int K, EpiArgs ep, const __grid_constant__ EpiMaps maps) {
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw_addr = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw_addr + 1023) & ~1023u) - raw_addr);
   uint8_t* tiles = smem;
-  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + kStages2 * kStage2Bytes);
+  uint8_t* staging = smem + kStages2 * kStage2Bytes;  // 8 epilogue warps x kStageEpi
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(staging + 8 * kStageEpi);
   uint64_t* empty_bar = full_bar + kStages2;
   uint64_t* tfull_bar = empty_bar + kStages2;
   uint64_t* tempty_bar = tfull_bar + 2;
@@ -361,6 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    tma_prefetch(&maps.C);
     for (int s = 0; s < kStages2; ++s) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
@@ -442,12 +582,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   } else {
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
+    uint8_t* stg = staging + (warp - 2) * kStageEpi;
     int it = 0;
     for (int u = cluster; u < num_tiles * ep.ksplit; u += nclusters, ++it) {
       int tile, kb0, nkb;
       unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
-      EpiArgs eu = ep;
-      eu.C = (char*)ep.C + (u / num_tiles) * ep.split_stride * (EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU ? 2 : 4);
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       const int m0 = mb * 256 + rank * 128;
@@ -456,7 +595,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const uint32_t use = it >> 1;
       mbar_wait(&tfull_bar[buf], use & 1);
       tc_fence_after();
-      const int64_t row = m0 + quad * 32 + lane;
+      const int row0 = m0 + quad * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * 256 + half * 128;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
@@ -469,9 +608,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (lane == 0) mbar_arrive_leader(&tempty_bar[buf]);
         }
         const int col = n0 + c * 32;
-        if (row < M && col < N) epilogue_chunk<EPI>(eu, row, col, N, r);
+        if (row0 < M && col < N)
+          epilogue_chunk_tma<EPI>(ep, maps, stg, lane, row0 + lane, row0, col, u / num_tiles, M, N, r);
       }
     }
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
   }
   tc_fence_before();
   cluster_sync_all();
@@ -550,9 +692,38 @@ static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, in
   return FB_OK;
 }
 
+// Output map for the TMA-store epilogue: {N, M, splits}, box {32 cols, 32 rows, 1}.
+static int make_out_map(CUtensorMap* m, void* ptr, bool bf16, int M, int N, int64_t ld, int splits,
+                        int64_t split_stride) {
+  const int es = bf16 ? 2 : 4;
+  cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)M, (cuuint64_t)splits};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * es, (cuuint64_t)(splits > 1 ? split_stride : (int64_t)M * ld) * es};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t el[3] = {1, 1, 1};
+  CUresult r = g_encode(m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr, dims,
+                        strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        bf16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(output M=%d N=%d ld=%lld) failed: %d", M, N, (long long)ld, (int)r);
+    return FB_CUDA_ERROR;
+  }
+  return FB_OK;
+}
+
 template <int A_MN, int B_MN, int EPI>
 static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiArgs& ep,
                           cudaStream_t st) {
+  constexpr bool kBf16Out = EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU;
+  EpiMaps maps;
+  int rc = make_out_map(&maps.C, ep.C, kBf16Out, M, N, ep.ldc, ep.ksplit, ep.split_stride);
+  if (rc) return rc;
+  if (EPI == FB_EPI_GELU || EPI == FB_EPI_RESID_F32_BF16) {
+    rc = make_out_map(&maps.Aux, ep.aux_out, true, M, N, EPI == FB_EPI_GELU ? ep.ld_aux : ep.ldc, 1, 0);
+    if (rc) return rc;
+  } else {
+    maps.Aux = maps.C;
+  }
   auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -561,7 +732,7 @@ static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, i
   }
   const int tiles = ((M + 255) / 256) * ((N + 255) / 256) * ep.ksplit;
   const int clusters = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
-  kern<<<2 * clusters, kGemmThreads, kSmem2, st>>>(ta, tb, M, N, K, ep);
+  kern<<<2 * clusters, kGemmThreads, kSmem2, st>>>(ta, tb, M, N, K, ep, maps);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }
@@ -622,6 +793,8 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   const bool need_aux_out = epilogue == FB_EPI_GELU || epilogue == FB_EPI_RESID_F32_BF16;
   FB_REQUIRE(!need_aux || d_aux, "gemm: epilogue %d needs aux", epilogue);
   FB_REQUIRE(!need_aux_out || d_aux_out, "gemm: epilogue %d needs aux_out", epilogue);
+  FB_REQUIRE(!need_aux_out || ((uintptr_t)d_aux_out % 16 == 0 && (epilogue != FB_EPI_GELU || ld_aux % 8 == 0)),
+             "gemm: aux_out must be 16-byte aligned with ld_aux %% 8 == 0");
   int rc = get_encoder();
   if (rc) return rc;
   // 2-SM 256x256 tiles when they fill the 74 CTA pairs; else 1-SM 128x256, else 128x128

@@ -17,7 +17,11 @@ shapes = [  # name, M, N, K, a_major, b_major, epi
     ("proj_wgrad", 2048, 2048, Mt, 1, 1, "acc_f32"), ("head_fwd", 8192, 32000, 2048, 0, 0, "f32"),
     ("c2_qkv_wgrad", 1536, 512, Mt, 1, 1, "acc_f32"), ("c2_proj_wgrad", 512, 512, Mt, 1, 1, "acc_f32"),
 ]
+ONLY = [x for x in os.environ.get("GB_ONLY", "").split(",") if x]
 for name, M, N, K, am, bm, epi in shapes:
+    if ONLY and name not in ONLY:
+        continue
+    epi = os.environ.get("GB_EPI", epi)
     A = torch.randn((K, M) if am else (M, K), device="cuda").to(torch.bfloat16)
     B = torch.randn((K, N) if bm else (N, K), device="cuda").to(torch.bfloat16)
     cdt = torch.bfloat16 if epi in ("bf16", "gelu", "dgelu") else torch.float32
