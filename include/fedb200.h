@@ -133,12 +133,17 @@ int fb_ln_bwd(const float* d_x, const float* d_gamma, const float* d_mean, const
               const float* d_dy, const float* d_dres, float* d_dx, void* d_dx_bf16,
               float* d_dgamma, float* d_dbeta, float* d_work, int rows, int d, void* stream);
 /* Causal attention with the reference's ALiBi slopes 2^(-8(h+1)/H) (model.py:46-65, 92-98).
- * qkv: [B*T][3d] bf16 (q|k|v, head h at columns h*dh); o: [B*T][d] bf16; lse: [B][H][T] f32 */
-int fb_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int H, int dh,
-                int use_alibi, void* stream);
+ * qkv: [B*T][3d] bf16 (q|k|v, head h at columns h*dh); o: [B*T][d] bf16; lse: [B][H][T] f32
+ * (base 2). d_live (optional, uint8 [B][H][T/128][T/64]): the forward marks each causal
+ * block of 128 queries x 64 keys live (1) or dead (0: every softmax weight underflowed to
+ * exactly 0, which ALiBi causes far from the diagonal) and skips the dead blocks' PV; the
+ * backward skips the MMAs of blocks the map says are dead. Results are bit-identical with
+ * and without the map. T % 128 == 0, dh in {64, 128}. */
+int fb_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, uint8_t* d_live, int B, int T, int H,
+                int dh, int use_alibi, void* stream);
 int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
-                void* d_dqkv, float* d_work, int B, int T, int H, int dh, int use_alibi,
-                void* stream);
+                const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh,
+                int use_alibi, void* stream);
 /* Mean next-token CE over B*(T-1) positions (model.py:226-229): logits f32 [rows][V]
  * for a chunk of rows [row0, row0+rows) of a B x T batch; writes dlogits(bf16) =
  * scale*(softmax - onehot) (0 on each sequence's last position) and adds the summed

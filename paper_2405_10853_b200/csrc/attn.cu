@@ -55,14 +55,15 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16*
 }
 
 template <int DH>
-int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, int B, int T, int H, int use_alibi, cudaStream_t st);
+int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, uint8_t* live, int B, int T, int H, int use_alibi,
+                       cudaStream_t st);
 template <int DH>
-int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const float* Dbuf, float* dq, void* dqkv,
-                       int B, int T, int H, int use_alibi, cudaStream_t st);
+int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live, const float* Dbuf,
+                       float* dq, void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st);
 
 template <int DH>
-static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const float* lse, void* dqkv, float* work,
-                           int B, int T, int H, int use_alibi, cudaStream_t st) {
+static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const float* lse, const uint8_t* live,
+                           void* dqkv, float* work, int B, int T, int H, int use_alibi, cudaStream_t st) {
   const int d = H * DH;
   float* Dbuf = work;
   float* dq = work + (int64_t)B * H * T;
@@ -70,7 +71,7 @@ static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const
   attn_bwd_dot_kernel<<<(nw + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dO, Dbuf, dq, B, T, H,
                                                     DH);
   FB_LAUNCH_CHECK();
-  int rc = attn_bwd_tc_launch<DH>(qkv, dO, lse, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
+  int rc = attn_bwd_tc_launch<DH>(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
   if (rc) return rc;
   dq_finalize_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq, (__nv_bfloat16*)dqkv, B * T, d);
   FB_LAUNCH_CHECK();
@@ -81,32 +82,33 @@ static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const
 
 using namespace fb;
 
-extern "C" int fb_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, int B, int T, int H, int dh, int use_alibi,
-                           void* stream) {
+extern "C" int fb_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, uint8_t* d_live, int B, int T, int H, int dh,
+                           int use_alibi, void* stream) {
   FB_REQUIRE(B > 0 && H > 0 && T > 0 && T % 128 == 0, "attn_fwd: T must be a positive multiple of 128 (T=%d)", T);
   cudaStream_t st = (cudaStream_t)stream;
   // algorithmic flops: causal lower triangle, QK^T and PV (2*T*d per layer-token fwd)
   const double fl = 2.0 * 2.0 * B * H * (double)T * (T + 1) / 2.0 * dh;
   const int pi = prof_on() ? prof_start(1, st) : -1;
   int rc = FB_UNSUPPORTED;
-  if (dh == 64) rc = attn_fwd_tc_launch<64>(d_qkv, d_o, d_lse, B, T, H, use_alibi, st);
-  else if (dh == 128) rc = attn_fwd_tc_launch<128>(d_qkv, d_o, d_lse, B, T, H, use_alibi, st);
+  if (dh == 64) rc = attn_fwd_tc_launch<64>(d_qkv, d_o, d_lse, d_live, B, T, H, use_alibi, st);
+  else if (dh == 128) rc = attn_fwd_tc_launch<128>(d_qkv, d_o, d_lse, d_live, B, T, H, use_alibi, st);
   prof_stop(1, pi, st, fl);
   if (rc != FB_UNSUPPORTED) return rc;
   set_error("attn_fwd: head dim %d unsupported (64 or 128)", dh);
   return FB_UNSUPPORTED;
 }
 
-extern "C" int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse, void* d_dqkv,
-                           float* d_work, int B, int T, int H, int dh, int use_alibi, void* stream) {
+extern "C" int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
+                           const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh, int use_alibi,
+                           void* stream) {
   FB_REQUIRE(B > 0 && H > 0 && T > 0 && T % 128 == 0, "attn_bwd: T must be a positive multiple of 128 (T=%d)", T);
   FB_REQUIRE(d_work != nullptr, "attn_bwd: needs a work buffer of B*H*T + B*T*H*dh floats");
   cudaStream_t st = (cudaStream_t)stream;
   const double fl = 2.0 * 2.0 * 2.0 * B * H * (double)T * (T + 1) / 2.0 * dh;  // bwd = 2x fwd
   const int pi = prof_on() ? prof_start(2, st) : -1;
   int rc = FB_UNSUPPORTED;
-  if (dh == 64) rc = attn_bwd_launch<64>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, H, use_alibi, st);
-  else if (dh == 128) rc = attn_bwd_launch<128>(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, H, use_alibi, st);
+  if (dh == 64) rc = attn_bwd_launch<64>(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, use_alibi, st);
+  else if (dh == 128) rc = attn_bwd_launch<128>(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, use_alibi, st);
   prof_stop(2, pi, st, fl);
   if (rc != FB_UNSUPPORTED) return rc;
   set_error("attn_bwd: head dim %d unsupported (64 or 128)", dh);

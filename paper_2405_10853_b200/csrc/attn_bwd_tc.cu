@@ -42,6 +42,30 @@ __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, 
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
 
+// Live query tiles of one key block, from the forward's dead-block map (attn_tc.cu): a
+// forward block (128 queries x 64 keys) whose every p was exactly 0 has P = 0 and dS = 0
+// here too (lse >= the forward's running max), so its MMAs and exps are skipped. Warp 0
+// ballots the map into a compact list tl[0..n) of tile offsets from `first`; every role then
+// walks the same list. qshift: log2(query tile / 128) + 1 maps a tile to its forward row
+// block (64-row tiles: >> 1, 128-row tiles: >> 0).
+__device__ __forceinline__ void build_live_list(const uint8_t* __restrict__ live, int bh, int T, int kb, int first,
+                                                int ntiles, int qshift, uint8_t* tl, uint32_t* nlive) {
+  const int lane = threadIdx.x & 31;
+  int n = 0;
+  for (int base = 0; base < ntiles; base += 32) {
+    const int t = base + lane;
+    bool ok = t < ntiles;
+    if (ok && live) {
+      const uint8_t* row = live + ((int64_t)bh * (T / 128) + ((first + t) >> qshift)) * (T / 64) + 2 * kb;
+      ok = (row[0] | row[1]) != 0;
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, ok);
+    if (ok) tl[n + __popc(m & ((1u << lane) - 1u))] = (uint8_t)t;
+    n += __popc(m);
+  }
+  if (lane == 0) *nlive = (uint32_t)n;
+}
+
 // ---------------------------------------------------------------------------------------
 // dh = 128 variant with 64-query tiles and a software pipeline across query tiles:
 //   MMA order per tile t:  [pds_full(t)]  S^T(t+1), dP^T(t+1)  dV(t)  dK(t)  [dq_empty(t-1)] dQ^T(t)
@@ -64,13 +88,14 @@ struct AttnBwd64Cfg {
   static constexpr int X_OFF = S_OFF + 2 * PT;   // dQ staging: 64 rows x 128 f32
   static constexpr int L_OFF = X_OFF + 64 * DH * 4;  // e[2][64], D[2][64]
   static constexpr int BAR_OFF = L_OFF + 4 * 64 * 4;
-  static constexpr int SMEM = BAR_OFF + 192 + 1024;
+  static constexpr int SMEM = BAR_OFF + 512 + 1024;  // mbarriers, TMEM slot, live count + list; align
+  static_assert(SMEM <= 232448, "attention bwd (dh 128) smem");
 };
 
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_tc64_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
-                         const float* __restrict__ lse2, const float* __restrict__ Dd,
+                         const float* __restrict__ lse2, const uint8_t* __restrict__ live, const float* __restrict__ Dd,
                          __nv_bfloat16* __restrict__ dqkv, int T, int H, float scale_log2, float scale, int use_alibi) {
   using Cf = AttnBwd64Cfg;
   constexpr int DH = Cf::DH;
@@ -89,6 +114,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* dq_full = bar + 13;
   uint64_t* dq_empty = bar + 14;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint32_t* nlive_p = tmem_slot + 1;
+  uint8_t* tl = reinterpret_cast<uint8_t*>(tmem_slot + 2);
   float* sE0 = reinterpret_cast<float*>(smem + Cf::L_OFF);  // e[2][64] (double-buffered)
   float* sD0 = sE0 + 128;                                     // D[2][64]
 
@@ -119,11 +146,13 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(dq_empty, 8);
     fence_barrier_init();
   }
+  if (warp == 2) build_live_list(live, bh, T, kb, first, ntiles, 1, tl, nlive_p);
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int nlive = (int)*nlive_p;
   const uint32_t sK = smem_u32(smem + Cf::K_OFF), sV = smem_u32(smem + Cf::V_OFF), sQ0 = smem_u32(smem + Cf::Q_OFF),
                  sO0 = smem_u32(smem + Cf::O_OFF), sP0 = smem_u32(smem + Cf::P_OFF), sS0 = smem_u32(smem + Cf::S_OFF),
                  sX = smem_u32(smem + Cf::X_OFF);
@@ -134,10 +163,10 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive_expect_tx(kv_full, 2 * Cf::KT);
       tma_load_3d(smem + Cf::K_OFF, &tm_kv, kv_full, 0, row0 + k0, zk);
       tma_load_3d(smem + Cf::V_OFF, &tm_kv, kv_full, 0, row0 + k0, zv);
-      for (int t = 0; t < ntiles; ++t) {
+      for (int t = 0; t < nlive; ++t) {
         const int s = t & 1;
         const uint32_t ph = (t >> 1) & 1;
-        const int q0 = (first + t) * 64;
+        const int q0 = (first + tl[t]) * 64;
         mbar_wait(&q_empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&q_full[s], Cf::QT);
         tma_load_3d(smem + Cf::Q_OFF + s * Cf::QT, &tm_q, &q_full[s], 0, row0 + q0, zq);
@@ -168,16 +197,16 @@ __global__ void __launch_bounds__(320, 1)
         }
         umma_commit(s_full);
       };
-      mbar_wait(kv_full, 0);
-      issue_sp(0);
-      for (int t = 0; t < ntiles; ++t) {
+      mbar_wait(kv_full, 0);  // also when no tile is live: the K/V loads must land before exit
+      if (nlive > 0) issue_sp(0);
+      for (int t = 0; t < nlive; ++t) {
         const int s = t & 1;
         const uint32_t ph = t & 1;
         const uint32_t sQ = sQ0 + s * Cf::QT, sO = sO0 + s * Cf::QT;
         const uint32_t sP = sP0 + s * Cf::PT, sS = sS0 + s * Cf::PT;
         mbar_wait(pds_full, ph);  // S^T/dP^T(t) consumed; P^T(t), dS^T(t) in smem
         TRACE(16 * t + 0);
-        if (t + 1 < ntiles) issue_sp(t + 1);
+        if (t + 1 < nlive) issue_sp(t + 1);
         TRACE(16 * t + 1);
         tc_fence_after();
 #pragma unroll
@@ -214,7 +243,7 @@ __global__ void __launch_bounds__(320, 1)
     const int tid = threadIdx.x - 64;  // 0..255
     float* Xs = reinterpret_cast<float*>(smem + Cf::X_OFF);
     auto drain = [&](int t) {  // dQ^T(t) -> staging [64 q][128 dh] -> TMA reduce-add into dq rows
-      const int q0 = (first + t) * 64;
+      const int q0 = (first + tl[t]) * 64;
       mbar_wait(dq_full, t & 1);
       tc_fence_after();
       uint32_t v[32];
@@ -242,19 +271,19 @@ __global__ void __launch_bounds__(320, 1)
     // e/D of tile t live in buffer t & 1; tile t+1's are prefetched before drain(t-1), whose
     // CTA-wide barriers publish them (all readers of that buffer finished tile t-1 earlier)
     auto load_ed = [&](int t) {
-      const int q0 = (first + t) * 64;
+      const int q0 = (first + tl[t]) * 64;
       float* E = sE0 + (t & 1) * 64;
       float* Dv = sD0 + (t & 1) * 64;
       if (tid < 64) E[tid] = sl * (float)(q0 + tid) + lse2[(int64_t)bh * T + q0 + tid];
       else if (tid < 128) Dv[tid - 64] = Dd[(int64_t)bh * T + q0 + tid - 64];
     };
-    load_ed(0);
+    if (nlive > 0) load_ed(0);
     asm volatile("bar.sync 1, 256;" ::: "memory");
-    for (int t = 0; t < ntiles; ++t) {
+    for (int t = 0; t < nlive; ++t) {
       const int s = t & 1;
       const uint32_t ph = t & 1;
-      const int q0 = (first + t) * 64;
-      const bool diag = (t < 2);
+      const int q0 = (first + tl[t]) * 64;
+      const bool diag = (tl[t] < 2);  // the two 64-row tiles that cross the key block's diagonal
       const float* sE = sE0 + (t & 1) * 64;
       const float* sD = sD0 + (t & 1) * 64;
       if (warp == 2 && lane == 0) TRACE(16 * t + 4);
@@ -296,12 +325,12 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(pds_full);
       if (warp == 2 && lane == 0) TRACE(16 * t + 6);
-      if (t + 1 < ntiles) load_ed(t + 1);
+      if (t + 1 < nlive) load_ed(t + 1);
       if (t > 0) drain(t - 1);  // overlaps the MMAs of tile t
       else asm volatile("bar.sync 1, 256;" ::: "memory");  // publish e/D(1) on the first tile
       if (warp == 2 && lane == 0) TRACE(16 * t + 7);
     }
-    drain(ntiles - 1);
+    if (nlive > 0) drain(nlive - 1);
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     // dK, dV (the last dK/dV MMAs completed before the last dq_full)
     const int64_t ld = 3 * (int64_t)d;
@@ -314,6 +343,10 @@ __global__ void __launch_bounds__(320, 1)
       tmem_ld_32x32b_x32(tmem + 384 + lane_off + col, kv);
       tmem_ld_32x32b_x32(tmem + 256 + lane_off + col, vv);
       tmem_ld_wait();
+      if (nlive == 0) {  // every query of this key block was dead: dK = dV = 0
+#pragma unroll
+        for (int i = 0; i < 32; ++i) kv[i] = vv[i] = 0u;
+      }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float* fk = reinterpret_cast<const float*>(kv) + 8 * q;
@@ -352,13 +385,15 @@ struct AttnBwdD64Cfg {
   static constexpr int X_OFF = P_OFF + 2 * PT;   // dQ staging: 2 boxes of 128 rows x 32 f32 (swizzled)
   static constexpr int L_OFF = X_OFF + 128 * DH * 4;
   static constexpr int BAR_OFF = L_OFF + 2 * 128 * 4;
-  static constexpr int SMEM = BAR_OFF + 192 + 1024;
+  static constexpr int SMEM = BAR_OFF + 512 + 1024;
+  static_assert(SMEM <= 232448, "attention bwd (dh 64) smem");
 };
 
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_tcd64_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
                           const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2,
-                          const float* __restrict__ Dd, __nv_bfloat16* __restrict__ dqkv, int T, int H,
+                          const uint8_t* __restrict__ live, const float* __restrict__ Dd,
+                          __nv_bfloat16* __restrict__ dqkv, int T, int H,
                           float scale_log2, float scale, int use_alibi) {
   using Cf = AttnBwdD64Cfg;
   constexpr int DH = Cf::DH;
@@ -379,6 +414,8 @@ __global__ void __launch_bounds__(320, 1)
   uint64_t* p_free = bar + 15;
   uint64_t* ds_full = bar + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
+  uint32_t* nlive_p = tmem_slot + 1;
+  uint8_t* tl = reinterpret_cast<uint8_t*>(tmem_slot + 2);
   float* sE = reinterpret_cast<float*>(smem + Cf::L_OFF);
   float* sD = sE + 128;
 
@@ -410,11 +447,13 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(dq_empty, 8);
     fence_barrier_init();
   }
+  if (warp == 2) build_live_list(live, bh, T, kb, first, ntiles, 0, tl, nlive_p);
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const int nlive = (int)*nlive_p;
   const uint32_t sK = smem_u32(smem + Cf::K_OFF), sV = smem_u32(smem + Cf::V_OFF), sQ0 = smem_u32(smem + Cf::Q_OFF),
                  sO0 = smem_u32(smem + Cf::O_OFF), sP0 = smem_u32(smem + Cf::P_OFF), sX = smem_u32(smem + Cf::X_OFF);
 
@@ -424,10 +463,10 @@ __global__ void __launch_bounds__(320, 1)
       mbar_arrive_expect_tx(kv_full, 2 * Cf::KT);
       tma_load_3d(smem + Cf::K_OFF, &tm_qkv, kv_full, 0, row0 + k0, zk);
       tma_load_3d(smem + Cf::V_OFF, &tm_qkv, kv_full, 0, row0 + k0, zv);
-      for (int t = 0; t < ntiles; ++t) {
+      for (int t = 0; t < nlive; ++t) {
         const int s = t & 1;
         const uint32_t ph = (t >> 1) & 1;
-        const int q0 = (first + t) * 128;
+        const int q0 = (first + tl[t]) * 128;
         mbar_wait(&q_empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&q_full[s], Cf::QT);
         tma_load_3d(smem + Cf::Q_OFF + s * Cf::QT, &tm_qkv, &q_full[s], 0, row0 + q0, zq);
@@ -457,15 +496,15 @@ __global__ void __launch_bounds__(320, 1)
         }
         umma_commit(s_full);
       };
-      mbar_wait(kv_full, 0);
-      issue_sp(0);
-      for (int t = 0; t < ntiles; ++t) {
+      mbar_wait(kv_full, 0);  // also when no tile is live: the K/V loads must land before exit
+      if (nlive > 0) issue_sp(0);
+      for (int t = 0; t < nlive; ++t) {
         const int s = t & 1;
         const uint32_t ph = t & 1;
         const uint32_t sQ = sQ0 + s * Cf::QT, sO = sO0 + s * Cf::QT;
         const uint32_t sP = sP0 + s * Cf::PT, sS = sP;  // dS^T overwrites P^T after dV
         mbar_wait(p_full, ph);
-        if (t + 1 < ntiles) issue_sp(t + 1);
+        if (t + 1 < nlive) issue_sp(t + 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // dV += P^T dO  (K = 128 queries)
@@ -505,7 +544,7 @@ __global__ void __launch_bounds__(320, 1)
     const int tid = threadIdx.x - 64;
     const uint32_t xbox = sX + g * 16384;  // this warpgroup's 128 x 32 f32 staging box
     auto drain = [&](int t) {
-      const int q0 = (first + t) * 128;
+      const int q0 = (first + tl[t]) * 128;
       mbar_wait(dq_full, t & 1);
       tc_fence_after();
       uint32_t v[32];
@@ -534,11 +573,11 @@ __global__ void __launch_bounds__(320, 1)
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
-    for (int t = 0; t < ntiles; ++t) {
+    for (int t = 0; t < nlive; ++t) {
       const int s = t & 1;
       const uint32_t ph = t & 1;
-      const int q0 = (first + t) * 128;
-      const bool diag = (t == 0);
+      const int q0 = (first + tl[t]) * 128;
+      const bool diag = (tl[t] == 0);
       asm volatile("bar.sync 1, 256;" ::: "memory");
       if (tid < 128) sE[tid] = sl * (float)(q0 + tid) + lse2[(int64_t)bh * T + q0 + tid];
       else sD[tid - 128] = Dd[(int64_t)bh * T + q0 + tid - 128];
@@ -594,7 +633,7 @@ __global__ void __launch_bounds__(320, 1)
       if (lane == 0) mbar_arrive(ds_full);
       if (t > 0) drain(t - 1);
     }
-    drain(ntiles - 1);
+    if (nlive > 0) drain(nlive - 1);
     if (quad == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     const int64_t ld = 3 * (int64_t)d;
     __nv_bfloat16* dkrow = dqkv + ((int64_t)row0 + kj) * ld + d + h * DH + 32 * g;
@@ -603,6 +642,10 @@ __global__ void __launch_bounds__(320, 1)
     tmem_ld_32x32b_x32(tmem + 384 + lane_off + 32 * g, kv);
     tmem_ld_32x32b_x32(tmem + 320 + lane_off + 32 * g, vv);
     tmem_ld_wait();
+    if (nlive == 0) {  // every query of this key block was dead: dK = dV = 0
+#pragma unroll
+      for (int i = 0; i < 32; ++i) kv[i] = vv[i] = 0u;
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const float* fk = reinterpret_cast<const float*>(kv) + 8 * q;
@@ -654,7 +697,8 @@ static int encode_box(CUtensorMap* m, const void* base, int64_t rows, int cols, 
   return FB_OK;
 }
 
-static int attn_bwd_tc64_launch(const void* qkv, const void* dO, const float* lse, const float* Dbuf, float* dq,
+static int attn_bwd_tc64_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live,
+                                const float* Dbuf, float* dq,
                                 void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
   using Cf = AttnBwd64Cfg;
   constexpr int DH = 128;
@@ -682,13 +726,14 @@ static int attn_bwd_tc64_launch(const void* qkv, const void* dO, const float* ls
   auto k = attn_bwd_tc64_kernel;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale = 1.0f / sqrtf((float)DH);
-  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tkv, tq, to, tdq, lse, Dbuf, (__nv_bfloat16*)dqkv, T, H,
+  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tkv, tq, to, tdq, lse, live, Dbuf, (__nv_bfloat16*)dqkv, T, H,
                                                  1.4426950408889634f * scale, scale, use_alibi);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }
 
-static int attn_bwd_tcd64_launch(const void* qkv, const void* dO, const float* lse, const float* Dbuf, float* dq,
+static int attn_bwd_tcd64_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live,
+                                 const float* Dbuf, float* dq,
                                  void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
   using Cf = AttnBwdD64Cfg;
   constexpr int DH = 64;
@@ -714,15 +759,15 @@ static int attn_bwd_tcd64_launch(const void* qkv, const void* dO, const float* l
   auto k = attn_bwd_tcd64_kernel;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale = 1.0f / sqrtf((float)DH);
-  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tq, to, tdq, lse, Dbuf, (__nv_bfloat16*)dqkv, T, H,
+  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tq, to, tdq, lse, live, Dbuf, (__nv_bfloat16*)dqkv, T, H,
                                                  1.4426950408889634f * scale, scale, use_alibi);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }
 
 template <int DH>
-int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const float* Dbuf, float* dq, void* dqkv,
-                       int B, int T, int H, int use_alibi, cudaStream_t st) {
+int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live, const float* Dbuf,
+                       float* dq, void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
   if (!g_enc_bwd) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -733,15 +778,16 @@ int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const 
     }
     g_enc_bwd = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  if (DH == 128) return attn_bwd_tc64_launch(qkv, dO, lse, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
-  if (DH == 64) return attn_bwd_tcd64_launch(qkv, dO, lse, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
+  FB_REQUIRE(T <= 16384, "attn_bwd: T=%d above 16384", T);
+  if (DH == 128) return attn_bwd_tc64_launch(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
+  if (DH == 64) return attn_bwd_tcd64_launch(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
   return FB_UNSUPPORTED;
 }
 
-template int attn_bwd_tc_launch<64>(const void*, const void*, const float*, const float*, float*, void*, int, int, int,
-                                    int, cudaStream_t);
-template int attn_bwd_tc_launch<128>(const void*, const void*, const float*, const float*, float*, void*, int, int,
-                                     int, int, cudaStream_t);
+template int attn_bwd_tc_launch<64>(const void*, const void*, const float*, const uint8_t*, const float*, float*,
+                                    void*, int, int, int, int, cudaStream_t);
+template int attn_bwd_tc_launch<128>(const void*, const void*, const float*, const uint8_t*, const float*, float*,
+                                     void*, int, int, int, int, cudaStream_t);
 
 }  // namespace fb
 

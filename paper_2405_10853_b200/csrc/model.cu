@@ -64,6 +64,7 @@ struct Arena {
 struct Acts {  // per-layer saved activations
   float *x_in, *mean1, *rstd1, *x_mid, *mean2, *rstd2, *lse;
   __nv_bfloat16 *ln1, *qkv, *ao, *ln2, *pre, *act;
+  uint8_t* live;  // attention dead-block map [B][H][T/128][T/64] (forward writes, backward reads)
 };
 
 // split-K partials of the weight-gradient GEMMs: auto-split stops once the 74 CTA pairs are
@@ -89,6 +90,7 @@ static WS carve(const fb_model_cfg& c, int B, int T, Arena& A) {
     a.qkv = A.take<__nv_bfloat16>(M * 3 * d);
     a.ao = A.take<__nv_bfloat16>(M * d);
     a.lse = A.take<float>(B * H * T);
+    a.live = A.take<uint8_t>((int64_t)B * H * (T / 128) * (T / 64));
     a.x_mid = A.take<float>(M * d);
     a.mean2 = A.take<float>(M);
     a.rstd2 = A.take<float>(M);
@@ -179,7 +181,7 @@ extern "C" int fb_model_fwd_bwd(const fb_model_cfg* cfgp, const float* P, const 
     float* x_next = (l + 1 < c.n_layers) ? w.L[l + 1].x_in : w.x_out;
     TRY(fb_ln_fwd(a.x_in, P + b.ln1_w, P + b.ln1_b, a.ln1, a.mean1, a.rstd1, M, d, st));
     TRY(fb_gemm_bf16(M, 3 * d, d, a.ln1, d, 0, S + b.qkv, d, 0, a.qkv, 3 * d, FB_EPI_BF16, nullptr, nullptr, 0, st));
-    TRY(fb_attn_fwd(a.qkv, a.ao, a.lse, B, T, H, dh, c.use_alibi, st));
+    TRY(fb_attn_fwd(a.qkv, a.ao, a.lse, a.live, B, T, H, dh, c.use_alibi, st));
     TRY(fb_gemm_bf16(M, d, d, a.ao, d, 0, S + b.proj, d, 0, a.x_mid, d, FB_EPI_RESID_F32, a.x_in, nullptr, d, st));
     TRY(fb_ln_fwd(a.x_mid, P + b.ln2_w, P + b.ln2_b, a.ln2, a.mean2, a.rstd2, M, d, st));
     TRY(fb_gemm_bf16(M, 4 * d, d, a.ln2, d, 0, S + b.fc, d, 0, a.act, 4 * d, FB_EPI_GELU, nullptr, a.pre, 4 * d, st));
@@ -225,7 +227,7 @@ extern "C" int fb_model_fwd_bwd(const fb_model_cfg* cfgp, const float* P, const 
     // attention: x_mid = x_in + proj(attn(ln1(x_in)))
     TRY(fb_gemm_bf16(M, d, d, w.dxb, d, 0, S + b.proj, d, 1, w.dao, d, FB_EPI_BF16, nullptr, nullptr, 0, st));
     TRY(wgrad(d, d, w.dxb, d, a.ao, d, G + b.proj));
-    TRY(fb_attn_bwd(a.qkv, a.ao, w.dao, a.lse, w.dqkv, w.attn_work, B, T, H, dh, c.use_alibi, st));
+    TRY(fb_attn_bwd(a.qkv, a.ao, w.dao, a.lse, a.live, w.dqkv, w.attn_work, B, T, H, dh, c.use_alibi, st));
     TRY(fb_gemm_bf16(M, d, 3 * d, w.dqkv, 3 * d, 0, S + b.qkv, d, 1, w.dln, d, FB_EPI_F32, nullptr, nullptr, 0, st));
     TRY(wgrad(3 * d, d, w.dqkv, 3 * d, a.ln1, d, G + b.qkv));
     TRY(fb_ln_bwd(a.x_in, P + b.ln1_w, a.mean1, a.rstd1, w.dln, w.dx, w.dx, w.dxb, G + b.ln1_w, G + b.ln1_b,

@@ -49,8 +49,8 @@ SIGNATURES = {
     "fb_embed_bwd": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp],
     "fb_ln_fwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp],
     "fb_ln_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp],
-    "fb_attn_fwd": [_vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
-    "fb_attn_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
+    "fb_attn_fwd": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
+    "fb_attn_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "fb_ce_fwd_bwd": [_vp, _vp, _vp, _i, _i, _i, _i, C.c_float, _vp, _vp],
     "fb_gather_batch": [_vp, _vp, _i64, _i64, _i, _i, _vp, _vp],
     "fb_profile_begin": [_i],

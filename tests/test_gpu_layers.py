@@ -47,7 +47,9 @@ def test_attention_fwd_bwd(fb, B, T, H, dh, alibi):
     qkv = torch.randn(B * T, 3 * d, device=dev).to(torch.bfloat16)
     o = torch.empty(B * T, d, dtype=torch.bfloat16, device=dev)
     lse2 = torch.empty(B * H * T, dtype=torch.float32, device=dev)
-    fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), B, T, H, dh, alibi, fb.stream_handle())
+    live = torch.empty(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device=dev)
+    fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), live.data_ptr(), B, T, H, dh, alibi,
+            fb.stream_handle())
     q32 = qkv.float().requires_grad_()
     o_ref, lse_ref = attn_ref(q32, B, T, H, dh, alibi)
     torch.cuda.synchronize()
@@ -57,8 +59,8 @@ def test_attention_fwd_bwd(fb, B, T, H, dh, alibi):
     o_ref.backward(do.float())
     dqkv = torch.empty_like(qkv)
     work = torch.empty(B * H * T + B * T * d, dtype=torch.float32, device=dev)
-    fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse2.data_ptr(), dqkv.data_ptr(),
-            work.data_ptr(), B, T, H, dh, alibi, fb.stream_handle())
+    fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse2.data_ptr(), live.data_ptr(),
+            dqkv.data_ptr(), work.data_ptr(), B, T, H, dh, alibi, fb.stream_handle())
     torch.cuda.synchronize()
     g = q32.grad
     for sl, name in [(slice(0, d), "dq"), (slice(d, 2 * d), "dk"), (slice(2 * d, 3 * d), "dv")]:
@@ -67,6 +69,65 @@ def test_attention_fwd_bwd(fb, B, T, H, dh, alibi):
         err = (got - ref).abs().max().item()
         scale = ref.abs().max().item()
         assert err <= 3e-2 * scale + 1e-2, (name, err, scale)
+
+
+def _attn_run(fb, qkv, do, B, T, H, dh, live):
+    d = H * dh
+    dev = qkv.device
+    o = torch.empty(B * T, d, dtype=torch.bfloat16, device=dev)
+    lse2 = torch.empty(B * H * T, dtype=torch.float32, device=dev)
+    dqkv = torch.empty_like(qkv)
+    work = torch.empty(B * H * T + B * T * d, dtype=torch.float32, device=dev)
+    lp = live.data_ptr() if live is not None else None
+    fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), lp, B, T, H, dh, 1, fb.stream_handle())
+    fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse2.data_ptr(), lp, dqkv.data_ptr(),
+            work.data_ptr(), B, T, H, dh, 1, fb.stream_handle())
+    torch.cuda.synchronize()
+    return o, lse2, dqkv
+
+
+@pytest.mark.parametrize("B,T,H,dh", [(2, 2048, 16, 128), (1, 1024, 12, 64), (1, 1408, 16, 128)])
+def test_attention_dead_block_skip_is_exact(fb, B, T, H, dh):
+    """ALiBi drives far-from-diagonal softmax weights to exactly 0 (ex2 flush); the forward
+    marks those blocks dead and skips their PV, the backward skips their MMAs. The outputs
+    must be bit-identical to the run without the map, and the map must hold dead blocks."""
+    torch.manual_seed(5)
+    dev = torch.device("cuda")
+    d = H * dh
+    qkv = torch.randn(B * T, 3 * d, device=dev).to(torch.bfloat16)
+    do = torch.randn(B * T, d, device=dev).to(torch.bfloat16)
+    live = torch.full((B * H * (T // 128) * (T // 64),), 7, dtype=torch.uint8, device=dev)
+    o1, l1, g1 = _attn_run(fb, qkv, do, B, T, H, dh, live)
+    o0, l0, g0 = _attn_run(fb, qkv, do, B, T, H, dh, None)
+    assert torch.equal(o1, o0) and torch.equal(l1, l0) and torch.equal(g1, g0)
+    m = live.view(B, H, T // 128, T // 64).cpu().numpy()
+    causal = np.array([[kt <= 2 * qt + 1 for kt in range(T // 64)] for qt in range(T // 128)])
+    vals = m[:, :, causal]
+    assert set(np.unique(vals)) <= {0, 1}
+    dead = (vals == 0).mean()
+    assert dead > 0.05, dead  # steep heads: most far blocks are dead
+    # the diagonal blocks are always live
+    for qt in range(T // 128):
+        assert (m[:, :, qt, 2 * qt + 1] == 1).all()
+
+
+def test_attention_bwd_all_dead_map_zeroes(fb):
+    """A map that marks every block dead: the backward must finish and produce exact zeros."""
+    B, T, H, dh = 1, 256, 2, 128
+    dev = torch.device("cuda")
+    d = H * dh
+    qkv = torch.randn(B * T, 3 * d, device=dev).to(torch.bfloat16)
+    do = torch.randn(B * T, d, device=dev).to(torch.bfloat16)
+    o = torch.empty(B * T, d, dtype=torch.bfloat16, device=dev)
+    lse2 = torch.empty(B * H * T, dtype=torch.float32, device=dev)
+    fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), None, B, T, H, dh, 1, fb.stream_handle())
+    live = torch.zeros(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device=dev)
+    dqkv = torch.full_like(qkv, 3.0)
+    work = torch.empty(B * H * T + B * T * d, dtype=torch.float32, device=dev)
+    fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse2.data_ptr(), live.data_ptr(),
+            dqkv.data_ptr(), work.data_ptr(), B, T, H, dh, 1, fb.stream_handle())
+    torch.cuda.synchronize()
+    assert (dqkv.float() == 0).all()
 
 
 @pytest.mark.parametrize("rows,d", [(256, 512), (100, 768), (64, 2048), (33, 128)])

@@ -14,12 +14,13 @@ for B, T, H, dh in [(8, 2048, 16, 128), (8, 2048, 12, 64), (16, 1024, 8, 64)]:
     qkv = torch.randn(B * T, 3 * d, device="cuda").to(torch.bfloat16)
     o = torch.empty(B * T, d, dtype=torch.bfloat16, device="cuda")
     lse = torch.empty(B * H * T, device="cuda")
+    live = torch.empty(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device="cuda")
     do = torch.randn_like(o)
     dqkv = torch.empty_like(qkv)
     work = torch.empty(B * H * T + B * T * d, device="cuda")
     st = ext.stream_handle()
-    fwd = lambda: ext.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T, H, dh, 1, st)
-    bwd = lambda: ext.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), dqkv.data_ptr(),
+    fwd = lambda: ext.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), live.data_ptr(), B, T, H, dh, 1, st)
+    bwd = lambda: ext.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), live.data_ptr(), dqkv.data_ptr(),
                            work.data_ptr(), B, T, H, dh, 1, st)
     res = {"B": B, "T": T, "H": H, "dh": dh}
     fl = 2.0 * B * H * dh * T * (T + 1)  # causal fwd (QK^T + PV, lower triangle)

@@ -13,13 +13,14 @@ d = H * dh
 qkv = torch.randn(B * T, 3 * d, device="cuda").to(torch.bfloat16)
 o = torch.empty(B * T, d, dtype=torch.bfloat16, device="cuda")
 lse = torch.empty(B * H * T, device="cuda")
+live = torch.empty(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device="cuda")
 do = torch.randn_like(o)
 dqkv = torch.empty_like(qkv)
 work = torch.empty(B * H * T + B * T * d, device="cuda")
 st = ext.stream_handle()
 for _ in range(2):
-    ext.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), B, T, H, dh, 1, st)
-    ext.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), dqkv.data_ptr(),
+    ext.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), live.data_ptr(), B, T, H, dh, 1, st)
+    ext.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), live.data_ptr(), dqkv.data_ptr(),
              work.data_ptr(), B, T, H, dh, 1, st)
 torch.cuda.synchronize()
 print("ok")
