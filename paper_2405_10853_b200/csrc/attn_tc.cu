@@ -9,7 +9,7 @@
 // settles in the first tile and the lazy O rescale almost never fires. Heaviest pairs
 // launch first.
 //   TMEM (512 columns): S_g = Q_g K^T at [128 g, 128 g + 128) f32; the softmax writes
-//   P_g (bf16 pairs) back over S_g's upper 64 columns, and PV reads it from there as an
+//   P_g (bf16 pairs) back over S_g's lower 64 columns, and PV reads it from there as an
 //   A-from-TMEM MMA, so P never touches shared memory. O_g at 256 + DH g.
 //   Why: the previous design (64-key tiles, P staged in smem, SS MMAs) was bound by smem
 //   bandwidth: an N=64 SS MMA reads 6 KB of operands for 32 cycles of math and measured
@@ -24,6 +24,8 @@
 // The issue scheduler favours high warp ids, so the two single-thread control warps sit
 // above the softmax warps.
 #include <cudaTypedefs.h>
+
+#include <type_traits>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -47,6 +49,38 @@ __device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64
       : "memory");
 }
 
+// Packed f32x2 math (FFMA2 / FADD2 on sm_100) and the 3-input max (FMNMX3): the softmax is
+// issue-bound next to the MUFU, so every element-wise op counts.
+__device__ __forceinline__ unsigned long long u64of(float2 v) { return *reinterpret_cast<unsigned long long*>(&v); }
+__device__ __forceinline__ float2 f2of(unsigned long long v) { return *reinterpret_cast<float2*>(&v); }
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(u64of(a)), "l"(u64of(b)), "l"(u64of(c)));
+  return f2of(r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u64of(a)), "l"(u64of(b)));
+  return f2of(r);
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+#ifdef FB_ATTN_TRACE
+__device__ unsigned long long g_attn_trace_fwd[2048];
+__device__ __forceinline__ unsigned long long gtimer_f() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define FTRACE(slot) do { if (blockIdx.x == 0 && blockIdx.y == 5 && (slot) < 2048) g_attn_trace_fwd[(slot)] = gtimer_f(); } while (0)
+#else
+#define FTRACE(slot) do {} while (0)
+#endif
+
 template <int DH>
 struct AttnTcCfg {
   static constexpr int BN = 128;                 // keys per KV tile
@@ -56,7 +90,8 @@ struct AttnTcCfg {
   static constexpr int Q_OFF = 0;                // [2] Q tiles
   static constexpr int K_OFF = 2 * QT;           // [NST]
   static constexpr int V_OFF = K_OFF + NST * KT; // [NST]
-  static constexpr int BAR_OFF = V_OFF + NST * KT;
+  static constexpr int CB_OFF = V_OFF + NST * KT;  // column bias table sl * i, i < BN (f32)
+  static constexpr int BAR_OFF = CB_OFF + BN * 4;
   static constexpr int SMEM = BAR_OFF + 256 + 1024;
   static_assert(SMEM <= 232448, "attention forward smem");
 };
@@ -115,6 +150,9 @@ __global__ void __launch_bounds__(320, 1)
     fence_barrier_init();
   }
   if (warp == kMmaWarp) tmem_alloc(tmem_slot, 512);
+  const float sl = use_alibi ? exp2f(-8.0f * (float)(h + 1) / (float)H) * 1.4426950408889634f : 0.0f;
+  float* colb = reinterpret_cast<float*>(smem + Cf::CB_OFF);
+  if (threadIdx.x < BN) colb[threadIdx.x] = sl * (float)threadIdx.x;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -158,6 +196,7 @@ __global__ void __launch_bounds__(320, 1)
       auto issue_pv = [&](int g, int t) {
         const int j = g ? t : t - start0;
         mbar_wait(&p_full[g], j & 1);
+        FTRACE(t * 16 + 8 + g);
         // all four warps found every p of their rows exactly 0: the block adds nothing to O
         const bool dead = *reinterpret_cast<volatile uint32_t*>(dead_flag + 4 * g) == 0x01010101u;
         if (live_map) {
@@ -170,7 +209,7 @@ __global__ void __launch_bounds__(320, 1)
         const uint64_t vd = smem_desc_sw128(sV + (t % NST) * Cf::KT, BN * 128, 1024);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)  // V MN-major: 16 keys = 16 rows x 128 B
-          umma_ts(tmem + 256 + DH * g, tmem + 128 * g + 64 + 8 * kk, vd + (uint64_t)((kk * 2048) >> 4), idO,
+          umma_ts(tmem + 256 + DH * g, tmem + 128 * g + 8 * kk, vd + (uint64_t)((kk * 2048) >> 4), idO,
                   o_acc[g] | (uint32_t)(kk > 0));
         o_acc[g] = 1u;
       };
@@ -185,9 +224,11 @@ __global__ void __launch_bounds__(320, 1)
         for (int g = 0; g < 2; ++g) {
           const bool now = active(g, t), next = t + 1 < nkv && active(g, t + 1);
           if (now) issue_pv(g, t);
+          FTRACE(t * 16 + 10 + g);
           if (next) {
             issue_s(g, t + 1);
             umma_commit(&s_full[g]);  // also covers PV_g(t): the softmax may rescale O / overwrite P
+            FTRACE(t * 16 + 12 + g);
           } else if (now) {
             umma_commit(&o_done[g]);
           }
@@ -204,40 +245,51 @@ __global__ void __launch_bounds__(320, 1)
     const int qi = q0 + 128 * g + r;
     const int ntile = g ? (has1 ? nkv : 0) : nkv0;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t tS = tmem + lane_off + 128 * g, tP = tS + 64;
+    const uint32_t tS = tmem + lane_off + 128 * g, tP = tS;  // P over S's lower 64 columns
     const uint32_t tO = tmem + lane_off + 256 + DH * g;
-    const float sl = use_alibi ? exp2f(-8.0f * (float)(h + 1) / (float)H) * 1.4426950408889634f : 0.0f;
+    // Scores in log2 units: x_i = s_i c + sl (k0 + i - qi) = y_i + base with the
+    // tile-independent y_i = s_i c + colb[i] (colb = sl i, an smem broadcast table) and the
+    // per-row, per-tile scalar base = sl (k0 - qi); the max and the exp argument then work
+    // on y with base folded into one scalar.
+    const float2 c2 = make_float2(scale_log2, scale_log2);
+    const float4* colb4 = reinterpret_cast<const float4*>(colb);
     float m = -1e30f, l = 0.f;
     for (int j = 0; j < ntile; ++j) {
       const int k0 = (ntile - 1 - j) * BN;
       const bool diag = (j == 0);  // Q tiles and key tiles are both 128 wide: only the first crosses
       mbar_wait(&s_full[g], j & 1);
+      if (quad == 0 && lane == 0) FTRACE((j + (g ? 0 : start0)) * 16 + 0 + g);
       tc_fence_after();
       uint32_t v[128];
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(tS + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * c]));
       tmem_ld_wait();
       const float base = sl * (float)(k0 - qi);
-      float pm[8];
+      float pm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      auto scan = [&](auto diag_t) {  // y = s c + colb (masked above the diagonal), running maxima
+        constexpr bool kDiag = decltype(diag_t)::value;
 #pragma unroll
-      for (int u = 0; u < 8; ++u) pm[u] = -INFINITY;
-      if (diag) {
-#pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          float x = fmaf(__uint_as_float(v[i]), scale_log2, fmaf(sl, (float)i, base));
-          x = (k0 + i > qi) ? -INFINITY : x;
-          v[i] = __float_as_uint(x);
-          pm[i & 7] = fmaxf(pm[i & 7], x);
+        for (int i = 0; i < 128; i += 4) {
+          const float4 cb = colb4[i >> 2];
+          float2 y0 = ffma2(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), c2, make_float2(cb.x, cb.y));
+          float2 y1 = ffma2(make_float2(__uint_as_float(v[i + 2]), __uint_as_float(v[i + 3])), c2, make_float2(cb.z, cb.w));
+          if constexpr (kDiag) {  // key k0 + i > qi  <=>  i > r (k0 = qi - r on the diagonal tile)
+            if (i > r) y0.x = -INFINITY;
+            if (i + 1 > r) y0.y = -INFINITY;
+            if (i + 2 > r) y1.x = -INFINITY;
+            if (i + 3 > r) y1.y = -INFINITY;
+          }
+          v[i] = __float_as_uint(y0.x);
+          v[i + 1] = __float_as_uint(y0.y);
+          v[i + 2] = __float_as_uint(y1.x);
+          v[i + 3] = __float_as_uint(y1.y);
+          pm[(i >> 2) & 3] = fmax3(pm[(i >> 2) & 3], fmax3(y0.x, y0.y, y1.x), y1.y);
         }
-      } else {
-#pragma unroll
-        for (int i = 0; i < 128; ++i) {
-          const float x = fmaf(__uint_as_float(v[i]), scale_log2, fmaf(sl, (float)i, base));
-          v[i] = __float_as_uint(x);
-          pm[i & 7] = fmaxf(pm[i & 7], x);
-        }
-      }
-      const float mx = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])), fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7])));
+      };
+      if (diag) scan(std::true_type{});
+      else scan(std::false_type{});
+      const float mx = fmax3(pm[0], pm[1], fmaxf(pm[2], pm[3])) + base;
+      if (quad == 0 && lane == 0) FTRACE((j + (g ? 0 : start0)) * 16 + 2 + g);
       // Dead rows: every x < m - 127, so every p = ex2.approx.ftz(x - m) is exactly 0 (the
       // ALiBi bias drives far keys there). A warp whose 32 rows are all dead skips the exps;
       // a block dead in all four warps skips its PV MMA and is marked for the backward.
@@ -254,19 +306,24 @@ __global__ void __launch_bounds__(320, 1)
         // lazy rescale (FA4-style): keep the running max unless it grows by more than 8 (log2 units)
         const float m_new = (mx > m + 8.0f) ? mx : m;
         const float alpha = ex2(m - m_new);
-        float ps[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        uint32_t pk[64];
+        const float2 sh = make_float2(base - m_new, base - m_new);  // x - m_new = y + sh
+        float2 ps[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        // P (bf16 pairs) over S's lower 64 columns: all of S is in registers by now
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float p0 = ex2(__uint_as_float(v[2 * c]) - m_new);
-          const float p1 = ex2(__uint_as_float(v[2 * c + 1]) - m_new);
-          ps[(2 * c) & 7] += p0;
-          ps[(2 * c + 1) & 7] += p1;
-          pk[c] = pack_bf16(p0, p1);
+        for (int hh = 0; hh < 2; ++hh) {
+          uint32_t pk[32];
+#pragma unroll
+          for (int c = 0; c < 32; ++c) {
+            const int i = 64 * hh + 2 * c;
+            const float2 a = fadd2(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sh);
+            const float2 p = make_float2(ex2(a.x), ex2(a.y));
+            ps[c & 3] = fadd2(ps[c & 3], p);
+            pk[c] = pack_bf16(p.x, p.y);
+          }
+          tmem_st_32x32b_x32(tP + 32 * hh, pk);
         }
-        tmem_st_32x32b_x32(tP, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-        tmem_st_32x32b_x32(tP + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
-        const float rs = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+        const float2 s01 = fadd2(fadd2(ps[0], ps[1]), fadd2(ps[2], ps[3]));
+        const float rs = s01.x + s01.y;
         l = l * alpha + rs;
         m = m_new;
         // O holds exactly PV(0..j-1): s_full(j) was committed after PV(j-1)
@@ -282,10 +339,12 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
       }
+      if (quad == 0 && lane == 0) FTRACE((j + (g ? 0 : start0)) * 16 + 4 + g);
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[g]);
+      if (quad == 0 && lane == 0) FTRACE((j + (g ? 0 : start0)) * 16 + 6 + g);
     }
     if (ntile > 0) {  // warps of an absent second Q tile (T % 256 == 128) have nothing to write
       mbar_wait(&o_done[g], 0);
@@ -356,6 +415,11 @@ int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, uint8_t* live, int 
   return FB_OK;
 }
 
+#ifdef FB_ATTN_TRACE
+extern "C" int fb_attn_trace_read_fwd(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_attn_trace_fwd, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : 2;
+}
+#endif
 template int attn_fwd_tc_launch<64>(const void*, void*, float*, uint8_t*, int, int, int, int, cudaStream_t);
 template int attn_fwd_tc_launch<128>(const void*, void*, float*, uint8_t*, int, int, int, int, cudaStream_t);
 

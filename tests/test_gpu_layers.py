@@ -99,7 +99,11 @@ def test_attention_dead_block_skip_is_exact(fb, B, T, H, dh):
     live = torch.full((B * H * (T // 128) * (T // 64),), 7, dtype=torch.uint8, device=dev)
     o1, l1, g1 = _attn_run(fb, qkv, do, B, T, H, dh, live)
     o0, l0, g0 = _attn_run(fb, qkv, do, B, T, H, dh, None)
-    assert torch.equal(o1, o0) and torch.equal(l1, l0) and torch.equal(g1, g0)
+    assert torch.equal(o1, o0) and torch.equal(l1, l0)
+    # dK / dV come from one CTA each: bit-identical. dQ is reduce-added across key blocks by
+    # the TMA (f32 adds in arrival order), so it is identical only up to summation order.
+    assert torch.equal(g1[:, H * dh:], g0[:, H * dh:])
+    torch.testing.assert_close(g1[:, :H * dh].float(), g0[:, :H * dh].float(), atol=1e-2, rtol=1e-2)
     m = live.view(B, H, T // 128, T // 64).cpu().numpy()
     causal = np.array([[kt <= 2 * qt + 1 for kt in range(T // 64)] for qt in range(T // 128)])
     vals = m[:, :, causal]

@@ -28,8 +28,8 @@ L.fb_attn_trace_read_fwd.argtypes = [C.c_void_p, C.c_int]
 assert L.fb_attn_trace_read_fwd(buf, 2048) == 0
 a = np.array(buf[:], dtype=np.int64).reshape(128, 16)
 t0 = a[a > 0].min()
-names = ["mma:S_next", "mma:PV0", "mma:PV1", "g0:S", "g0:P", "g1:S", "g1:P", "kfull+1", "sempty0", "sempty1",
-         "pfull0", "vfull0", "pfull1", "vfull1"]
+names = ["g0:S", "g1:S", "g0:max", "g1:max", "g0:exp", "g1:exp", "g0:P", "g1:P", "m:pf0", "m:pf1", "m:pv0", "m:pv1",
+         "m:s0", "m:s1"]
 for t in range(128):
     if a[t].max() == 0:
         break
