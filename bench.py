@@ -208,7 +208,7 @@ def run_ours(args, cfgname):
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
-    prof = (C.c_double * 9)()
+    prof = (C.c_double * 12)()
     ext.check(ext.lib().fb_profile_end(prof), "profile")
     ms = e0.elapsed_time(e1)
     if world > 1:
@@ -225,6 +225,7 @@ def run_ours(args, cfgname):
     gemm_ms, gemm_n, gemm_fl = prof[0], int(prof[1]), prof[2]
     afw_ms, afw_n, afw_fl = prof[3], int(prof[4]), prof[5]
     abw_ms, abw_n, abw_fl = prof[6], int(prof[7]), prof[8]
+    gemm_total = prof[9]
     torch.cuda.empty_cache()
     Kc = c["K"]
     mine = clients_of(rank, world, Kc)
@@ -327,7 +328,7 @@ def run_ours(args, cfgname):
                                       f"capture; algorithmic operand+output bytes {traffic_alg}") if traffic else None,
                      "launches_sampled": gemm_n, "avg_launch_ms": round(gemm_avg_ms, 4),
                      "peak_kind": peak_kind,
-                     "gemm_share_of_step": round(gemm_ms / (ms_step * K) if gemm_n else 0, 3)},
+                     "gemm_share_of_step": round(gemm_ms / gemm_n * gemm_total / (ms_step * K) if gemm_n else 0, 3)},
         "attention": {"fwd_tflops": round(afw_fl / max(afw_ms, 1e-9) / 1e9, 1),
                       "bwd_tflops": round(abw_fl / max(abw_ms, 1e-9) / 1e9, 1)},
         "clocks": clk,

@@ -200,10 +200,11 @@ int fb_train_step(const fb_model_cfg* cfg, float* d_params, void* d_shadow, floa
 /* ---- live kernel profiling (used by bench.py inside its timed region) --------------
  * While enabled, every fb_gemm_bf16 / fb_attn_* launch is bracketed by CUDA events on
  * its own stream (first max_launches launches per category). fb_profile_end syncs
- * and returns per category {total ms, launches, algorithmic flops} for
- * categories 0 = GEMM, 1 = attention fwd, 2 = attention bwd: out[9]. */
+ * and returns per category {total ms, timed launches, algorithmic flops} for
+ * categories 0 = GEMM, 1 = attention fwd, 2 = attention bwd in out[0..8], and the
+ * number of launches seen per category (timed or past the cap) in out[9..11]. */
 int fb_profile_begin(int max_launches);
-int fb_profile_end(double* out9);
+int fb_profile_end(double* out12);
 
 #ifdef __cplusplus
 }

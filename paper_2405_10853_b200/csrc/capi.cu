@@ -34,6 +34,7 @@ namespace fb {
 struct ProfCat {
   std::vector<cudaEvent_t> ev;
   int n = 0;
+  long total = 0;  // launches seen while on, including those past the event cap
   double flops = 0.0;
 };
 static struct {
@@ -47,7 +48,9 @@ bool prof_on() { return g_prof.on; }
 int prof_start(int cat, cudaStream_t st) {
   std::lock_guard<std::mutex> lk(g_prof.mu);
   ProfCat& c = g_prof.cat[cat];
-  if (!g_prof.on || c.n >= g_prof.cap) return -1;
+  if (!g_prof.on) return -1;
+  ++c.total;
+  if (c.n >= g_prof.cap) return -1;
   const int i = c.n++;
   cudaEventRecord(c.ev[2 * i], st);
   return i;
@@ -71,6 +74,7 @@ extern "C" int fb_profile_begin(int max_launches) {
       c.ev.push_back(e);
     }
     c.n = 0;
+    c.total = 0;
     c.flops = 0.0;
   }
   fb::g_prof.cap = max_launches;
@@ -93,6 +97,7 @@ extern "C" int fb_profile_end(double* out) {
     out[3 * k + 0] = ms;
     out[3 * k + 1] = c.n;
     out[3 * k + 2] = c.flops;
+    out[9 + k] = (double)c.total;
   }
   return FB_OK;
 }
