@@ -86,16 +86,37 @@ def splitk_splits(M, N, K):
     return s
 
 
+def tail_split(M, N, K):
+    """Mirror of plan_tail_split (csrc/gemm_sm100.cu): last-wave split S of a 2-SM GEMM (1 = none)."""
+    tiles, P, num_kb = ((M + 255) // 256) * ((N + 255) // 256), 74, (K + 63) // 64
+    if M < 256 or N < 256 or tiles < P:
+        return 1
+    F = tiles // P * P
+    R = tiles - F
+    if R == 0:
+        return 1
+    base = F / P + 1.0
+    best, best_t = 1, base
+    for S in range(2, 17):
+        per = (num_kb + S - 1) // S
+        if num_kb - (S - 1) * per < 4 or R * S > 256:
+            break
+        t = F / P + ((R * S + P - 1) // P) / S + 0.01 * S
+        if t < best_t:
+            best, best_t = S, t
+    return best if best_t <= 0.96 * base else 1
+
+
 def launches_per_step(c):
     """Kernel launches of our library per local step (fb_train_step), from the runtime's schedule."""
     L, d, M = c["L"], c["d"], c["B"] * c["T"]
     chunks = math.ceil(M / 8192)
     # forward: gather + embed + L x (ln, qkv, attn, proj, ln, fc, proj2) + ln_f + chunks x (logits, ce, dgrad, wgrad)
-    fwd = 1 + 1 + 7 * L + 1 + 4 * chunks
+    fwd = 1 + 1 + 7 * L + 1 + 4 * chunks + chunks * (tail_split(8192, d, c["V"]) > 1)  # + head-dgrad reductions
     # backward: ln_f bwd(2) + L x (dgelu, wgrad, dgrad, wgrad, ln bwd(2), dgrad, wgrad, attn bwd(3), dgrad, wgrad,
     # ln bwd(2)) + split-K reduction launches + embed bwd
     wg = [(d, 4 * d), (4 * d, d), (d, d), (3 * d, d)]
-    red = sum(1 for (mm, nn) in wg if splitk_splits(mm, nn, M) > 1)
+    red = sum(1 for (mm, nn) in wg if splitk_splits(mm, nn, M) > 1 or tail_split(mm, nn, M) > 1)
     bwd = 2 + L * (15 + red) + 1
     return c["micro"] * (fwd + bwd) + 4  # + sumsq, step_prepare, adamw, telemetry
 

@@ -57,7 +57,42 @@ struct EpiArgs {
   int64_t ld_aux;
   int ksplit;            // > 1: work unit u = (split, tile); split s writes C + s * split_stride
   int64_t split_stride;  // elements
+  // Last-wave split (2-SM kernel only; tail_split > 1 enables it): tiles [0, full_tiles) are
+  // whole-K units that fill complete waves of the 74 CTA pairs; each remaining tile is cut
+  // into tail_split K ranges whose raw f32 partials go to a [piece][256][256] workspace,
+  // reduced in fixed order by tail_reduce_kernel (deterministic).
+  int full_tiles;
+  int tail_split;
+  void* tail_ws;         // f32 [pieces][256][256]
+  int units;             // work units of the launch
 };
+
+// work unit -> (tile, first k-block, k-block count, tail piece or -1), 2-SM kernel
+__device__ __forceinline__ void unit_coords2(int u, int num_tiles, int num_kb, const EpiArgs& e, int& tile, int& kb0,
+                                             int& nkb, int& piece) {
+  if (e.tail_split > 1) {
+    piece = -1;
+    if (u < e.full_tiles) {
+      tile = u;
+      kb0 = 0;
+      nkb = num_kb;
+      return;
+    }
+    const int v = u - e.full_tiles;
+    tile = e.full_tiles + v / e.tail_split;
+    const int per = (num_kb + e.tail_split - 1) / e.tail_split;
+    kb0 = (v % e.tail_split) * per;
+    nkb = min(num_kb, kb0 + per) - kb0;
+    piece = v;
+    return;
+  }
+  tile = u % num_tiles;
+  const int sp = u / num_tiles;
+  const int per = (num_kb + e.ksplit - 1) / e.ksplit;
+  kb0 = sp * per;
+  nkb = min(num_kb, kb0 + per) - kb0;
+  piece = -1;
+}
 
 // work unit -> (tile, first k-block, k-block count)
 __device__ __forceinline__ void unit_coords(int u, int num_tiles, int num_kb, int ksplit, int& tile, int& kb0, int& nkb) {
@@ -103,6 +138,49 @@ __device__ __forceinline__ float gelu_erf(float x) { return x * norm_cdf(x); }
 __device__ __forceinline__ float gelu_erf_grad(float x) {
   // Phi(x) + x phi(x), phi(x) = exp(-x^2/2) / sqrt(2 pi)
   return fmaf(x, ex2_approx(fmaf(x * x, -0.72134752f, -1.32574806f)), norm_cdf(x));
+}
+
+// Pair forms on the packed f32x2 pipe (FFMA2 / FMUL2, sm_100): each lane rounds exactly like
+// the scalar FFMA / FMUL above, so the results are bit-identical, at about 60% of the issue
+// slots. The fused GELU / dGELU GEMMs are epilogue-heavy and run at the power cap.
+__device__ __forceinline__ float2 f2_fma(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 f2_mul(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 f2s(float c) { return make_float2(c, c); }
+// Phi(x) for two values; xx = x * x (shared with the dGELU density term)
+__device__ __forceinline__ float2 norm_cdf2(float2 x, float2 xx) {
+  const float2 t = make_float2(rcp_approx(fmaf(fabsf(x.x), 0.353553391f, 1.0f)),
+                               rcp_approx(fmaf(fabsf(x.y), 0.353553391f, 1.0f)));
+  float2 q = f2_fma(f2s(0.246517298f), t, f2s(-1.18611495f));
+  q = f2_fma(q, t, f2s(2.14747446f));
+  q = f2_fma(q, t, f2s(-1.63775315f));
+  q = f2_fma(q, t, f2s(0.402321582f));
+  q = f2_fma(q, t, f2s(-0.26875686f));
+  q = f2_fma(q, t, f2s(0.139630057f));
+  q = f2_fma(q, t, f2s(0.539700616f));
+  q = f2_fma(q, t, f2s(1.4427292f));
+  q = f2_fma(q, t, f2s(-2.82574822f));
+  const float2 a = f2_fma(xx, f2s(-0.72134752f), q);
+  const float2 h = f2_mul(t, make_float2(ex2_approx(a.x), ex2_approx(a.y)));
+  return make_float2(x.x >= 0.f ? 1.0f - h.x : h.x, x.y >= 0.f ? 1.0f - h.y : h.y);
+}
+__device__ __forceinline__ float2 gelu_erf2(float2 x) { return f2_mul(x, norm_cdf2(x, f2_mul(x, x))); }
+__device__ __forceinline__ float2 gelu_erf_grad2(float2 x) {
+  const float2 xx = f2_mul(x, x);
+  const float2 a = f2_fma(xx, f2s(-0.72134752f), f2s(-1.32574806f));
+  return f2_fma(x, make_float2(ex2_approx(a.x), ex2_approx(a.y)), norm_cdf2(x, xx));
 }
 
 // Process 32 consecutive columns [col, col+32) of one row held in registers.
@@ -372,9 +450,27 @@ __device__ __forceinline__ void stg_put_bf16(uint8_t* stg, int r, int j, const f
 }
 
 struct EpiMaps {
-  CUtensorMap C;    // {N, M, splits} box {32, 32, 1}
-  CUtensorMap Aux;  // bf16 second output (GELU pre-activation, RESID_F32_BF16 copy), {N, M, 1}
+  CUtensorMap C;     // {N, M, splits} box {32, 32, 1}
+  CUtensorMap Aux;   // bf16 second output (GELU pre-activation, RESID_F32_BF16 copy), {N, M, 1}
+  CUtensorMap Part;  // f32 last-wave partials {256, 256, pieces} box {32, 32, 1}
 };
+
+// Raw f32 accumulator chunk -> last-wave partial workspace (no epilogue op).
+__device__ __forceinline__ void partial_chunk_tma(const CUtensorMap* map, uint8_t* stg, int lane, int x, int y, int z,
+                                                  const uint32_t (&r)[32]) {
+  if (lane == 0) bulk_wait_read<0>();
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    stg_put_f32(stg, lane, j, __uint_as_float(r[4 * j]), __uint_as_float(r[4 * j + 1]), __uint_as_float(r[4 * j + 2]),
+                __uint_as_float(r[4 * j + 3]));
+  fence_proxy_async_smem();
+  __syncwarp();
+  if (lane == 0) {
+    tma_store_3d(map, stg, x, y, z);
+    bulk_commit();
+  }
+}
 
 // One 32-column chunk of one warp: lane = row (row0 + lane), r[] = TMEM accumulator values.
 template <int EPI>
@@ -405,8 +501,13 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& e, const EpiMa
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
       pre[i] = pack_bf16(v[2 * i], v[2 * i + 1]);
-      v[2 * i] = gelu_erf(__uint_as_float(pre[i] << 16));
-      v[2 * i + 1] = gelu_erf(__uint_as_float(pre[i] & 0xFFFF0000u));
+#ifdef FB_EXP_GELU_ID
+      const float2 g = make_float2(__uint_as_float(pre[i] << 16), __uint_as_float(pre[i] & 0xFFFF0000u));
+#else
+      const float2 g = gelu_erf2(make_float2(__uint_as_float(pre[i] << 16), __uint_as_float(pre[i] & 0xFFFF0000u)));
+#endif
+      v[2 * i] = g.x;
+      v[2 * i + 1] = g.y;
     }
   } else if constexpr (EPI == FB_EPI_DGELU) {
     const __nv_bfloat16* P = reinterpret_cast<const __nv_bfloat16*>(e.aux) + row * e.ld_aux + col;
@@ -416,7 +517,16 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& e, const EpiMa
         uint4 pk = *reinterpret_cast<const uint4*>(P + 8 * q);
         const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&pk);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[8 * q + i] *= gelu_erf_grad(__bfloat162float(pb[i]));
+        for (int i = 0; i < 8; i += 2) {
+#ifdef FB_EXP_GELU_ID
+          const float2 g = make_float2(__bfloat162float(pb[i]), __bfloat162float(pb[i + 1]));
+#else
+          const float2 g = gelu_erf_grad2(make_float2(__bfloat162float(pb[i]), __bfloat162float(pb[i + 1])));
+#endif
+          const float2 o = f2_mul(make_float2(v[8 * q + i], v[8 * q + i + 1]), g);
+          v[8 * q + i] = o.x;
+          v[8 * q + i + 1] = o.y;
+        }
       }
     } else {
       _Pragma("unroll") for (int i = 0; i < 32; ++i) v[i] = (in && col + i < N) ? v[i] * gelu_erf_grad(__bfloat162float(P[i])) : 0.f;
@@ -521,9 +631,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = cluster; u < num_tiles * ep.ksplit; u += nclusters) {
-        int tile, kb0, nkb;
-        unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
+      for (int u = cluster; u < ep.units; u += nclusters) {
+        int tile, kb0, nkb, piece;
+        unit_coords2(u, num_tiles, num_kb, ep, tile, kb0, nkb, piece);
         int mb, nb;
         tile_coords(tile, num_m, num_n, mb, nb);
         const int m0 = mb * 256 + rank * 128;
@@ -548,9 +658,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int u = cluster; u < num_tiles * ep.ksplit; u += nclusters, ++it) {
-        int tile, kb0, nkb;
-        unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
+      for (int u = cluster; u < ep.units; u += nclusters, ++it) {
+        int tile, kb0, nkb, piece;
+        unit_coords2(u, num_tiles, num_kb, ep, tile, kb0, nkb, piece);
         const int buf = it & 1;
         const uint32_t use = it >> 1;
         mbar_wait(&tempty_bar[buf], (use & 1) ^ 1);
@@ -584,9 +694,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
     const int half = (warp - 2) >> 2;
     uint8_t* stg = staging + (warp - 2) * kStageEpi;
     int it = 0;
-    for (int u = cluster; u < num_tiles * ep.ksplit; u += nclusters, ++it) {
-      int tile, kb0, nkb;
-      unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
+    for (int u = cluster; u < ep.units; u += nclusters, ++it) {
+      int tile, kb0, nkb, piece;
+      unit_coords2(u, num_tiles, num_kb, ep, tile, kb0, nkb, piece);
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       const int m0 = mb * 256 + rank * 128;
@@ -608,8 +718,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (lane == 0) mbar_arrive_leader(&tempty_bar[buf]);
         }
         const int col = n0 + c * 32;
-        if (row0 < M && col < N)
-          epilogue_chunk_tma<EPI>(ep, maps, stg, lane, row0 + lane, row0, col, u / num_tiles, M, N, r);
+        if (row0 < M && col < N) {
+          if (piece >= 0)
+            partial_chunk_tma(&maps.Part, stg, lane, col - nb * 256, row0 - mb * 256, piece, r);
+          else
+            epilogue_chunk_tma<EPI>(ep, maps, stg, lane, row0 + lane, row0, col, u / num_tiles, M, N, r);
+        }
       }
     }
     if (lane == 0) bulk_wait_read<0>();
@@ -628,6 +742,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static thread_local void* g_split_ws = nullptr;  // split-K workspace for the current call
 static thread_local int g_split_n = 1;
+static thread_local void* g_tail_ws = nullptr;  // last-wave split for the current call
+static thread_local int g_tail_full = 0, g_tail_split = 1;
 int g_gemm_2sm = 1;  // fb_gemm_set_2sm() toggles it (A/B tests)
 
 static int get_encoder() {
@@ -724,15 +840,24 @@ static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, i
   } else {
     maps.Aux = maps.C;
   }
+  if (ep.tail_split > 1) {
+    const int pieces = (((M + 255) / 256) * ((N + 255) / 256) - ep.full_tiles) * ep.tail_split;
+    rc = make_out_map(&maps.Part, ep.tail_ws, false, 256, 256, 256, pieces, 65536);
+    if (rc) return rc;
+  } else {
+    maps.Part = maps.C;
+  }
   auto kern = gemm_bf16_tc2_kernel<A_MN, B_MN, EPI>;
   static bool attr_set = false;
   if (!attr_set) {
     FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem2));
     attr_set = true;
   }
-  const int tiles = ((M + 255) / 256) * ((N + 255) / 256) * ep.ksplit;
-  const int clusters = tiles < kNumSMs / 2 ? tiles : kNumSMs / 2;
-  kern<<<2 * clusters, kGemmThreads, kSmem2, st>>>(ta, tb, M, N, K, ep, maps);
+  EpiArgs e2 = ep;
+  const int tiles = ((M + 255) / 256) * ((N + 255) / 256);
+  e2.units = ep.tail_split > 1 ? ep.full_tiles + (tiles - ep.full_tiles) * ep.tail_split : tiles * ep.ksplit;
+  const int clusters = e2.units < kNumSMs / 2 ? e2.units : kNumSMs / 2;
+  kern<<<2 * clusters, kGemmThreads, kSmem2, st>>>(ta, tb, M, N, K, e2, maps);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }
@@ -809,7 +934,12 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   const int bbox = use2 ? 128 : BN;  // 2-SM: each CTA stages 128 of the 256 B rows
   rc = b_major ? make_map_mnmajor(&tb, d_B, N, K, ldb, bbox) : make_map_kmajor(&tb, d_B, N, K, ldb, bbox);
   if (rc) return rc;
-  EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux, 1, 0};
+  EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux, 1, 0, 0, 1, nullptr, 0};
+  if (g_tail_ws && use2) {  // set by fb_gemm_bf16_splitk for this call only
+    ep.full_tiles = g_tail_full;
+    ep.tail_split = g_tail_split;
+    ep.tail_ws = g_tail_ws;
+  }
   if (g_split_ws) {  // set by fb_gemm_bf16_splitk for this call only
     ep.ksplit = g_split_n;
     ep.C = g_split_ws;
@@ -874,6 +1004,51 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ W, int S, int64_t
     *c = acc;
   }
 }
+
+// Last-wave split: C[tile] (+)= sum_s part[(tile - F) * S + s] in fixed order, for the tiles
+// [F, num_tiles) of the 2-SM raster (deterministic). Block x = tail tile, y = row slab.
+__global__ void tail_reduce_kernel(const float* __restrict__ W, int S, int F, int num_m, int num_n, int M, int N,
+                                   float* __restrict__ C, int64_t ldc, int accumulate) {
+  int mb, nb;
+  tile_coords(F + blockIdx.x, num_m, num_n, mb, nb);
+  const float* w0 = W + (int64_t)blockIdx.x * S * 65536;
+  for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < 256 * 64; i += gridDim.y * blockDim.x) {
+    const int r = i >> 6, c = (i & 63) * 4;
+    const int m = mb * 256 + r, n = nb * 256 + c;
+    if (m >= M || n >= N) continue;
+    float4 acc = *reinterpret_cast<const float4*>(w0 + r * 256 + c);
+    for (int sp = 1; sp < S; ++sp) {
+      const float4 v = *reinterpret_cast<const float4*>(w0 + (int64_t)sp * 65536 + r * 256 + c);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    float4* cp = reinterpret_cast<float4*>(C + (int64_t)m * ldc + n);
+    if (accumulate) {
+      const float4 o = *cp;
+      acc.x = o.x + acc.x; acc.y = o.y + acc.y; acc.z = o.z + acc.z; acc.w = o.w + acc.w;
+    }
+    *cp = acc;
+  }
+}
+
+// Plan the last-wave split of a 2-SM GEMM with `tiles` 256x256 tiles and num_kb k-blocks:
+// returns S > 1 (and F) when cutting the ragged last wave into S K-ranges beats running it
+// whole by >= 4% of the launch, within `max_pieces` workspace tiles.
+static int plan_tail_split(int tiles, int num_kb, int max_pieces, int& F) {
+  const int P = kNumSMs / 2;
+  F = (tiles / P) * P;
+  const int R = tiles - F;
+  if (R == 0) return 1;
+  const double base = F / (double)P + 1.0;
+  int best = 1;
+  double best_t = base;
+  for (int S = 2; S <= 16; ++S) {
+    const int per = (num_kb + S - 1) / S;
+    if (num_kb - (S - 1) * per < 4 || R * S > max_pieces) break;
+    const double t = F / (double)P + (double)((R * S + P - 1) / P) / S + 0.01 * S;
+    if (t < best_t) { best_t = t; best = S; }
+  }
+  return best_t <= 0.96 * base ? best : 1;
+}
 }  // namespace fb
 
 // Split-K GEMM for short-M/N, long-K products (weight gradients over many tokens):
@@ -888,6 +1063,27 @@ extern "C" int fb_gemm_bf16_splitk(int M, int N, int K, const void* d_A, int64_t
   const int tiles2 = ((M + 255) / 256) * ((N + 255) / 256);
   const int num_kb = (K + BK - 1) / BK;
   if (ksplit <= 0) {
+    // 2-SM raster with a full first wave: split only the ragged last wave (tile-local partials)
+    if (g_gemm_2sm && M >= 256 && N >= 256 && tiles2 >= kNumSMs / 2 && d_ws) {
+      int F = 0;
+      const int S = plan_tail_split(tiles2, num_kb, (int)(ws_bytes / (65536 * 4)), F);
+      if (S > 1) {
+        g_tail_ws = d_ws;
+        g_tail_full = F;
+        g_tail_split = S;
+        int rc = fb_gemm_bf16(M, N, K, d_A, lda, a_major, d_B, ldb, b_major, d_C, ldc, epilogue, nullptr, nullptr, 0,
+                              stream);
+        g_tail_ws = nullptr;
+        g_tail_full = 0;
+        g_tail_split = 1;
+        if (rc) return rc;
+        fb::tail_reduce_kernel<<<dim3(tiles2 - F, 16), 256, 0, (cudaStream_t)stream>>>(
+            (const float*)d_ws, S, F, (M + 255) / 256, (N + 255) / 256, M, N, (float*)d_C, ldc,
+            epilogue == FB_EPI_ACC_F32);
+        FB_LAUNCH_CHECK();
+        return FB_OK;
+      }
+    }
     ksplit = 1;
     while (tiles2 * ksplit < kNumSMs / 2 && num_kb / (ksplit + 1) >= 16) ++ksplit;
   }

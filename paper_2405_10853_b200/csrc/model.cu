@@ -197,8 +197,8 @@ extern "C" int fb_model_fwd_bwd(const fb_model_cfg* cfgp, const float* P, const 
     TRY(fb_ce_fwd_bwd(w.logits, tok, w.dlogits, r0, rows, T, V, grad_scale, row_loss, st));
     if (want_grad) {
       // d(lnf) = dlogits . W_head ; dW_head += dlogits^T . lnf
-      TRY(fb_gemm_bf16(rows, d, V, w.dlogits, V, 0, S + Lo.head, d, 1, w.dln + (int64_t)r0 * d, d, FB_EPI_F32,
-                       nullptr, nullptr, 0, st));
+      TRY(fb_gemm_bf16_splitk(rows, d, V, w.dlogits, V, 0, S + Lo.head, d, 1, w.dln + (int64_t)r0 * d, d,
+                              FB_EPI_F32, 0, w.splitk, kSplitKFloats * 4, st));
       TRY(fb_gemm_bf16(V, d, rows, w.dlogits, V, 1, w.lnf + (int64_t)r0 * d, d, 1, G + Lo.head, d, FB_EPI_ACC_F32,
                        nullptr, nullptr, 0, st));
     }

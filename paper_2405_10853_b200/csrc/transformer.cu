@@ -127,6 +127,60 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const float* __restrict__ x
   }
 }
 
+// Warp-per-row variant for d = 128 * NV4 (the GPU configs): lane owns float4 columns
+// lane*4 + 128*j, so every load / store instruction of the warp is one coalesced 512 B
+// (f32) or 256 B (bf16) segment; no block barriers, so rows stream back to back. The
+// next row's loads are issued before the current row is reduced and written.
+template <int NV4>
+__global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
+                                                          const float* __restrict__ beta,
+                                                          __nv_bfloat16* __restrict__ y, float* __restrict__ mean_out,
+                                                          float* __restrict__ rstd_out, int rows) {
+  constexpr int d = 128 * NV4;
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  float4 cur[NV4];
+  if (row < rows) {
+#pragma unroll
+    for (int j = 0; j < NV4; ++j) cur[j] = __ldcs(reinterpret_cast<const float4*>(x + (int64_t)row * d + 128 * j) + lane);
+  }
+  for (; row < rows; row += warps) {
+    float4 nxt[NV4];
+    const int nrow = row + warps;
+    if (nrow < rows) {
+#pragma unroll
+      for (int j = 0; j < NV4; ++j)
+        nxt[j] = __ldcs(reinterpret_cast<const float4*>(x + (int64_t)nrow * d + 128 * j) + lane);
+    }
+    float sum = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV4; ++j) sum += (cur[j].x + cur[j].y) + (cur[j].z + cur[j].w);
+    const float mean = warp_sum(sum) * (1.0f / d);
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV4; ++j) {
+      const float a = cur[j].x - mean, b = cur[j].y - mean, c = cur[j].z - mean, e = cur[j].w - mean;
+      q += (a * a + b * b) + (c * c + e * e);
+    }
+    const float rstd = rsqrtf(warp_sum(q) * (1.0f / d) + 1e-5f);
+    if (lane == 0) {
+      mean_out[row] = mean;
+      rstd_out[row] = rstd;
+    }
+#pragma unroll
+    for (int j = 0; j < NV4; ++j) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(gamma + 128 * j) + lane);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(beta + 128 * j) + lane);
+      const uint2 pk = make_uint2(pack_bf16((cur[j].x - mean) * rstd * g.x + b.x, (cur[j].y - mean) * rstd * g.y + b.y),
+                                  pack_bf16((cur[j].z - mean) * rstd * g.z + b.z, (cur[j].w - mean) * rstd * g.w + b.w));
+      *(reinterpret_cast<uint2*>(y + (int64_t)row * d + 128 * j) + lane) = pk;
+    }
+#pragma unroll
+    for (int j = 0; j < NV4; ++j) cur[j] = nxt[j];
+  }
+}
+
 // dx = dres + rstd * (g - mean(g) - xhat * mean(g * xhat)),  g = dy * gamma
 // One 256-thread CTA walks rows; thread t owns VPT consecutive columns, so the
 // per-column dgamma/dbeta partials stay in a few registers across rows.
@@ -231,27 +285,37 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ x
   }
 }
 
-// 32 columns per CTA; warp w sums partials w, w+8, ... (fixed order), then the 8 warp
-// sums are combined in fixed order: deterministic and 64x more parallel than a column loop.
+// 16 columns per CTA, 16 partial streams (half-warps): stream s sums partials s, s+16, ...
+// (fixed order, 4 loads in flight), then the 16 stream sums are combined in fixed order.
+// Deterministic; d / 16 CTAs keep most SMs busy on the [nparts][2][d] partial block.
 __global__ void __launch_bounds__(256) ln_bwd_reduce_kernel(const float* __restrict__ work, int nparts, int d,
                                                             float* __restrict__ dgamma, float* __restrict__ dbeta) {
-  __shared__ float sg[8][32], sb[8][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int c = blockIdx.x * 32 + lane;
+  __shared__ float sg[16][17], sb[16][17];
+  const int cl = threadIdx.x & 15, sidx = threadIdx.x >> 4;
+  const int c = blockIdx.x * 16 + cl;
   float a = 0.f, b = 0.f;
   if (c < d) {
-    for (int p = w; p < nparts; p += 8) {
-      a += work[((int64_t)p * 2 + 0) * d + c];
+    int p = sidx;
+    for (; p + 48 < nparts; p += 64) {
+      const float a0 = work[((int64_t)p * 2) * d + c], a1 = work[((int64_t)(p + 16) * 2) * d + c];
+      const float a2 = work[((int64_t)(p + 32) * 2) * d + c], a3 = work[((int64_t)(p + 48) * 2) * d + c];
+      const float b0 = work[((int64_t)p * 2 + 1) * d + c], b1 = work[((int64_t)(p + 16) * 2 + 1) * d + c];
+      const float b2 = work[((int64_t)(p + 32) * 2 + 1) * d + c], b3 = work[((int64_t)(p + 48) * 2 + 1) * d + c];
+      a = (((a + a0) + a1) + a2) + a3;
+      b = (((b + b0) + b1) + b2) + b3;
+    }
+    for (; p < nparts; p += 16) {
+      a += work[((int64_t)p * 2) * d + c];
       b += work[((int64_t)p * 2 + 1) * d + c];
     }
   }
-  sg[w][lane] = a;
-  sb[w][lane] = b;
+  sg[sidx][cl] = a;
+  sb[sidx][cl] = b;
   __syncthreads();
-  if (w == 0 && c < d) {
+  if (threadIdx.x < 16 && c < d) {
     float ta = 0.f, tb = 0.f;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) { ta += sg[i][lane]; tb += sb[i][lane]; }
+    for (int i = 0; i < 16; ++i) { ta += sg[i][cl]; tb += sb[i][cl]; }
     dgamma[c] += ta;
     dbeta[c] += tb;
   }
@@ -363,8 +427,22 @@ extern "C" int fb_embed_bwd(const int32_t* d_tok, const float* d_dx, float* d_ge
 extern "C" int fb_ln_fwd(const float* d_x, const float* d_gamma, const float* d_beta, void* d_y_bf16, float* d_mean,
                          float* d_rstd, int rows, int d, void* stream) {
   FB_REQUIRE(rows > 0 && d > 0 && d <= 4096, "ln_fwd: bad shape rows=%d d=%d", rows, d);
-  const int vpt = (d + 255) / 256;
   cudaStream_t st = (cudaStream_t)stream;
+  if (d % 128 == 0 && (d / 128 == 4 || d / 128 == 6 || d / 128 == 8 || d / 128 == 16) &&
+      ((uintptr_t)d_x | (uintptr_t)d_gamma | (uintptr_t)d_beta | (uintptr_t)d_y_bf16) % 16 == 0) {
+    const int grid = std::min((rows + 7) / 8, kNumSMs * 4);
+#define CALL_W(N) ln_fwd_warp_kernel<N><<<grid, 256, 0, st>>>(d_x, d_gamma, d_beta, (__nv_bfloat16*)d_y_bf16, d_mean, d_rstd, rows)
+    switch (d / 128) {
+      case 4: CALL_W(4); break;
+      case 6: CALL_W(6); break;
+      case 8: CALL_W(8); break;
+      default: CALL_W(16); break;
+    }
+#undef CALL_W
+    FB_LAUNCH_CHECK();
+    return FB_OK;
+  }
+  const int vpt = (d + 255) / 256;
   const int grid = std::min(rows, kNumSMs * 8);
 #define CALL_F(N) ln_fwd_kernel<N><<<grid, 256, 0, st>>>(d_x, d_gamma, d_beta, (__nv_bfloat16*)d_y_bf16, d_mean, d_rstd, rows, d)
   if (vpt <= 1) CALL_F(1);
@@ -395,7 +473,7 @@ extern "C" int fb_ln_bwd(const float* d_x, const float* d_gamma, const float* d_
   else CALL_B(16);
 #undef CALL_B
   FB_LAUNCH_CHECK();
-  ln_bwd_reduce_kernel<<<(d + 31) / 32, 256, 0, st>>>(d_work, grid, d, d_dgamma, d_dbeta);
+  ln_bwd_reduce_kernel<<<(d + 15) / 16, 256, 0, st>>>(d_work, grid, d, d_dgamma, d_dbeta);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }

@@ -206,3 +206,28 @@ def test_gemm_splitk_wgrad(fb, M, N, K, ks):
             fb.EPI["acc_f32"], ks, ws.data_ptr(), ws.numel() * 4, fb.stream_handle())
     torch.cuda.synchronize()
     assert torch.equal(C1, C2)
+
+
+@pytest.mark.parametrize("M,N,K,am,epi", [(6144, 2048, 16384, 1, "acc_f32"), (2048, 8192, 16384, 1, "acc_f32"),
+                                         (4160, 2560, 4096, 1, "acc_f32"), (8192, 2048, 32000, 0, "f32")])
+def test_gemm_last_wave_split(fb, M, N, K, am, epi):
+    """Last-wave split (2-SM raster, ragged final wave cut into K ranges, fixed-order tile-local
+    reduction): == torch fp32 within reassociation, deterministic, and the same answer whether
+    or not the split is taken (ksplit = 1 runs the plain kernel)."""
+    torch.manual_seed(7)
+    dev = torch.device("cuda")
+    A = torch.randn((K, M) if am else (M, K), device=dev).to(torch.bfloat16)
+    B = torch.randn(K, N, device=dev).to(torch.bfloat16)  # MN-major B
+    base = torch.randn(M, N, device=dev) if epi == "acc_f32" else torch.zeros(M, N, device=dev)
+    ws = torch.empty(16 << 20, dtype=torch.float32, device=dev)
+    outs = []
+    for ks in (0, 0, 1):
+        C = base.clone()
+        fb.call("fb_gemm_bf16_splitk", M, N, K, A.data_ptr(), M if am else K, am, B.data_ptr(), N, 1, C.data_ptr(), N,
+                fb.EPI[epi], ks, ws.data_ptr(), ws.numel() * 4, fb.stream_handle())
+        outs.append(C)
+    torch.cuda.synchronize()
+    ref = (A.float().t() if am else A.float()) @ B.float() + (base if epi == "acc_f32" else 0)
+    torch.testing.assert_close(outs[0], ref, atol=2e-3 * K ** 0.5, rtol=1e-4)
+    assert torch.equal(outs[0], outs[1])
+    torch.testing.assert_close(outs[0], outs[2], atol=1e-3 * K ** 0.5, rtol=1e-5)

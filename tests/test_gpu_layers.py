@@ -134,7 +134,7 @@ def test_attention_bwd_all_dead_map_zeroes(fb):
     assert (dqkv.float() == 0).all()
 
 
-@pytest.mark.parametrize("rows,d", [(256, 512), (100, 768), (64, 2048), (33, 128)])
+@pytest.mark.parametrize("rows,d", [(256, 512), (100, 768), (64, 2048), (33, 128), (5003, 2048)])
 def test_layernorm(fb, rows, d):
     torch.manual_seed(1)
     dev = torch.device("cuda")

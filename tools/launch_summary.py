@@ -1,4 +1,8 @@
-"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list by kernel."""
+"""Summarise an ncu --metrics gpu__time_duration.sum --csv launch list by kernel.
+
+usage: launch_summary.py LIST.csv [START_KERNEL N]: with START_KERNEL, only the launches from
+the N-th launch whose name contains START_KERNEL up to the (N+1)-th are counted (one
+micro-batch of tools/profile_micro.py: START_KERNEL = embed_fwd_kernel, N = 2)."""
 import collections
 import csv
 import re
@@ -12,6 +16,11 @@ for r in rows:
         continue
     if hdr and len(r) == len(hdr):
         data.append(dict(zip(hdr, r)))
+data = [d for d in data if d["Metric Name"] == "gpu__time_duration.sum"]
+if len(sys.argv) > 3:
+    key, nth = sys.argv[2], int(sys.argv[3])
+    marks = [i for i, d in enumerate(data) if key in d["Kernel Name"]]
+    data = data[marks[nth - 1]: marks[nth] if len(marks) > nth else len(data)]
 agg = collections.defaultdict(lambda: [0, 0.0])
 scale = {"n": 1e-3, "u": 1.0, "m": 1e3}
 for d in data:
