@@ -108,6 +108,8 @@ enum fb_epilogue {
 /* 1 (default): use the 2-SM cta_group::2 256x256-tile kernel where the tile count fills the
  * 74 CTA pairs; 0: 1-SM kernels only (A/B comparison and tests) */
 int fb_gemm_set_2sm(int enable);
+/* A/B experiments: force the 2-SM raster group height (0 = automatic). */
+int fb_gemm_set_group_m(int group_m);
 int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, int a_major,
                  const void* d_B, int64_t ldb, int b_major, void* d_C, int64_t ldc, int epilogue,
                  const void* d_aux, void* d_aux_out, int64_t ld_aux, void* stream);

@@ -15,6 +15,7 @@
 //   TMEM        2 x BN fp32 columns: the accumulator is double-buffered so the
 //               epilogue of tile i overlaps the main loop of tile i+1
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -39,7 +40,7 @@ struct GemmCfg {
 // Grouped raster: tiles walk GROUP_M m-blocks at a time (m fastest), so the ~148 concurrently
 // resident tiles touch GROUP_M A blocks and a few B blocks that stay L2-resident.
 constexpr int kGroupM = 16;
-__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb) {
+__device__ __forceinline__ void tile_coords(int tile, int num_m, int num_n, int& mb, int& nb, int kGroupM = 16) {
   const int group_size = kGroupM * num_n;
   const int g = tile / group_size;
   const int first_m = g * kGroupM;
@@ -65,6 +66,7 @@ struct EpiArgs {
   int tail_split;
   void* tail_ws;         // f32 [pieces][256][256]
   int units;             // work units of the launch
+  int group_m;           // raster group height (2-SM kernel)
 };
 
 // work unit -> (tile, first k-block, k-block count, tail piece or -1), 2-SM kernel
@@ -635,7 +637,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
         int tile, kb0, nkb, piece;
         unit_coords2(u, num_tiles, num_kb, ep, tile, kb0, nkb, piece);
         int mb, nb;
-        tile_coords(tile, num_m, num_n, mb, nb);
+        tile_coords(tile, num_m, num_n, mb, nb, ep.group_m);
         const int m0 = mb * 256 + rank * 128;
         const int n0 = nb * 256 + rank * 128;
         for (int kb = kb0; kb < kb0 + nkb; ++kb) {
@@ -698,7 +700,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       int tile, kb0, nkb, piece;
       unit_coords2(u, num_tiles, num_kb, ep, tile, kb0, nkb, piece);
       int mb, nb;
-      tile_coords(tile, num_m, num_n, mb, nb);
+      tile_coords(tile, num_m, num_n, mb, nb, ep.group_m);
       const int m0 = mb * 256 + rank * 128;
       const int n0 = nb * 256 + half * 128;
       const int buf = it & 1;
@@ -745,6 +747,7 @@ static thread_local int g_split_n = 1;
 static thread_local void* g_tail_ws = nullptr;  // last-wave split for the current call
 static thread_local int g_tail_full = 0, g_tail_split = 1;
 int g_gemm_2sm = 1;  // fb_gemm_set_2sm() toggles it (A/B tests)
+int g_group_m_forced = 0;  // fb_gemm_set_group_m(): raster group override (A/B tests)
 
 static int get_encoder() {
   if (g_encode) return FB_OK;
@@ -898,6 +901,8 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, i
 
 namespace fb {
 extern int g_gemm_2sm;
+extern int g_group_m_forced;
+int raster_group_m(int K, int num_n);
 int gemm_dispatch(int key, int epilogue, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
                   const EpiArgs& ep, cudaStream_t st);
 }
@@ -934,7 +939,7 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   const int bbox = use2 ? 128 : BN;  // 2-SM: each CTA stages 128 of the 256 B rows
   rc = b_major ? make_map_mnmajor(&tb, d_B, N, K, ldb, bbox) : make_map_kmajor(&tb, d_B, N, K, ldb, bbox);
   if (rc) return rc;
-  EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux, 1, 0, 0, 1, nullptr, 0};
+  EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux, 1, 0, 0, 1, nullptr, 0, raster_group_m(K, (N + 255) / 256)};
   if (g_tail_ws && use2) {  // set by fb_gemm_bf16_splitk for this call only
     ep.full_tiles = g_tail_full;
     ep.tail_split = g_tail_split;
@@ -964,6 +969,7 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
 
 namespace fb {
 extern int g_gemm_2sm;
+extern int g_group_m_forced;
 int gemm_dispatch(int key, int epilogue, const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K,
                   const EpiArgs& ep, cudaStream_t st) {
   switch (key) {
@@ -979,6 +985,12 @@ int gemm_dispatch(int key, int epilogue, const CUtensorMap& ta, const CUtensorMa
   return FB_BAD_ARG;
 }
 }  // namespace fb
+
+extern "C" int fb_gemm_set_group_m(int group_m) {
+  FB_REQUIRE(group_m >= 0 && group_m <= 1024, "bad group_m %d", group_m);
+  fb::g_group_m_forced = group_m;
+  return FB_OK;
+}
 
 extern "C" int fb_gemm_set_2sm(int enable) {
   fb::g_gemm_2sm = enable ? 1 : 0;
@@ -1007,10 +1019,10 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ W, int S, int64_t
 
 // Last-wave split: C[tile] (+)= sum_s part[(tile - F) * S + s] in fixed order, for the tiles
 // [F, num_tiles) of the 2-SM raster (deterministic). Block x = tail tile, y = row slab.
-__global__ void tail_reduce_kernel(const float* __restrict__ W, int S, int F, int num_m, int num_n, int M, int N,
-                                   float* __restrict__ C, int64_t ldc, int accumulate) {
+__global__ void tail_reduce_kernel(const float* __restrict__ W, int S, int F, int num_m, int num_n, int group_m, int M,
+                                   int N, float* __restrict__ C, int64_t ldc, int accumulate) {
   int mb, nb;
-  tile_coords(F + blockIdx.x, num_m, num_n, mb, nb);
+  tile_coords(F + blockIdx.x, num_m, num_n, mb, nb, group_m);
   const float* w0 = W + (int64_t)blockIdx.x * S * 65536;
   for (int i = blockIdx.y * blockDim.x + threadIdx.x; i < 256 * 64; i += gridDim.y * blockDim.x) {
     const int r = i >> 6, c = (i & 63) * 4;
@@ -1028,6 +1040,16 @@ __global__ void tail_reduce_kernel(const float* __restrict__ W, int S, int F, in
     }
     *cp = acc;
   }
+}
+
+// Raster group height of the 2-SM kernel. Short K: 16 m-blocks (the A panels of a group are
+// small and stay in L2 across its waves). Long K (>= 4096, panels >= 2 MB): a wave of the 74
+// CTA pairs covers whole rows of n-blocks, so every A and B k-slice is shared by the tiles
+// that read it at the same time and no panel is re-fetched from DRAM in a later wave.
+int raster_group_m(int K, int num_n) {
+  if (g_group_m_forced > 0) return g_group_m_forced;  // fb_gemm_set_group_m (A/B experiments)
+  if (K >= 4096 && num_n <= kNumSMs / 2) return (kNumSMs / 2 + num_n - 1) / num_n;
+  return kGroupM;
 }
 
 // Plan the last-wave split of a 2-SM GEMM with `tiles` 256x256 tiles and num_kb k-blocks:
@@ -1078,7 +1100,8 @@ extern "C" int fb_gemm_bf16_splitk(int M, int N, int K, const void* d_A, int64_t
         g_tail_split = 1;
         if (rc) return rc;
         fb::tail_reduce_kernel<<<dim3(tiles2 - F, 16), 256, 0, (cudaStream_t)stream>>>(
-            (const float*)d_ws, S, F, (M + 255) / 256, (N + 255) / 256, M, N, (float*)d_C, ldc,
+            (const float*)d_ws, S, F, (M + 255) / 256, (N + 255) / 256, raster_group_m(K, (N + 255) / 256), M, N,
+            (float*)d_C, ldc,
             epilogue == FB_EPI_ACC_F32);
         FB_LAUNCH_CHECK();
         return FB_OK;

@@ -55,6 +55,7 @@ SIGNATURES = {
     "fb_gather_batch": [_vp, _vp, _i64, _i64, _i, _i, _vp, _vp],
     "fb_profile_begin": [_i],
     "fb_gemm_set_2sm": [_i],
+    "fb_gemm_set_group_m": [_i],
     "fb_profile_end": [_vp],
     "fb_model_fwd_bwd": [_vp, _vp, _vp, _vp, _vp, _i, _i, C.c_float, _vp, _i, _vp, _i64, _vp],
     "fb_train_step": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, AdamWCfg, _d, _d, _d, _vp, _vp, _vp, _vp, _i64, _vp],

@@ -35,3 +35,17 @@ for i in range(1 + a.iters):
              B, T, 1.0 / (B * (T - 1)), rl.data_ptr(), 1, ws.data_ptr(), ws.numel(), ext.stream_handle())
     torch.cuda.synchronize()
     print("iter", i, "loss", rl.sum().item() / (B * (T - 1)), flush=True)
+
+if os.environ.get("PM_TIME"):
+    # back-to-back micro-batches (no host sync in between), device-timed
+    n = int(os.environ["PM_TIME"])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for rep in range(3):
+        e0.record()
+        for i in range(n):
+            ext.call("fb_model_fwd_bwd", C.byref(ev._mcfg), w.data_ptr(), shadow.data_ptr(), grad.data_ptr(),
+                     tok.data_ptr(), B, T, 1.0 / (B * (T - 1)), rl.data_ptr(), 1, ws.data_ptr(), ws.numel(),
+                     ext.stream_handle())
+        e1.record()
+        torch.cuda.synchronize()
+        print(f"rep {rep}: {e0.elapsed_time(e1) / n:.2f} ms per micro-batch over {n}", flush=True)
