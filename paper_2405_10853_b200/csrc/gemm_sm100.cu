@@ -1110,6 +1110,8 @@ extern "C" int fb_gemm_bf16_splitk(int M, int N, int K, const void* d_A, int64_t
     ksplit = 1;
     while (tiles2 * ksplit < kNumSMs / 2 && num_kb / (ksplit + 1) >= 16) ++ksplit;
   }
+  // every split must own >= 1 k-block (ceil-sized splits: the last ones could be empty)
+  while (ksplit > 1 && (ksplit - 1) * ((num_kb + ksplit - 1) / ksplit) >= num_kb) --ksplit;
   if (ksplit <= 1) return fb_gemm_bf16(M, N, K, d_A, lda, a_major, d_B, ldb, b_major, d_C, ldc, epilogue, nullptr,
                                        nullptr, 0, stream);
   FB_REQUIRE(d_ws && ws_bytes >= (int64_t)ksplit * M * N * 4, "split-K workspace too small (%d splits)", ksplit);

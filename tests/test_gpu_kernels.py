@@ -231,3 +231,18 @@ def test_gemm_last_wave_split(fb, M, N, K, am, epi):
     torch.testing.assert_close(outs[0], ref, atol=2e-3 * K ** 0.5, rtol=1e-4)
     assert torch.equal(outs[0], outs[1])
     torch.testing.assert_close(outs[0], outs[2], atol=1e-3 * K ** 0.5, rtol=1e-5)
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 32000), (512, 768, 32000), (8192, 512, 32000), (128, 2048, 32000)])
+def test_gemm_splitk_head_dgrad(fb, M, N, K):
+    """LM-head dgrad through the split-K entry (K-major dlogits A, MN-major W_head B, f32 out)."""
+    torch.manual_seed(8)
+    dev = torch.device("cuda")
+    A = torch.randn(M, K, device=dev).to(torch.bfloat16)
+    B = torch.randn(K, N, device=dev).to(torch.bfloat16)
+    C = torch.full((M, N), 7.0, device=dev)
+    ws = torch.empty(16 << 20, dtype=torch.float32, device=dev)
+    fb.call("fb_gemm_bf16_splitk", M, N, K, A.data_ptr(), K, 0, B.data_ptr(), N, 1, C.data_ptr(), N, fb.EPI["f32"], 0,
+            ws.data_ptr(), ws.numel() * 4, fb.stream_handle())
+    torch.cuda.synchronize()
+    torch.testing.assert_close(C, A.float() @ B.float(), atol=2e-3 * K ** 0.5, rtol=1e-4)
