@@ -103,7 +103,8 @@ enum fb_epilogue {
   FB_EPI_RESID_F32 = 3,  /* C(f32) = aux(f32) + acc  (residual add; aux may alias C) */
   FB_EPI_GELU = 4,       /* C(bf16) = gelu_erf(acc); aux_out(bf16) = acc (pre-activation) */
   FB_EPI_DGELU = 5,      /* C(bf16) = acc * gelu_erf'(aux(bf16)) */
-  FB_EPI_RESID_F32_BF16 = 6 /* C(f32) = aux(f32) + acc and aux_out(bf16) = same */
+  FB_EPI_RESID_F32_BF16 = 6, /* C(f32) = aux(f32) + acc and aux_out(bf16) = same */
+  FB_EPI_BF16_ROWDOT = 7     /* C(bf16) = acc and per-head row dots with aux: fb_gemm_bf16_rowdot only */
 };
 /* 1 (default): use the 2-SM cta_group::2 256x256-tile kernel where the tile count fills the
  * 74 CTA pairs; 0: 1-SM kernels only (A/B comparison and tests) */
@@ -120,6 +121,16 @@ int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, int a_major,
 int fb_gemm_bf16_splitk(int M, int N, int K, const void* d_A, int64_t lda, int a_major,
                         const void* d_B, int64_t ldb, int b_major, void* d_C, int64_t ldc, int epilogue,
                         int ksplit, void* d_ws, int64_t ws_bytes, void* stream);
+
+/* Attention-backward pre-pass fused into the out-projection dgrad (dO = dY W_proj):
+ * C(bf16) = dO and D[b][h][t] = sum_{c in head h} bf16(dO)[row][c] * O[row][c] (row = b*T + t,
+ * f32 [B][H][T], the rowsum(dO o O) of the attention backward, model.py:92-98). Runs on the
+ * 2-SM kernel only (each epilogue warp drains 128 head-aligned columns of its rows);
+ * returns FB_UNSUPPORTED (nothing launched) when that kernel does not apply, so the caller
+ * falls back to fb_gemm_bf16 + fb_attn_bwd's own pre-pass. Needs 128 % dh == 0, dh % 32 == 0. */
+int fb_gemm_bf16_rowdot(int M, int N, int K, const void* d_A, int64_t lda, int a_major,
+                        const void* d_B, int64_t ldb, int b_major, void* d_C, int64_t ldc,
+                        const void* d_O, int64_t ld_o, float* d_D, int T, int dh, void* stream);
 
 /* ---- transformer pieces (model.py:75-150, :222-229) --------------------------------- */
 int fb_embed_fwd(const int32_t* d_tok, const float* d_emb, const float* d_pos, float* d_x,
@@ -146,6 +157,12 @@ int fb_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, uint8_t* d_live, int
 int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
                 const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh,
                 int use_alibi, void* stream);
+/* flags: FB_ATTN_D_READY = d_work[0 : B*H*T] already holds D = rowsum(dO o O)
+ * (fb_gemm_bf16_rowdot), so the pre-pass only zeroes the dQ accumulator. */
+enum { FB_ATTN_D_READY = 1 };
+int fb_attn_bwd_ex(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
+                   const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh,
+                   int use_alibi, int flags, void* stream);
 /* Mean next-token CE over B*(T-1) positions (model.py:226-229): logits f32 [rows][V]
  * for a chunk of rows [row0, row0+rows) of a B x T batch; writes dlogits(bf16) =
  * scale*(softmax - onehot) (0 on each sequence's last position) and adds the summed

@@ -63,14 +63,18 @@ int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const 
 
 template <int DH>
 static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const float* lse, const uint8_t* live,
-                           void* dqkv, float* work, int B, int T, int H, int use_alibi, cudaStream_t st) {
+                           void* dqkv, float* work, int B, int T, int H, int use_alibi, int flags, cudaStream_t st) {
   const int d = H * DH;
   float* Dbuf = work;
   float* dq = work + (int64_t)B * H * T;
   const int nw = B * T * H;
-  attn_bwd_dot_kernel<<<(nw + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dO, Dbuf, dq, B, T, H,
-                                                    DH);
-  FB_LAUNCH_CHECK();
+  if (flags & FB_ATTN_D_READY) {  // D came from the out-projection dgrad epilogue: only zero dQ
+    FB_CUDA_TRY(cudaMemsetAsync(dq, 0, sizeof(float) * (size_t)B * T * d, st));
+  } else {
+    attn_bwd_dot_kernel<<<(nw + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dO, Dbuf, dq, B, T,
+                                                      H, DH);
+    FB_LAUNCH_CHECK();
+  }
   int rc = attn_bwd_tc_launch<DH>(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
   if (rc) return rc;
   dq_finalize_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq, (__nv_bfloat16*)dqkv, B * T, d);
@@ -101,14 +105,21 @@ extern "C" int fb_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, uint8_t* 
 extern "C" int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
                            const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh, int use_alibi,
                            void* stream) {
+  return fb_attn_bwd_ex(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, dh, use_alibi, 0, stream);
+}
+
+extern "C" int fb_attn_bwd_ex(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
+                              const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh,
+                              int use_alibi, int flags, void* stream) {
   FB_REQUIRE(B > 0 && H > 0 && T > 0 && T % 128 == 0, "attn_bwd: T must be a positive multiple of 128 (T=%d)", T);
   FB_REQUIRE(d_work != nullptr, "attn_bwd: needs a work buffer of B*H*T + B*T*H*dh floats");
   cudaStream_t st = (cudaStream_t)stream;
   const double fl = 2.0 * 2.0 * 2.0 * B * H * (double)T * (T + 1) / 2.0 * dh;  // bwd = 2x fwd
   const int pi = prof_on() ? prof_start(2, st) : -1;
   int rc = FB_UNSUPPORTED;
-  if (dh == 64) rc = attn_bwd_launch<64>(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, use_alibi, st);
-  else if (dh == 128) rc = attn_bwd_launch<128>(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, use_alibi, st);
+  if (dh == 64) rc = attn_bwd_launch<64>(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, use_alibi, flags, st);
+  else if (dh == 128)
+    rc = attn_bwd_launch<128>(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, use_alibi, flags, st);
   prof_stop(2, pi, st, fl);
   if (rc != FB_UNSUPPORTED) return rc;
   set_error("attn_bwd: head dim %d unsupported (64 or 128)", dh);

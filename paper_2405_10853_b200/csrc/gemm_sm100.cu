@@ -67,6 +67,7 @@ struct EpiArgs {
   void* tail_ws;         // f32 [pieces][256][256]
   int units;             // work units of the launch
   int group_m;           // raster group height (2-SM kernel)
+  int rd_T, rd_dh;       // FB_EPI_BF16_ROWDOT: sequence length, head dim
 };
 
 // work unit -> (tile, first k-block, k-block count, tail piece or -1), 2-SM kernel
@@ -478,7 +479,7 @@ __device__ __forceinline__ void partial_chunk_tma(const CUtensorMap* map, uint8_
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& e, const EpiMaps& mp, uint8_t* stg, int lane,
                                                    int64_t row, int row0, int col, int split, int M, int N,
-                                                   const uint32_t (&r)[32]) {
+                                                   const uint32_t (&r)[32], float& rd) {
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -534,10 +535,29 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& e, const EpiMa
       _Pragma("unroll") for (int i = 0; i < 32; ++i) v[i] = (in && col + i < N) ? v[i] * gelu_erf_grad(__bfloat162float(P[i])) : 0.f;
     }
   }
+  if constexpr (EPI == FB_EPI_BF16_ROWDOT) {  // rd += bf16(dO) . O over these 32 columns of the head
+    if (in && full) {
+      const __nv_bfloat16* O = reinterpret_cast<const __nv_bfloat16*>(e.aux) + row * e.ld_aux + col;
+      float acc = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 pk = *reinterpret_cast<const uint4*>(O + 8 * q);
+        const __nv_bfloat162* ob = reinterpret_cast<const __nv_bfloat162*>(&pk);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 o2 = __bfloat1622float2(ob[i]);
+          const float2 g2 = __bfloat1622float2(__floats2bfloat162_rn(v[8 * q + 2 * i], v[8 * q + 2 * i + 1]));
+          acc = fmaf(g2.x, o2.x, acc);
+          acc = fmaf(g2.y, o2.y, acc);
+        }
+      }
+      rd += acc;
+    }
+  }
   // ---- staging (the previous chunk's bulk store must have read the tile) ----
   if (lane == 0) bulk_wait_read<0>();
   __syncwarp();
-  constexpr bool kBf16Out = EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU;
+  constexpr bool kBf16Out = EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU || EPI == FB_EPI_BF16_ROWDOT;
   if constexpr (kBf16Out) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) stg_put_bf16(stg, lane, j, v + 8 * j);
@@ -709,6 +729,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       tc_fence_after();
       const int row0 = m0 + quad * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * 256 + half * 128;
+      float rd = 0.f;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t r[32];
@@ -724,7 +745,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (piece >= 0)
             partial_chunk_tma(&maps.Part, stg, lane, col - nb * 256, row0 - mb * 256, piece, r);
           else
-            epilogue_chunk_tma<EPI>(ep, maps, stg, lane, row0 + lane, row0, col, u / num_tiles, M, N, r);
+            epilogue_chunk_tma<EPI>(ep, maps, stg, lane, row0 + lane, row0, col, u / num_tiles, M, N, r, rd);
+        }
+        if constexpr (EPI == FB_EPI_BF16_ROWDOT) {  // head boundary: D[b][h][t] of this lane's row
+          if ((col + 32) % ep.rd_dh == 0) {
+            const int row = row0 + lane;
+            if (row < M && col < N) {
+              const int T = ep.rd_T, nh = N / ep.rd_dh;
+              reinterpret_cast<float*>(ep.aux_out)[((int64_t)(row / T) * nh + col / ep.rd_dh) * T + row % T] = rd;
+            }
+            rd = 0.f;
+          }
         }
       }
     }
@@ -746,6 +777,7 @@ static thread_local void* g_split_ws = nullptr;  // split-K workspace for the cu
 static thread_local int g_split_n = 1;
 static thread_local void* g_tail_ws = nullptr;  // last-wave split for the current call
 static thread_local int g_tail_full = 0, g_tail_split = 1;
+static thread_local int g_rd_T = 0, g_rd_dh = 0;  // fb_gemm_bf16_rowdot for the current call
 int g_gemm_2sm = 1;  // fb_gemm_set_2sm() toggles it (A/B tests)
 int g_group_m_forced = 0;  // fb_gemm_set_group_m(): raster group override (A/B tests)
 
@@ -833,7 +865,7 @@ static int make_out_map(CUtensorMap* m, void* ptr, bool bf16, int M, int N, int6
 template <int A_MN, int B_MN, int EPI>
 static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiArgs& ep,
                           cudaStream_t st) {
-  constexpr bool kBf16Out = EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU;
+  constexpr bool kBf16Out = EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU || EPI == FB_EPI_BF16_ROWDOT;
   EpiMaps maps;
   int rc = make_out_map(&maps.C, ep.C, kBf16Out, M, N, ep.ldc, ep.ksplit, ep.split_stride);
   if (rc) return rc;
@@ -876,6 +908,7 @@ static int dispatch_epi2(int epi, const CUtensorMap& ta, const CUtensorMap& tb, 
     case FB_EPI_GELU: return launch_gemm2_t<A_MN, B_MN, FB_EPI_GELU>(ta, tb, M, N, K, ep, st);
     case FB_EPI_DGELU: return launch_gemm2_t<A_MN, B_MN, FB_EPI_DGELU>(ta, tb, M, N, K, ep, st);
     case FB_EPI_RESID_F32_BF16: return launch_gemm2_t<A_MN, B_MN, FB_EPI_RESID_F32_BF16>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_BF16_ROWDOT: return launch_gemm2_t<A_MN, B_MN, FB_EPI_BF16_ROWDOT>(ta, tb, M, N, K, ep, st);
   }
   set_error("unknown epilogue %d", epi);
   return FB_BAD_ARG;
@@ -939,7 +972,12 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   const int bbox = use2 ? 128 : BN;  // 2-SM: each CTA stages 128 of the 256 B rows
   rc = b_major ? make_map_mnmajor(&tb, d_B, N, K, ldb, bbox) : make_map_kmajor(&tb, d_B, N, K, ldb, bbox);
   if (rc) return rc;
-  EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux, 1, 0, 0, 1, nullptr, 0, raster_group_m(K, (N + 255) / 256)};
+  if (epilogue == FB_EPI_BF16_ROWDOT && (!use2 || g_rd_T <= 0)) {
+    set_error("gemm: the row-dot epilogue needs the 2-SM kernel (fb_gemm_bf16_rowdot)");
+    return FB_UNSUPPORTED;
+  }
+  EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux, 1, 0, 0, 1, nullptr, 0, raster_group_m(K, (N + 255) / 256),
+             g_rd_T, g_rd_dh};
   if (g_tail_ws && use2) {  // set by fb_gemm_bf16_splitk for this call only
     ep.full_tiles = g_tail_full;
     ep.tail_split = g_tail_split;
@@ -985,6 +1023,25 @@ int gemm_dispatch(int key, int epilogue, const CUtensorMap& ta, const CUtensorMa
   return FB_BAD_ARG;
 }
 }  // namespace fb
+
+extern "C" int fb_gemm_bf16_rowdot(int M, int N, int K, const void* d_A, int64_t lda, int a_major, const void* d_B,
+                                   int64_t ldb, int b_major, void* d_C, int64_t ldc, const void* d_O, int64_t ld_o,
+                                   float* d_D, int T, int dh, void* stream) {
+  FB_REQUIRE(d_O && d_D && T > 0 && M % T == 0, "rowdot: needs O, D and M %% T == 0");
+  FB_REQUIRE(dh >= 32 && dh % 32 == 0 && 128 % dh == 0 && N % dh == 0, "rowdot: head dim %d unsupported", dh);
+  FB_REQUIRE(ld_o % 8 == 0 && (uintptr_t)d_O % 16 == 0, "rowdot: O must be 16-byte aligned rows");
+  const int tiles2 = ((M + 255) / 256) * ((N + 255) / 256);
+  if (!(g_gemm_2sm && M >= 256 && N >= 256 && tiles2 >= kNumSMs / 2)) {
+    set_error("rowdot: the 2-SM kernel does not apply to %d x %d", M, N);
+    return FB_UNSUPPORTED;
+  }
+  g_rd_T = T;
+  g_rd_dh = dh;
+  const int rc = fb_gemm_bf16(M, N, K, d_A, lda, a_major, d_B, ldb, b_major, d_C, ldc, FB_EPI_BF16_ROWDOT, d_O, d_D,
+                              ld_o, stream);
+  g_rd_T = g_rd_dh = 0;
+  return rc;
+}
 
 extern "C" int fb_gemm_set_group_m(int group_m) {
   FB_REQUIRE(group_m >= 0 && group_m <= 1024, "bad group_m %d", group_m);

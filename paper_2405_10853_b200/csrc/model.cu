@@ -141,6 +141,10 @@ using namespace fb;
 
 extern "C" int fb_gemm_bf16(int, int, int, const void*, int64_t, int, const void*, int64_t, int, void*, int64_t, int,
                             const void*, void*, int64_t, void*);
+extern "C" int fb_gemm_bf16_rowdot(int, int, int, const void*, int64_t, int, const void*, int64_t, int, void*, int64_t,
+                                   const void*, int64_t, float*, int, int, void*);
+extern "C" int fb_attn_bwd_ex(const void*, const void*, const void*, const float*, const uint8_t*, void*, float*, int,
+                              int, int, int, int, int, void*);
 extern "C" int fb_gemm_bf16_splitk(int, int, int, const void*, int64_t, int, const void*, int64_t, int, void*, int64_t,
                                    int, int, void*, int64_t, void*);
 
@@ -225,9 +229,16 @@ extern "C" int fb_model_fwd_bwd(const fb_model_cfg* cfgp, const float* P, const 
     TRY(fb_ln_bwd(a.x_mid, P + b.ln2_w, a.mean2, a.rstd2, w.dln, w.dx, w.dx, w.dxb, G + b.ln2_w, G + b.ln2_b,
                   w.ln_work, M, d, st));
     // attention: x_mid = x_in + proj(attn(ln1(x_in)))
-    TRY(fb_gemm_bf16(M, d, d, w.dxb, d, 0, S + b.proj, d, 1, w.dao, d, FB_EPI_BF16, nullptr, nullptr, 0, st));
+    // dO = dY W_proj; its epilogue also forms the attention backward's D = rowsum(dO o O)
+    int aflags = FB_ATTN_D_READY;
+    int rc = fb_gemm_bf16_rowdot(M, d, d, w.dxb, d, 0, S + b.proj, d, 1, w.dao, d, a.ao, d, w.attn_work, T, dh, st);
+    if (rc == FB_UNSUPPORTED) {
+      aflags = 0;
+      rc = fb_gemm_bf16(M, d, d, w.dxb, d, 0, S + b.proj, d, 1, w.dao, d, FB_EPI_BF16, nullptr, nullptr, 0, st);
+    }
+    TRY(rc);
     TRY(wgrad(d, d, w.dxb, d, a.ao, d, G + b.proj));
-    TRY(fb_attn_bwd(a.qkv, a.ao, w.dao, a.lse, a.live, w.dqkv, w.attn_work, B, T, H, dh, c.use_alibi, st));
+    TRY(fb_attn_bwd_ex(a.qkv, a.ao, w.dao, a.lse, a.live, w.dqkv, w.attn_work, B, T, H, dh, c.use_alibi, aflags, st));
     TRY(fb_gemm_bf16(M, d, 3 * d, w.dqkv, 3 * d, 0, S + b.qkv, d, 1, w.dln, d, FB_EPI_F32, nullptr, nullptr, 0, st));
     TRY(wgrad(3 * d, d, w.dqkv, 3 * d, a.ln1, d, G + b.qkv));
     TRY(fb_ln_bwd(a.x_in, P + b.ln1_w, a.mean1, a.rstd1, w.dln, w.dx, w.dx, w.dxb, G + b.ln1_w, G + b.ln1_b,

@@ -17,7 +17,7 @@ FB_OK, FB_BAD_ARG, FB_CUDA_ERROR, FB_NONFINITE, FB_UNSUPPORTED = 0, 1, 2, 3, 4
 FB_RED_BLOCKS = 1184
 FB_MAX_CLIENTS = 64
 
-EPI = {"bf16": 0, "f32": 1, "acc_f32": 2, "resid_f32": 3, "gelu": 4, "dgelu": 5, "resid_f32_bf16": 6}
+EPI = {"bf16": 0, "f32": 1, "acc_f32": 2, "resid_f32": 3, "gelu": 4, "dgelu": 5, "resid_f32_bf16": 6, "bf16_rowdot": 7}
 
 _vp, _i, _i64, _d = C.c_void_p, C.c_int, C.c_int64, C.c_double
 
@@ -51,6 +51,8 @@ SIGNATURES = {
     "fb_ln_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp],
     "fb_attn_fwd": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "fb_attn_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
+    "fb_attn_bwd_ex": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
+    "fb_gemm_bf16_rowdot": [_i, _i, _i, _vp, _i64, _i, _vp, _i64, _i, _vp, _i64, _vp, _i64, _vp, _i, _i, _vp],
     "fb_ce_fwd_bwd": [_vp, _vp, _vp, _i, _i, _i, _i, C.c_float, _vp, _vp],
     "fb_gather_batch": [_vp, _vp, _i64, _i64, _i, _i, _vp, _vp],
     "fb_profile_begin": [_i],

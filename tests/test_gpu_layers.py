@@ -215,3 +215,54 @@ def test_cross_entropy(fb, V):
     torch.cuda.synchronize()
     assert row_loss.sum().item() * scale == pytest.approx(ref.item(), rel=1e-5)
     torch.testing.assert_close(dl.float(), lg.grad.view(B * T, V), atol=1e-6, rtol=1e-2)
+
+
+@pytest.mark.parametrize("B,T,H,dh", [(8, 2048, 16, 128), (16, 1024, 8, 64), (1, 512, 4, 128)])
+def test_outproj_dgrad_rowdot_feeds_attention_bwd(fb, B, T, H, dh):
+    """dO = dY W_proj with D = rowsum(bf16(dO) o O) fused into the GEMM epilogue (fb_gemm_bf16_rowdot):
+    dO is bit-identical to the plain bf16 GEMM, D matches torch, and fb_attn_bwd_ex(FB_ATTN_D_READY)
+    gives the same dQ/dK/dV as fb_attn_bwd (which forms D itself) up to f32 summation order."""
+    torch.manual_seed(3)
+    dev = torch.device("cuda")
+    d, M = H * dh, B * T
+    dY = (torch.randn(M, d, device=dev) * 0.5).to(torch.bfloat16)
+    W = (torch.randn(d, d, device=dev) * d ** -0.5).to(torch.bfloat16)   # proj weight [out][in], MN-major B for dgrad
+    O = torch.randn(M, d, device=dev).to(torch.bfloat16)
+    dO_plain = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+    dO = torch.empty_like(dO_plain)
+    D = torch.full((B * H * T,), float("nan"), device=dev)
+    fb.call("fb_gemm_bf16", M, d, d, dY.data_ptr(), d, 0, W.data_ptr(), d, 1, dO_plain.data_ptr(), d, fb.EPI["bf16"],
+            None, None, 0, fb.stream_handle())
+    rc = fb.lib().fb_gemm_bf16_rowdot(M, d, d, dY.data_ptr(), d, 0, W.data_ptr(), d, 1, dO.data_ptr(), d,
+                                      O.data_ptr(), d, D.data_ptr(), T, dh, fb.stream_handle())
+    if M < 256 or (M // 256) * (d // 256) < 74:  # only the 2-SM kernel fuses; the model then falls back
+        assert rc == fb.FB_UNSUPPORTED
+        return
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert torch.equal(dO, dO_plain)
+    ref = (dO.float() * O.float()).view(B, T, H, dh).sum(-1).permute(0, 2, 1).reshape(-1)
+    torch.testing.assert_close(D, ref, atol=1e-3, rtol=1e-4)
+    # attention backward with the fused D vs with its own pre-pass
+    qkv = torch.randn(M, 3 * d, device=dev).to(torch.bfloat16)
+    o = torch.empty(M, d, dtype=torch.bfloat16, device=dev)
+    lse2 = torch.empty(B * H * T, dtype=torch.float32, device=dev)
+    live = torch.empty(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device=dev)
+    fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), live.data_ptr(), B, T, H, dh, 1,
+            fb.stream_handle())
+    rc = fb.lib().fb_gemm_bf16_rowdot(M, d, d, dY.data_ptr(), d, 0, W.data_ptr(), d, 1, dO.data_ptr(), d,
+                                      o.data_ptr(), d, D.data_ptr(), T, dh, fb.stream_handle())
+    assert rc == 0
+    work = torch.empty(B * H * T + M * d, dtype=torch.float32, device=dev)
+    work[: B * H * T].copy_(D)
+    work[B * H * T:].fill_(123.0)  # the D_READY path must zero dQ itself
+    g1 = torch.empty_like(qkv)
+    g2 = torch.empty_like(qkv)
+    fb.call("fb_attn_bwd_ex", qkv.data_ptr(), o.data_ptr(), dO.data_ptr(), lse2.data_ptr(), live.data_ptr(),
+            g1.data_ptr(), work.data_ptr(), B, T, H, dh, 1, 1, fb.stream_handle())
+    work2 = torch.empty_like(work)
+    fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), dO.data_ptr(), lse2.data_ptr(), live.data_ptr(),
+            g2.data_ptr(), work2.data_ptr(), B, T, H, dh, 1, fb.stream_handle())
+    torch.cuda.synchronize()
+    torch.testing.assert_close(work[: B * H * T], work2[: B * H * T], atol=1e-3, rtol=1e-4)
+    torch.testing.assert_close(g1.float(), g2.float(), atol=2e-2, rtol=2e-2)
