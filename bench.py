@@ -112,7 +112,8 @@ def launches_per_step(c):
     L, d, M = c["L"], c["d"], c["B"] * c["T"]
     chunks = math.ceil(M / 8192)
     # forward: gather + embed + L x (ln, qkv, attn, proj, ln, fc, proj2) + ln_f + chunks x (logits, ce, dgrad, wgrad)
-    fwd = 1 + 1 + 7 * L + 1 + 4 * chunks + chunks * (tail_split(8192, d, c["V"]) > 1)  # + head-dgrad reductions
+    hd = min(M, 8192)  # head-dgrad rows per chunk: a last-wave split or a classic split-K adds one reduction
+    fwd = 1 + 1 + 7 * L + 1 + 4 * chunks + chunks * (tail_split(hd, d, c["V"]) > 1 or splitk_splits(hd, d, c["V"]) > 1)
     # backward: ln_f bwd(2) + L x (dgelu, wgrad, dgrad, wgrad, ln bwd(2), dgrad, wgrad, attn bwd(3), dgrad, wgrad,
     # ln bwd(2)) + split-K reduction launches + embed bwd
     wg = [(d, 4 * d), (4 * d, d), (d, d), (3 * d, d)]
