@@ -38,6 +38,29 @@ __device__ __forceinline__ float ex2b(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// packed f32x2 (FFMA2 / FADD2 / FMUL2): per-lane identical to the scalar ops, half the issue slots
+__device__ __forceinline__ float2 pk_fma(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 pk_sub(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 pk_mul(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
@@ -256,7 +279,11 @@ __global__ void __launch_bounds__(320, 1)
       if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       asm volatile("bar.sync 2, 256;" ::: "memory");
 #pragma unroll
-      for (int i = 0; i < 32; ++i) Xs[(32 * g + i) * DH + r] = __uint_as_float(v[i]) * scale;
+      for (int i = 0; i < 32; i += 2) {
+        const float2 sv2 = pk_mul(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), make_float2(scale, scale));
+        Xs[(32 * g + i) * DH + r] = sv2.x;
+        Xs[(32 * g + i + 1) * DH + r] = sv2.y;
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync 2, 256;" ::: "memory");
       if (tid == 0) {
@@ -307,11 +334,18 @@ __global__ void __launch_bounds__(320, 1)
         const float ev[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
         const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < 8; i += 2) {
+          const float2 be = pk_sub(make_float2(slk, slk), make_float2(ev[i], ev[i + 1]));
+          const float2 x = pk_fma(make_float2(__uint_as_float(sv[q * 8 + i]), __uint_as_float(sv[q * 8 + i + 1])),
+                                  make_float2(scale_log2, scale_log2), be);
           const int ql = 32 * g + q * 8 + i;
-          const float x = fmaf(__uint_as_float(sv[q * 8 + i]), scale_log2, slk - ev[i]);
-          p[i] = (diag && q0 + ql < kj) ? 0.f : ex2b(x);
-          ds[i] = p[i] * (__uint_as_float(pv[q * 8 + i]) - dv[i]);
+          p[i] = (diag && q0 + ql < kj) ? 0.f : ex2b(x.x);
+          p[i + 1] = (diag && q0 + ql + 1 < kj) ? 0.f : ex2b(x.y);
+          const float2 dd = pk_sub(make_float2(__uint_as_float(pv[q * 8 + i]), __uint_as_float(pv[q * 8 + i + 1])),
+                                   make_float2(dv[i], dv[i + 1]));
+          const float2 d2 = pk_mul(make_float2(p[i], p[i + 1]), dd);
+          ds[i] = d2.x;
+          ds[i + 1] = d2.y;
         }
         const int kc = 4 * g + q;
         const uint32_t sw = ((kc ^ (r & 7)) << 4);

@@ -29,11 +29,19 @@ torch.cuda.synchronize()
 buf = (C.c_ulonglong * 4096)()
 L.fb_attn_trace_read.argtypes = [C.c_void_p, C.c_int]
 assert L.fb_attn_trace_read(buf, 4096) == 0
-a = np.array(buf[:16 * 12], dtype=np.int64).reshape(12, 16)
-t0 = a[0, 0]
-names = ["mma:S", "mma:dP", "mma:p_full", "mma:ds_full", "sm:start", "sm:s_full", "sm:P_done", "sm:p_free",
-         "sm:dS_done", "sm:dq_full", "sm:drain_done"]
-for t in range(12):
-    if a[t, 0] == 0:
+a = np.array(buf[:16 * 24], dtype=np.int64).reshape(24, 16)
+t0 = a[0, 0] if a[0, 0] else a[0, 4]
+names = {0: "mma:pds_full", 1: "mma:S/dP(t+1) issued", 2: "mma:dV,dK issued", 3: "mma:dq_empty",
+         4: "sm:wait_S", 5: "sm:S_ready", 6: "sm:P/dS_stored", 7: "sm:drain(t-1)_done"}
+for t in range(24):
+    if a[t, 4] == 0:
         break
-    print(f"tile {t}: " + " ".join(f"{n}={(a[t, i] - t0) / 1000:.2f}" for i, n in enumerate(names)))
+    print(f"tile {t:2d}: " + " ".join(f"{n}={(a[t, i] - t0) / 1000:7.2f}" for i, n in names.items()))
+d = np.diff(a[:, 5][a[:, 5] > 0]) / 1000
+print("per-tile period (us):", np.round(d, 2))
+ew = (a[:, 6] - a[:, 5])[a[:, 5] > 0] / 1000
+dr = (a[:, 7] - a[:, 6])[a[:, 5] > 0] / 1000
+ws = (a[:, 5] - a[:, 4])[a[:, 5] > 0] / 1000
+print("elementwise (us):", np.round(ew, 2))
+print("drain (us):", np.round(dr, 2))
+print("wait for S (us):", np.round(ws, 2))
