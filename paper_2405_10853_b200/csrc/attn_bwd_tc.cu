@@ -15,6 +15,8 @@
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -324,6 +326,9 @@ __global__ void __launch_bounds__(320, 1)
       // P^T / dS^T buffers [s] were last read by the MMAs of tile t-2
       if (t >= 2) mbar_wait(&pds_free[s], ((t >> 1) & 1) ^ 1);
       const uint32_t prow = sP0 + s * Cf::PT + r * 128, srow = sS0 + s * Cf::PT + r * 128;
+      // the causal mask only touches the two diagonal tiles: the other tiles run a mask-free copy
+      auto elementwise = [&](auto diag_t) {
+      constexpr bool kDiag = decltype(diag_t)::value;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         float p[8], ds[8];
@@ -339,8 +344,8 @@ __global__ void __launch_bounds__(320, 1)
           const float2 x = pk_fma(make_float2(__uint_as_float(sv[q * 8 + i]), __uint_as_float(sv[q * 8 + i + 1])),
                                   make_float2(scale_log2, scale_log2), be);
           const int ql = 32 * g + q * 8 + i;
-          p[i] = (diag && q0 + ql < kj) ? 0.f : ex2b(x.x);
-          p[i + 1] = (diag && q0 + ql + 1 < kj) ? 0.f : ex2b(x.y);
+          p[i] = (kDiag && q0 + ql < kj) ? 0.f : ex2b(x.x);
+          p[i + 1] = (kDiag && q0 + ql + 1 < kj) ? 0.f : ex2b(x.y);
           const float2 dd = pk_sub(make_float2(__uint_as_float(pv[q * 8 + i]), __uint_as_float(pv[q * 8 + i + 1])),
                                    make_float2(dv[i], dv[i + 1]));
           const float2 d2 = pk_mul(make_float2(p[i], p[i + 1]), dd);
@@ -354,6 +359,9 @@ __global__ void __launch_bounds__(320, 1)
         asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(srow + sw), "r"(pack_bf16(ds[0], ds[1])),
                      "r"(pack_bf16(ds[2], ds[3])), "r"(pack_bf16(ds[4], ds[5])), "r"(pack_bf16(ds[6], ds[7])));
       }
+      };
+      if (diag) elementwise(std::true_type{});
+      else elementwise(std::false_type{});
       tc_fence_before();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
