@@ -118,7 +118,10 @@ def launches_per_step(c):
     # ln bwd(2)) + split-K reduction launches + embed bwd
     wg = [(d, 4 * d), (4 * d, d), (d, d), (3 * d, d)]
     red = sum(1 for (mm, nn) in wg if splitk_splits(mm, nn, M) > 1 or tail_split(mm, nn, M) > 1)
-    bwd = 2 + L * (15 + red) + 1
+    # attention bwd: 3 launches (D pre-pass, kernel, dQ finalize); 2 when the out-projection dgrad
+    # forms D in its epilogue (fb_gemm_bf16_rowdot: 2-SM raster, i.e. >= 74 256x256 tiles)
+    rowdot = M >= 256 and d >= 256 and (M // 256) * (d // 256) >= 74
+    bwd = 2 + L * (15 - rowdot + red) + 1
     return c["micro"] * (fwd + bwd) + 4  # + sumsq, step_prepare, adamw, telemetry
 
 
