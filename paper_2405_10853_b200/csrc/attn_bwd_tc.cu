@@ -268,6 +268,8 @@ __global__ void __launch_bounds__(320, 1)
     const int tid = threadIdx.x - 64;  // 0..255
     float* Xs = reinterpret_cast<float*>(smem + Cf::X_OFF);
     auto drain = [&](int t) {  // dQ^T(t) -> staging [64 q][128 dh] -> TMA reduce-add into dq rows
+      // each warpgroup g drains its own 32 query rows (one 32 x 128 reduce box, its own named
+      // barrier), so the two groups do not wait for each other's elementwise skew
       const int q0 = (first + tl[t]) * 64;
       mbar_wait(dq_full, t & 1);
       tc_fence_after();
@@ -277,9 +279,9 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
-      // the staging box of the previous reduce must have been read by TMA
-      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      asm volatile("bar.sync 2, 256;" ::: "memory");
+      // this group's staging box of the previous reduce must have been read by TMA
+      if ((tid & 127) == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         const float2 sv2 = pk_mul(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), make_float2(scale, scale));
@@ -287,24 +289,27 @@ __global__ void __launch_bounds__(320, 1)
         Xs[(32 * g + i + 1) * DH + r] = sv2.y;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync 2, 256;" ::: "memory");
-      if (tid == 0) {
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
+      if ((tid & 127) == 0) {
         asm volatile(
             "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                 reinterpret_cast<uint64_t>(&tm_dq)),
-            "r"(sX), "r"(h * DH), "r"(row0 + q0)
+            "r"(sX + g * 32 * DH * 4), "r"(h * DH), "r"(row0 + q0 + 32 * g)
             : "memory");
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
     // e/D of tile t live in buffer t & 1; tile t+1's are prefetched before drain(t-1), whose
-    // CTA-wide barriers publish them (all readers of that buffer finished tile t-1 earlier)
+    // warpgroup barriers publish them (all readers of that buffer finished tile t-1 earlier)
     auto load_ed = [&](int t) {
       const int q0 = (first + tl[t]) * 64;
       float* E = sE0 + (t & 1) * 64;
       float* Dv = sD0 + (t & 1) * 64;
-      if (tid < 64) E[tid] = sl * (float)(q0 + tid) + lse2[(int64_t)bh * T + q0 + tid];
-      else if (tid < 128) Dv[tid - 64] = Dd[(int64_t)bh * T + q0 + tid - 64];
+      // warpgroup g reads only queries [32g, 32g + 32) of the tile, so it loads that half itself
+      // (published to its readers by its own drain barriers)
+      const int j = tid & 127, qq = 32 * g + (j & 31);
+      if (j < 32) E[qq] = sl * (float)(q0 + qq) + lse2[(int64_t)bh * T + q0 + qq];
+      else if (j < 64) Dv[qq] = Dd[(int64_t)bh * T + q0 + qq];
     };
     if (nlive > 0) load_ed(0);
     asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(320, 1)
       if (warp == 2 && lane == 0) TRACE(16 * t + 7);
     }
     if (nlive > 0) drain(nlive - 1);
-    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    if ((tid & 127) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     // dK, dV (the last dK/dV MMAs completed before the last dq_full)
     const int64_t ld = 3 * (int64_t)d;
     __nv_bfloat16* dkrow = dqkv + ((int64_t)row0 + kj) * ld + d + h * DH + (DH / 2) * g;
@@ -755,7 +760,7 @@ static int attn_bwd_tc64_launch(const void* qkv, const void* dO, const float* ls
   {
     cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)B * T};
     cuuint64_t strides[1] = {(cuuint64_t)d * 4};
-    cuuint32_t box[2] = {DH, 64};
+    cuuint32_t box[2] = {DH, 32};  // one 32-query box per warpgroup
     cuuint32_t es[2] = {1, 1};
     CUresult r = g_enc_bwd(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
