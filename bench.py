@@ -428,7 +428,7 @@ def cpu_baseline(c, budget_s=20.0, sample_tokens=None):
     """The reference's CPU path (oracle port: torch-CPU fp32 fwd/bwd + numpy f64
     optimizer, all host cores) on a bounded sample at the workload's exact shapes,
     extrapolated linearly to one local step:
-      fwd/bwd: a 1-layer and a 2-layer model at the exact width/vocab/context on
+      fwd/bwd: a 1-layer and a 3-layer model at the exact width/vocab/context on
       1 x `tokens` tokens -> per-layer and embedding/head cost -> L layers, per token;
       optimizer: micro-accumulate / clip / AdamW / l2 on a 4M-param slice, per param."""
     import torch
@@ -440,16 +440,19 @@ def cpu_baseline(c, budget_s=20.0, sample_tokens=None):
     rng = np.random.default_rng(0)
     batch = rng.integers(33, 97, size=(1, tokens))
     times = {}
-    for nl in (1, 2):
+    for nl in (1, 3):  # one timed call each, after an untimed warm-up call
         n = V * d + nl * (12 * d * d + 4 * d) + 2 * d + d * V
         w = np.asarray(rng.normal(0, 0.02, n), dtype=np.float32)
-        if nl == 1:
-            model_ref.loss_and_grad(w, batch[:, :8], V, T, nl, d, H)  # warm-up: allocator + cached ALiBi buffer
+        model_ref.loss_and_grad(w, batch[:, :8], V, T, nl, d, H)  # warm-up: allocator + cached ALiBi buffer
         t0 = time.perf_counter()
         model_ref.loss_and_grad(w, batch, V, T, nl, d, H)
         times[nl] = time.perf_counter() - t0
         del w
-    per_layer = max(times[2] - times[1], 1e-9)
+    # per-layer cost from the 1- vs 3-layer difference; floored by the layer's FLOP share of the
+    # 1-layer time so timing noise cannot make the extrapolation optimistic
+    fl_layer = 24.0 * d * d + 4.0 * tokens * d
+    fl_rest = 4.0 * V * d
+    per_layer = max((times[3] - times[1]) / 2, times[1] * fl_layer / (fl_layer + fl_rest))
     base = max(times[1] - per_layer, 0.0)
     t_fb = base + L * per_layer
     n_s = 4_000_000
@@ -472,8 +475,8 @@ def cpu_baseline(c, budget_s=20.0, sample_tokens=None):
     tokens_step = c["B"] * c["micro"] * T
     step_s = t_fb / tokens * tokens_step + (c["micro"] * t_acc + t_opt) / n_s * N
     return {"value": round(tokens_step / step_s, 3), "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": f"oracle loss_and_grad on 1x{tokens} tokens with 1 and 2 layers at the exact d={d}/V={V}/"
-                      f"ctx={T} shape ({times[1]:.1f}s, {times[2]:.1f}s -> {L} layers) + accumulate/clip/AdamW on a "
+            "sample": f"oracle loss_and_grad on 1x{tokens} tokens with 1 and 3 layers at the exact d={d}/V={V}/"
+                      f"ctx={T} shape ({times[1]:.1f}s, {times[3]:.1f}s -> {L} layers) + accumulate/clip/AdamW on a "
                       f"{n_s // 10**6}M-param slice ({t_acc + t_opt:.2f}s), extrapolated to one local step "
                       f"({tokens_step} tokens, {N} params)"}
 
