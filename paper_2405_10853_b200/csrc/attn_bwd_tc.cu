@@ -640,26 +640,45 @@ __global__ void __launch_bounds__(320, 1)
       if (t >= 2) mbar_wait(&pds_free[s], ((t >> 1) & 1) ^ 1);
       const uint32_t prow = sP0 + s * Cf::PT + r * 128;
       uint32_t dsp[32];  // dS^T packed bf16x2, written once dV has consumed P^T
+      // the causal mask only touches the diagonal tile: the other tiles run a mask-free copy
+      auto elementwise = [&](auto diag_t) {
+        constexpr bool kDiag = decltype(diag_t)::value;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < 2; ++c) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          float p[8], ds[8];
+          for (int q = 0; q < 4; ++q) {
+            float p[8], ds[8];
+            const int qb = 64 * g + 32 * c + q * 8;
+            const float4 e0 = *reinterpret_cast<const float4*>(sE + qb), e1 = *reinterpret_cast<const float4*>(sE + qb + 4);
+            const float4 d0 = *reinterpret_cast<const float4*>(sD + qb), d1 = *reinterpret_cast<const float4*>(sD + qb + 4);
+            const float ev[8] = {e0.x, e0.y, e0.z, e0.w, e1.x, e1.y, e1.z, e1.w};
+            const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int ql = 64 * g + 32 * c + q * 8 + i;
-            const float x = fmaf(__uint_as_float(sv[c][q * 8 + i]), scale_log2, slk - sE[ql]);
-            p[i] = (diag && q0 + ql < kj) ? 0.f : ex2b(x);
-            ds[i] = p[i] * (__uint_as_float(pv[c][q * 8 + i]) - sD[ql]);
+            for (int i = 0; i < 8; i += 2) {  // packed f32x2, per-lane identical to the scalar form
+              const int ql = qb + i;
+              const float2 be = pk_sub(make_float2(slk, slk), make_float2(ev[i], ev[i + 1]));
+              const float2 x = pk_fma(make_float2(__uint_as_float(sv[c][q * 8 + i]), __uint_as_float(sv[c][q * 8 + i + 1])),
+                                      make_float2(scale_log2, scale_log2), be);
+              p[i] = (kDiag && q0 + ql < kj) ? 0.f : ex2b(x.x);
+              p[i + 1] = (kDiag && q0 + ql + 1 < kj) ? 0.f : ex2b(x.y);
+              const float2 d2 = pk_mul(make_float2(p[i], p[i + 1]),
+                                       pk_sub(make_float2(__uint_as_float(pv[c][q * 8 + i]),
+                                                          __uint_as_float(pv[c][q * 8 + i + 1])),
+                                              make_float2(dv[i], dv[i + 1])));
+              ds[i] = d2.x;
+              ds[i + 1] = d2.y;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dsp[c * 16 + q * 4 + i] = pack_bf16(ds[2 * i], ds[2 * i + 1]);
+            const int kc = 8 * g + 4 * c + q;  // 8-query chunk 0..15
+            const uint32_t sw = (kc >> 3) * (128 * 128) + (((kc & 7) ^ (r & 7)) << 4);
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(pack_bf16(p[0], p[1])),
+                         "r"(pack_bf16(p[2], p[3])), "r"(pack_bf16(p[4], p[5])), "r"(pack_bf16(p[6], p[7])));
           }
-#pragma unroll
-          for (int i = 0; i < 4; ++i) dsp[c * 16 + q * 4 + i] = pack_bf16(ds[2 * i], ds[2 * i + 1]);
-          const int kc = 8 * g + 4 * c + q;  // 8-query chunk 0..15
-          const uint32_t sw = (kc >> 3) * (128 * 128) + (((kc & 7) ^ (r & 7)) << 4);
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(pack_bf16(p[0], p[1])),
-                       "r"(pack_bf16(p[2], p[3])), "r"(pack_bf16(p[4], p[5])), "r"(pack_bf16(p[6], p[7])));
         }
-      }
+      };
+      if (diag) elementwise(std::true_type{});
+      else elementwise(std::false_type{});
       tc_fence_before();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
