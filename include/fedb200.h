@@ -24,6 +24,7 @@ enum fb_status { FB_OK = 0, FB_BAD_ARG = 1, FB_CUDA_ERROR = 2, FB_NONFINITE = 3,
 
 #define FB_ABI_VERSION 1
 #define FB_MAX_CLIENTS 64
+#define FB_MAX_REPLICAS 8  /* w' destinations besides w_out (peer GPUs), fb_fedagg_step_f32_peers */
 #define FB_RED_BLOCKS 1184 /* fixed reduction grid: 148 SMs x 8, deterministic partials */
 
 const char* fb_last_error(void);
@@ -46,6 +47,14 @@ int fb_fedagg_step_f32(const float* const* d_client_w, const int64_t* n_k, int n
                        int deterministic, const float* d_w, const float* d_m, float* d_w_out,
                        float* d_m_out, int64_t n, double eta, double mu, int nesterov,
                        double* d_stats, int64_t* d_first_bad, double* d_pg_out, void* stream);
+/* Multi-GPU variant (one rank's shard): client pointers may be NVLink peer addresses and
+ * w' is also stored to n_replicas peer copies of the global model, so the round-end
+ * all-to-all, fused step and all-gather are one kernel. Bit-identical to the above. */
+int fb_fedagg_step_f32_peers(const float* const* d_client_w, const int64_t* n_k, int n_clients,
+                             int deterministic, const float* d_w, const float* d_m, float* d_w_out,
+                             float* d_m_out, float* const* d_w_replicas, int n_replicas, int64_t n,
+                             double eta, double mu, int nesterov, double* d_stats, int64_t* d_first_bad,
+                             void* stream);
 /* Same fused step plus the round telemetry of compute_round_norms (fedforge/metrics.py:177-215)
  * as side reductions of the same HBM pass: d_stats[6 + K] = |pg|^2, |w'|^2, |m'|^2, |w|^2,
  * |sum p_k w_k|^2, |w - sum p_k w_k|^2, then |w_k|^2 per client (p_k = n_k / sum n). */

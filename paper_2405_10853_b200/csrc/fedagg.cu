@@ -27,6 +27,8 @@ struct AggParams {
   const TIn* src[FB_MAX_CLIENTS];
   double nk[FB_MAX_CLIENTS];
   double pk[FB_MAX_CLIENTS];  // n_k / sum n (f64), for the round-norm telemetry
+  float* wrep[FB_MAX_REPLICAS];  // extra destinations of w' (peer GPUs' replicas over NVLink)
+  int nrep;
 };
 
 // stats layout (f64): 0 |pg|^2, 1 |w'|^2, 2 |m'|^2, 3 |w|^2, 4 |sum p_k w_k|^2, 5 |w - sum p_k w_k|^2,
@@ -249,12 +251,18 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
     if constexpr (VEC == 4) {
       st_stream_f4(w_out + j0, make_float4(wo[0], wo[1], wo[2], wo[3]));
       st_stream_f4(m_out + j0, make_float4(mo[0], mo[1], mo[2], mo[3]));
+      for (int i = 0; i < P.nrep; ++i) st_stream_f4(P.wrep[i] + j0, make_float4(wo[0], wo[1], wo[2], wo[3]));
     } else if constexpr (VEC == 2) {
       *reinterpret_cast<float2*>(w_out + j0) = make_float2(wo[0], wo[1]);
       *reinterpret_cast<float2*>(m_out + j0) = make_float2(mo[0], mo[1]);
+      for (int i = 0; i < P.nrep; ++i) *reinterpret_cast<float2*>(P.wrep[i] + j0) = make_float2(wo[0], wo[1]);
     } else {
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) { w_out[j0 + e] = wo[e]; m_out[j0 + e] = mo[e]; }
+      for (int e = 0; e < VEC; ++e) {
+        w_out[j0 + e] = wo[e];
+        m_out[j0 + e] = mo[e];
+        for (int i = 0; i < P.nrep; ++i) P.wrep[i][j0 + e] = wo[e];
+      }
     }
   }
   // scalar tail (only when VEC > 1 and n % VEC != 0)
@@ -290,6 +298,7 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
       StepOut o = outer_step(w[j], m[j], pgv, eta, mu, nesterov);
       w_out[j] = o.w;
       m_out[j] = o.m;
+      for (int i = 0; i < P.nrep; ++i) P.wrep[i][j] = o.w;
       s_w += (double)o.w * (double)o.w;
       s_m += (double)o.m * (double)o.m;
       if (!(isfinite(o.w) && isfinite(o.m)) && (unsigned long long)j < bad) bad = (unsigned long long)j;
@@ -324,18 +333,27 @@ template <typename TIn>
 static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int deterministic,
                          const float* w, const float* m, float* w_out, float* m_out, int64_t n,
                          double eta, double mu, int nesterov, double* stats, int64_t* first_bad,
-                         double* pg_out, int stats_mode, cudaStream_t st) {
+                         double* pg_out, int stats_mode, cudaStream_t st, float* const* w_rep = nullptr,
+                         int n_rep = 0) {
   FB_REQUIRE(K >= 1 && K <= FB_MAX_CLIENTS, "n_clients=%d outside [1, %d]", K, FB_MAX_CLIENTS);
   FB_REQUIRE(n > 0, "model length must be positive, got %lld", (long long)n);
   FB_REQUIRE(eta > 0.0, "server eta must be > 0, got %g", eta);
   FB_REQUIRE(mu >= 0.0 && mu < 1.0, "server mu must be in [0, 1), got %g", mu);
   AggParams<TIn> P;
+  FB_REQUIRE(n_rep >= 0 && n_rep <= FB_MAX_REPLICAS, "n_replicas=%d outside [0, %d]", n_rep, FB_MAX_REPLICAS);
+  FB_REQUIRE(n_rep == 0 || w_out, "w' replicas need w_out");
+  P.nrep = n_rep;
+  for (int i = 0; i < n_rep; ++i) {
+    FB_REQUIRE(w_rep[i] != nullptr, "replica %d: null pointer", i);
+    P.wrep[i] = w_rep[i];
+  }
   double total = 0.0;
   int64_t itotal = 0;
   FB_REQUIRE((w_out == nullptr) == (m_out == nullptr), "w_out and m_out must both be set or both NULL");
   FB_REQUIRE(w_out || pg_out || stats, "nothing to compute");
   bool aligned = ((uintptr_t)w % 16 == 0) && ((uintptr_t)m % 16 == 0) && ((uintptr_t)w_out % 16 == 0) &&
                  ((uintptr_t)m_out % 16 == 0) && ((uintptr_t)pg_out % 8 == 0);
+  for (int i = 0; i < n_rep; ++i) aligned = aligned && ((uintptr_t)w_rep[i] % 16 == 0);
   for (int k = 0; k < K; ++k) {
     FB_REQUIRE(n_k[k] >= 1, "client %d: n_k must be >= 1, got %lld", k, (long long)n_k[k]);
     FB_REQUIRE(src[k] != nullptr, "client %d: null pointer", k);
@@ -391,6 +409,22 @@ extern "C" int fb_fedagg_step_f32(const float* const* d_client_w, const int64_t*
                                   void* stream) {
   return fb::launch_fedagg<float>(d_client_w, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n,
                                   eta, mu, nesterov, d_stats, d_first_bad, d_pg_out, 1, (cudaStream_t)stream);
+}
+
+// Multi-GPU fused round end over NVLink peer memory (dist.PeerAggregator): the client
+// pointers may be peer-GPU addresses (symmetric memory), so the kernel pulls every
+// client's slice of this rank's shard straight over NVLink, and w' is stored both to
+// w_out and to every replica (the other ranks' copies of the global model) - the
+// all-to-all, the reduction and the all-gather in one pass. Same arithmetic and client
+// order as fb_fedagg_step_f32, so the result is bit-identical to one GPU.
+extern "C" int fb_fedagg_step_f32_peers(const float* const* d_client_w, const int64_t* n_k, int n_clients,
+                                        int deterministic, const float* d_w, const float* d_m, float* d_w_out,
+                                        float* d_m_out, float* const* d_w_replicas, int n_replicas, int64_t n,
+                                        double eta, double mu, int nesterov, double* d_stats,
+                                        int64_t* d_first_bad, void* stream) {
+  return fb::launch_fedagg<float>(d_client_w, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n, eta, mu,
+                                  nesterov, d_stats, d_first_bad, nullptr, 1, (cudaStream_t)stream, d_w_replicas,
+                                  n_replicas);
 }
 
 extern "C" int fb_fedagg_round_norms_f32(const float* const* d_client_w, const int64_t* n_k, int n_clients,

@@ -111,3 +111,67 @@ def fused_kernel(srcs, nks, deterministic, w_slice, m_slice, w_out, m_out, eta, 
     ext.call("fb_fedagg_step_f32", ptrs, nk, len(srcs), int(deterministic), w_slice.data_ptr(), m_slice.data_ptr(),
              w_out.data_ptr(), m_out.data_ptr(), w_slice.numel(), float(eta), float(mu), int(nesterov),
              agg.stats.data_ptr(), agg.bad.data_ptr(), None, ext.stream_handle())
+
+
+class PeerAggregator:
+    """The round-end exchange as ONE kernel over NVLink peer memory (G > 1).
+
+    Every rank keeps its clients' end weights in a symmetric-memory buffer (torch
+    symmetric memory: the same allocation mapped into every peer GPU) and the global model
+    replica in another. For its shard [lo, hi) a rank runs fb_fedagg_step_f32_peers with
+    client k's pointer set to the owning rank's buffer (a peer address for remote clients),
+    so the kernel pulls the remote slices straight over NVLink, reduces all K in id order,
+    and stores w' to its own replica and to every peer's replica. That single pass replaces
+    the NCCL all-to-all, the shard-local kernel and the NCCL all-gather of
+    ShardedAggregator, with the same arithmetic in the same order: bit-identical to one GPU.
+    Two device-side barriers bracket it (all clients final before the reads; all replicas
+    written before w' is used). Momentum stays sharded. NVLink bytes per rank:
+    in 4 (N/G) (K - K/G), out 4 (N/G) (G - 1)."""
+
+    def __init__(self, n: int, n_clients: int, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n = n
+        self.K = n_clients
+        self.lo, self.hi, self.per = shard_bounds(n, self.world, self.rank)
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.slots = (n_clients + self.world - 1) // self.world
+        width = self.per * self.world
+        self.clients = symm.empty(self.slots, width, dtype=torch.float32, device=dev)
+        self.wbuf = symm.empty(width, dtype=torch.float32, device=dev)
+        grp = group if group is not None else dist.group.WORLD
+        self.hc = symm.rendezvous(self.clients, grp)
+        self.hw = symm.rendezvous(self.wbuf, grp)
+        self.cptr = [int(p) for p in self.hc.buffer_ptrs]
+        self.wptr = [int(p) for p in self.hw.buffer_ptrs]
+        self.stats = torch.empty(3, dtype=torch.float64, device=dev)
+        self.bad = torch.empty(1, dtype=torch.int64, device=dev)
+        self.width = width
+
+    def client_buffer(self, k: int):
+        """The [N] f32 slot where this rank keeps client k's end weights (k % world == rank)."""
+        assert k % self.world == self.rank, (k, self.rank)
+        return self.clients[k // self.world, : self.n]
+
+    def step(self, w, m_shard, n_k: dict, eta, mu, nesterov, deterministic=True, w_out=None):
+        import torch
+        cnt = self.hi - self.lo
+        ids = sorted(n_k) if deterministic else list(n_k)
+        srcs = [self.cptr[k % self.world] + 4 * ((k // self.world) * self.width + self.lo) for k in ids]
+        reps = [self.wptr[r] + 4 * self.lo for r in range(self.world) if r != self.rank]
+        m_new = torch.empty_like(m_shard)
+        wo = self.wbuf[self.lo:self.hi]
+        self.hc.barrier(channel=0)  # every rank's clients are final
+        if cnt > 0:
+            ext.call("fb_fedagg_step_f32_peers", (C.c_void_p * len(ids))(*srcs),
+                     (C.c_int64 * len(ids))(*[int(n_k[k]) for k in ids]), len(ids), int(deterministic),
+                     w[self.lo:self.hi].data_ptr(), m_shard.data_ptr(), wo.data_ptr(), m_new.data_ptr(),
+                     (C.c_void_p * max(1, len(reps)))(*reps), len(reps), cnt, float(eta), float(mu), int(nesterov),
+                     self.stats.data_ptr(), self.bad.data_ptr(), ext.stream_handle())
+        self.hc.barrier(channel=1)  # every shard of w' has landed in every replica
+        out = w_out if w_out is not None else torch.empty_like(w)
+        out.copy_(self.wbuf[: self.n])
+        return out, m_new

@@ -1,7 +1,8 @@
 """torchrun --nproc-per-node G tools/multi_gpu_check.py
-Round-end exchange over NCCL (all-to-all of client slices + shard-local fused kernel +
-all-gather) must be bit-identical to the single-GPU fused aggregation. Also reports the
-exchange time (max over ranks) for N params, K clients."""
+Round-end exchange, both multi-GPU forms, must be bit-identical to the single-GPU fused
+aggregation: (a) NCCL all-to-all of client slices + shard-local fused kernel + all-gather,
+(b) the single fused kernel over NVLink peer memory (PeerAggregator). Also reports each
+form's time (max over ranks) for N params, K clients."""
 import ctypes as C
 import json
 import os
@@ -12,7 +13,7 @@ import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_10853_b200 import ext  # noqa: E402
-from paper_2405_10853_b200.dist import ShardedAggregator, clients_of  # noqa: E402
+from paper_2405_10853_b200.dist import PeerAggregator, ShardedAggregator, clients_of  # noqa: E402
 
 N = int(os.environ.get("CHK_N", "70542336"))
 K = int(os.environ.get("CHK_K", "8"))
@@ -49,6 +50,22 @@ e1.record()
 torch.cuda.synchronize()
 ms = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+# (b) fused over NVLink peer memory
+peer = PeerAggregator(N, K)
+for k, t in mine.items():
+    peer.client_buffer(k).copy_(t)
+m_sh = m[peer.lo:peer.hi].contiguous()
+for _ in range(2):
+    w_peer, m_peer = peer.step(w, m_sh, nk, 0.7, 0.9, True)
+torch.cuda.synchronize()
+dist.barrier()
+e0.record()
+for _ in range(reps):
+    w_peer, m_peer = peer.step(w, m_sh, nk, 0.7, 0.9, True)
+e1.record()
+torch.cuda.synchronize()
+ms_peer = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
+dist.all_reduce(ms_peer, op=dist.ReduceOp.MAX)
 # single-GPU reference on every rank (all clients regenerated locally)
 allc = [client(k) for k in range(K)]
 ptrs = (C.c_void_p * K)(*[t.data_ptr() for t in allc])
@@ -59,12 +76,17 @@ ext.call("fb_fedagg_step_f32", ptrs, nks, K, 1, w.data_ptr(), m.data_ptr(), wr.d
 torch.cuda.synchronize()
 ok_w = torch.equal(w_new.view(torch.int32), wr.view(torch.int32))
 ok_m = torch.equal(m_shard.view(torch.int32), mr[agg.lo:agg.hi].view(torch.int32))
-flags = torch.tensor([int(ok_w), int(ok_m)], device="cuda")
+ok_pw = torch.equal(w_peer.view(torch.int32), wr.view(torch.int32))
+ok_pm = torch.equal(m_peer.view(torch.int32), mr[peer.lo:peer.hi].view(torch.int32))
+flags = torch.tensor([int(ok_w), int(ok_m), int(ok_pw), int(ok_pm)], device="cuda")
 dist.all_reduce(flags, op=dist.ReduceOp.MIN)
 per_rank_bytes = 4 * N * len(mine) * (world - 1) / world + 4 * N * (world - 1) / world
 if rank == 0:
     print(json.dumps({"world": world, "N": N, "K": K, "bit_identical_w": bool(flags[0]), "bit_identical_m": bool(flags[1]),
-                      "exchange_ms": round(float(ms), 3),
+                      "peer_bit_identical_w": bool(flags[2]), "peer_bit_identical_m": bool(flags[3]),
+                      "exchange_ms": round(float(ms), 3), "peer_fused_ms": round(float(ms_peer), 3),
+                      "peer_nvlink_in_bytes_per_rank": int(4 * (N // world) * (K - len(mine))),
+                      "peer_nvlink_in_gbs_per_rank": round(4 * (N // world) * (K - len(mine)) / (float(ms_peer) / 1e3) / 1e9, 1),
                       "nvlink_bytes_per_rank_per_dir": int(per_rank_bytes),
                       "nvlink_gbs_per_rank": round(per_rank_bytes / (float(ms) / 1e3) / 1e9, 1)}), flush=True)
 dist.destroy_process_group()
