@@ -151,6 +151,13 @@ class PeerAggregator:
         self.bad = torch.empty(1, dtype=torch.int64, device=dev)
         self.width = width
 
+    def exchange(self, local: dict):
+        """Stage this rank's clients into their symmetric slots (a local copy; no transfer)."""
+        for k, t in local.items():
+            buf = self.client_buffer(k)
+            if buf.data_ptr() != t.data_ptr():
+                buf.copy_(t[: self.n], non_blocking=True)
+
     def client_buffer(self, k: int):
         """The [N] f32 slot where this rank keeps client k's end weights (k % world == rank)."""
         assert k % self.world == self.rank, (k, self.rank)

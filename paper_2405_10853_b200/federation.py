@@ -4,8 +4,10 @@
 Clients are sharded over ranks (client k on rank k mod G, one process per GPU);
 every client on a rank trains with train_round (end weights stay in HBM), then the
 round ends with the fused aggregation + outer step (+ round-norm telemetry): on one
-GPU directly, on G GPUs through the NCCL all-to-all of client slices
-(dist.ShardedAggregator), bit-identical for every G. Optional validation pass
+GPU directly; on G GPUs as one fused kernel over NVLink peer memory
+(dist.PeerAggregator), or, where peers cannot be mapped, the NCCL all-to-all of client
+slices + shard-local kernel + all-gather (dist.ShardedAggregator). Bit-identical for
+every G. Optional validation pass
 (evaluate_mean_ce) and FEDP checkpoint of (global, momentum) on rank 0.
 """
 from __future__ import annotations
@@ -19,7 +21,7 @@ from . import ext
 from .checkpoint import write_checkpoint
 from .config import AdamWConfig, ScheduleConfig, TinyLMConfig, TrainTask
 from .data import BatchIterator, DataSplit, TokenizedCorpus
-from .dist import ShardedAggregator, clients_of
+from .dist import PeerAggregator, ShardedAggregator, clients_of
 from .fedopt import AggregatorState, DeviceVector, ServerOptState, server_step_with_norms
 from .model import LossEvaluator, init_params_host
 from .telemetry import RoundNorms, norms_from_stats
@@ -58,7 +60,14 @@ class Federation:
         self.ev = LossEvaluator(model_cfg)
         self.iters = {k: BatchIterator(corpus, split.shards[k], batch_size, data_seed) for k in self.mine}
         self.n_k = {k: split.shards[k].n_k for k in range(self.K)}
-        self.agg = ShardedAggregator(self.ev.n_params, self.K) if self.world > 1 else None
+        self.agg = None
+        if self.world > 1:  # fused peer-memory round end where NVLink peers map; NCCL exchange otherwise
+            try:
+                if dist.get_backend() != "nccl":
+                    raise RuntimeError("peer memory needs the NCCL (GPU) process group")
+                self.agg = PeerAggregator(self.ev.n_params, self.K)
+            except Exception:
+                self.agg = ShardedAggregator(self.ev.n_params, self.K)
 
     def init_state(self):
         import torch
