@@ -63,6 +63,15 @@ __device__ __forceinline__ float2 pk_mul(float2 a, float2 b) {
       : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
   return *reinterpret_cast<float2*>(&r);
 }
+// D[tmem] (+)= A[tmem] * B[smem]: A (M x 16) from TMEM, lane = row, 8 columns of bf16 pairs
+__device__ __forceinline__ void umma_ts_b(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 __device__ __forceinline__ void red_add_v4(float* p, float a, float b, float c, float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
 }
@@ -98,18 +107,21 @@ __device__ __forceinline__ void build_live_list(const uint8_t* __restrict__ live
 //   dQ^T = K^T dS^T (M = dh = 128, N = 64 queries, K = 128 keys) has its own TMEM columns;
 //   it is drained by the compute warps of the NEXT tile through a dedicated smem staging
 //   box and ONE TMA bulk reduce-add per tile (dq rows [q0, q0+64) x 128 cols).
-//   TMEM: S^T [0,64)  dP^T [64,128)  dQ^T [128,192)  dV [256,384)  dK [384,512).
+//   P^T (bf16 pairs) goes to TMEM and dV = P^T dO is an A-from-TMEM MMA; the 32 KB of
+//   smem that P^T no longer needs buy a third Q / dO stage, so the loads of tile t+2 are
+//   not gated by the dV / dK MMAs of tile t.
+//   TMEM: S^T [0,64)  dP^T [64,128)  dQ^T [128,192)  P^T[2] [192,256)  dV [256,384)  dK [384,512).
 struct AttnBwd64Cfg {
   static constexpr int DH = 128;
+  static constexpr int NQ = 3;                   // Q / dO ring depth
   static constexpr int KT = 128 * DH * 2;        // K or V tile (128 keys)
   static constexpr int QT = 64 * DH * 2;         // Q or dO tile (64 queries)
-  static constexpr int PT = 128 * 64 * 2;        // P^T or dS^T tile (128 keys x 64 q)
+  static constexpr int PT = 128 * 64 * 2;        // dS^T tile (128 keys x 64 q)
   static constexpr int K_OFF = 0;
   static constexpr int V_OFF = K_OFF + KT;
-  static constexpr int Q_OFF = V_OFF + KT;       // [2]
-  static constexpr int O_OFF = Q_OFF + 2 * QT;   // [2]
-  static constexpr int P_OFF = O_OFF + 2 * QT;   // [2]
-  static constexpr int S_OFF = P_OFF + 2 * PT;   // [2]
+  static constexpr int Q_OFF = V_OFF + KT;       // [NQ]
+  static constexpr int O_OFF = Q_OFF + NQ * QT;  // [NQ]
+  static constexpr int S_OFF = O_OFF + NQ * QT;  // [2]
   static constexpr int X_OFF = S_OFF + 2 * PT;   // dQ staging: 64 rows x 128 f32
   static constexpr int L_OFF = X_OFF + 64 * DH * 4;  // e[2][64], D[2][64]
   static constexpr int BAR_OFF = L_OFF + 4 * 64 * 4;
@@ -129,16 +141,16 @@ __global__ void __launch_bounds__(320, 1)
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + Cf::BAR_OFF);
   uint64_t* kv_full = bar + 0;
-  uint64_t* q_full = bar + 1;     // [2]
-  uint64_t* o_full = bar + 3;     // [2]
-  uint64_t* q_empty = bar + 5;    // [2]
-  uint64_t* o_empty = bar + 7;    // [2]
-  uint64_t* s_full = bar + 9;
-  uint64_t* pds_full = bar + 10;
-  uint64_t* pds_free = bar + 11;  // [2]
-  uint64_t* dq_full = bar + 13;
-  uint64_t* dq_empty = bar + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint64_t* q_full = bar + 1;     // [NQ]
+  uint64_t* o_full = bar + 4;     // [NQ]
+  uint64_t* q_empty = bar + 7;    // [NQ]
+  uint64_t* o_empty = bar + 10;   // [NQ]
+  uint64_t* s_full = bar + 13;
+  uint64_t* pds_full = bar + 14;
+  uint64_t* pds_free = bar + 15;  // [2]
+  uint64_t* dq_full = bar + 17;
+  uint64_t* dq_empty = bar + 18;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
   uint32_t* nlive_p = tmem_slot + 1;
   uint8_t* tl = reinterpret_cast<uint8_t*>(tmem_slot + 2);
   float* sE0 = reinterpret_cast<float*>(smem + Cf::L_OFF);  // e[2][64] (double-buffered)
@@ -158,13 +170,13 @@ __global__ void __launch_bounds__(320, 1)
     tma_prefetch(&tm_do);
     tma_prefetch(&tm_dq);
     mbar_init(kv_full, 1);
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < Cf::NQ; ++s) {
       mbar_init(&q_full[s], 1);
       mbar_init(&o_full[s], 1);
       mbar_init(&q_empty[s], 1);
       mbar_init(&o_empty[s], 1);
-      mbar_init(&pds_free[s], 1);
     }
+    for (int s = 0; s < 2; ++s) mbar_init(&pds_free[s], 1);
     mbar_init(s_full, 1);
     mbar_init(pds_full, 8);
     mbar_init(dq_full, 1);
@@ -179,8 +191,7 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t tmem = *tmem_slot;
   const int nlive = (int)*nlive_p;
   const uint32_t sK = smem_u32(smem + Cf::K_OFF), sV = smem_u32(smem + Cf::V_OFF), sQ0 = smem_u32(smem + Cf::Q_OFF),
-                 sO0 = smem_u32(smem + Cf::O_OFF), sP0 = smem_u32(smem + Cf::P_OFF), sS0 = smem_u32(smem + Cf::S_OFF),
-                 sX = smem_u32(smem + Cf::X_OFF);
+                 sO0 = smem_u32(smem + Cf::O_OFF), sS0 = smem_u32(smem + Cf::S_OFF), sX = smem_u32(smem + Cf::X_OFF);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -189,8 +200,8 @@ __global__ void __launch_bounds__(320, 1)
       tma_load_3d(smem + Cf::K_OFF, &tm_kv, kv_full, 0, row0 + k0, zk);
       tma_load_3d(smem + Cf::V_OFF, &tm_kv, kv_full, 0, row0 + k0, zv);
       for (int t = 0; t < nlive; ++t) {
-        const int s = t & 1;
-        const uint32_t ph = (t >> 1) & 1;
+        const int s = t % Cf::NQ;
+        const uint32_t ph = (t / Cf::NQ) & 1;
         const int q0 = (first + tl[t]) * 64;
         mbar_wait(&q_empty[s], ph ^ 1);
         mbar_arrive_expect_tx(&q_full[s], Cf::QT);
@@ -205,10 +216,10 @@ __global__ void __launch_bounds__(320, 1)
       constexpr uint32_t idSP = idesc_bf16_f32(128, 64, 0, 0);  // S^T, dP^T: M=128 keys, N=64 q, K=dh
       constexpr uint32_t idKV = idesc_bf16_f32(128, DH, 0, 1);  // dV, dK: K-major A (P^T/dS^T), MN-major B
       constexpr uint32_t idQ = idesc_bf16_f32(128, 64, 1, 1);   // dQ^T = K^T dS^T: MN-major A and B
-      const uint32_t tS = tmem, tP = tmem + 64, tQ = tmem + 128, tV = tmem + 256, tK = tmem + 384;
+      const uint32_t tS = tmem, tP = tmem + 64, tQ = tmem + 128, tPT = tmem + 192, tV = tmem + 256, tK = tmem + 384;
       auto issue_sp = [&](int t) {
-        const int s = t & 1;
-        const uint32_t sph = (t >> 1) & 1;
+        const int s = t % Cf::NQ;
+        const uint32_t sph = (t / Cf::NQ) & 1;
         const uint32_t sQ = sQ0 + s * Cf::QT, sO = sO0 + s * Cf::QT;
         mbar_wait(&q_full[s], sph);
         mbar_wait(&o_full[s], sph);
@@ -225,19 +236,18 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(kv_full, 0);  // also when no tile is live: the K/V loads must land before exit
       if (nlive > 0) issue_sp(0);
       for (int t = 0; t < nlive; ++t) {
-        const int s = t & 1;
+        const int s = t % Cf::NQ, b2 = t & 1;
         const uint32_t ph = t & 1;
         const uint32_t sQ = sQ0 + s * Cf::QT, sO = sO0 + s * Cf::QT;
-        const uint32_t sP = sP0 + s * Cf::PT, sS = sS0 + s * Cf::PT;
+        const uint32_t sS = sS0 + b2 * Cf::PT;
         mbar_wait(pds_full, ph);  // S^T/dP^T(t) consumed; P^T(t), dS^T(t) in smem
         TRACE(16 * t + 0);
         if (t + 1 < nlive) issue_sp(t + 1);
         TRACE(16 * t + 1);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO   (K = 64 queries)
-          umma_f16(tV, smem_desc_sw128(sP + kk * 32, 16, 1024), smem_desc_sw128(sO + kk * 2048, 64 * 128, 1024), idKV,
-                   (t | kk) > 0);
+        for (int kk = 0; kk < 4; ++kk)  // dV += P^T dO   (K = 64 queries; P^T from TMEM)
+          umma_ts_b(tV, tPT + 32 * b2 + 8 * kk, smem_desc_sw128(sO + kk * 2048, 64 * 128, 1024), idKV, (t | kk) > 0);
         umma_commit(&o_empty[s]);
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)  // dK += dS^T Q
@@ -253,7 +263,7 @@ __global__ void __launch_bounds__(320, 1)
           umma_f16(tQ, smem_desc_sw128(sK + kk * 2048, 128 * 128, 1024), smem_desc_sw128(sS + kk * 2048, 8192, 1024),
                    idQ, kk > 0);
         umma_commit(dq_full);
-        umma_commit(&pds_free[s]);
+        umma_commit(&pds_free[b2]);
       }
     }
   } else {
@@ -330,7 +340,8 @@ __global__ void __launch_bounds__(320, 1)
       tmem_ld_wait();
       // P^T / dS^T buffers [s] were last read by the MMAs of tile t-2
       if (t >= 2) mbar_wait(&pds_free[s], ((t >> 1) & 1) ^ 1);
-      const uint32_t prow = sP0 + s * Cf::PT + r * 128, srow = sS0 + s * Cf::PT + r * 128;
+      const uint32_t srow = sS0 + s * Cf::PT + r * 128;
+      uint32_t ptm[16];  // this group's 32 queries of P^T as bf16 pairs -> TMEM (A of the dV MMA)
       // the causal mask only touches the two diagonal tiles: the other tiles run a mask-free copy
       auto elementwise = [&](auto diag_t) {
       constexpr bool kDiag = decltype(diag_t)::value;
@@ -359,14 +370,16 @@ __global__ void __launch_bounds__(320, 1)
         }
         const int kc = 4 * g + q;
         const uint32_t sw = ((kc ^ (r & 7)) << 4);
-        asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(pack_bf16(p[0], p[1])),
-                     "r"(pack_bf16(p[2], p[3])), "r"(pack_bf16(p[4], p[5])), "r"(pack_bf16(p[6], p[7])));
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ptm[4 * q + i] = pack_bf16(p[2 * i], p[2 * i + 1]);
         asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(srow + sw), "r"(pack_bf16(ds[0], ds[1])),
                      "r"(pack_bf16(ds[2], ds[3])), "r"(pack_bf16(ds[4], ds[5])), "r"(pack_bf16(ds[6], ds[7])));
       }
       };
       if (diag) elementwise(std::true_type{});
       else elementwise(std::false_type{});
+      tmem_st_32x32b_x16(tmem + 192 + 32 * s + 16 * g + lane_off, ptm);
+      tmem_st_wait();
       tc_fence_before();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
