@@ -140,9 +140,19 @@ class PeerAggregator:
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.slots = (n_clients + self.world - 1) // self.world
         width = self.per * self.world
-        self.clients = symm.empty(self.slots, width, dtype=torch.float32, device=dev)
-        self.wbuf = symm.empty(width, dtype=torch.float32, device=dev)
         grp = group if group is not None else dist.group.WORLD
+        # allocate on every rank first and agree before the (collective) rendezvous, so a rank
+        # that cannot map symmetric memory makes ALL ranks fall back instead of leaving the
+        # others waiting in the rendezvous
+        ok = torch.ones(1, dtype=torch.int32, device=dev)
+        try:
+            self.clients = symm.empty(self.slots, width, dtype=torch.float32, device=dev)
+            self.wbuf = symm.empty(width, dtype=torch.float32, device=dev)
+        except Exception:
+            ok.zero_()
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN, group=group)
+        if int(ok.item()) == 0:
+            raise RuntimeError("symmetric memory unavailable on at least one rank")
         self.hc = symm.rendezvous(self.clients, grp)
         self.hw = symm.rendezvous(self.wbuf, grp)
         self.cptr = [int(p) for p in self.hc.buffer_ptrs]
