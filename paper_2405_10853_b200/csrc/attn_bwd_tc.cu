@@ -182,6 +182,16 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 8);
     fence_barrier_init();
+#ifndef FB_EXP_LATE_KV
+    // K / V of this key block are needed whatever is live: start them before the TMEM
+    // allocation, the live-list build and the CTA barrier
+    {
+      const int zk = (d + h * DH) / 64, zv = (2 * d + h * DH) / 64;
+      mbar_arrive_expect_tx(kv_full, 2 * Cf::KT);
+      tma_load_3d(smem + Cf::K_OFF, &tm_kv, kv_full, 0, row0 + k0, zk);
+      tma_load_3d(smem + Cf::V_OFF, &tm_kv, kv_full, 0, row0 + k0, zv);
+    }
+#endif
   }
   if (warp == 2) build_live_list(live, bh, T, kb, first, ntiles, 1, tl, nlive_p);
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -195,10 +205,13 @@ __global__ void __launch_bounds__(320, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const int zq = (h * DH) / 64, zk = (d + h * DH) / 64, zv = (2 * d + h * DH) / 64, zo = (h * DH) / 64;
+      const int zq = (h * DH) / 64, zo = (h * DH) / 64;
+#ifdef FB_EXP_LATE_KV
+      const int zk = (d + h * DH) / 64, zv = (2 * d + h * DH) / 64;
       mbar_arrive_expect_tx(kv_full, 2 * Cf::KT);
       tma_load_3d(smem + Cf::K_OFF, &tm_kv, kv_full, 0, row0 + k0, zk);
       tma_load_3d(smem + Cf::V_OFF, &tm_kv, kv_full, 0, row0 + k0, zv);
+#endif
       for (int t = 0; t < nlive; ++t) {
         const int s = t % Cf::NQ;
         const uint32_t ph = (t / Cf::NQ) & 1;
@@ -391,7 +404,12 @@ __global__ void __launch_bounds__(320, 1)
       if (warp == 2 && lane == 0) TRACE(16 * t + 7);
     }
     if (nlive > 0) drain(nlive - 1);
+#ifdef FB_EXP_FULL_WAIT
     if ((tid & 127) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+#else
+    // exit only needs the staging box read (the reduce-adds complete with the grid)
+    if ((tid & 127) == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
     // dK, dV (the last dK/dV MMAs completed before the last dq_full)
     const int64_t ld = 3 * (int64_t)d;
     __nv_bfloat16* dkrow = dqkv + ((int64_t)row0 + kj) * ld + d + h * DH + (DH / 2) * g;
