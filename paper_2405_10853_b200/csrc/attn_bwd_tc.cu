@@ -2,12 +2,14 @@
 //
 // Reference: gradient of fedforge/model.py:92-98 (scores/sqrt(dh) + ALiBi bias, softmax,
 // PV); the bias is constant, so dq = dS k / sqrt(dh), dk = dS^T q / sqrt(dh),
-// dv = P^T dO, dS = P o (dP - D), D = rowsum(dO o O) (precomputed in attn.cu).
+// dv = P^T dO, dS = P o (dP - D), D = rowsum(dO o O) (from the out-projection dgrad
+// epilogue, or the pre-pass in attn.cu).
 //
 // CTA = 128 keys of one (b, h); loop over the causal query tiles. Two kernels:
-//   dh = 128  attn_bwd_tc64_kernel: 64-query tiles, dQ^T = K^T dS^T in its own TMEM
-//             columns, one TMA bulk reduce-add of dQ per tile, software pipeline across
-//             query tiles (elementwise of tile t+1 overlaps the MMAs of tile t).
+//   dh = 128  attn_bwd_tc64_kernel: 64-query tiles, P^T in TMEM (dV as an A-from-TMEM
+//             MMA), 3-stage Q/dO ring, dQ^T = K^T dS^T in its own TMEM columns, one TMA
+//             bulk reduce-add per warpgroup per tile, software pipeline across query
+//             tiles (elementwise of tile t+1 overlaps the MMAs of tile t).
 //   dh = 64   attn_bwd_tcd64_kernel: 128-query tiles, dQ = dS K with dS^T read as an
 //             MN-major A operand, P/dS share a double-buffered smem tile.
 // Warp roles in both: warp 0 TMA producer, warp 1 TMEM owner + single-thread MMA issuer,

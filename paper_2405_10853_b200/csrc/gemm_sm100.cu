@@ -11,9 +11,15 @@
 //               tile is a single TMA), completion via mbarrier expect_tx
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (128xBNx16 UMMAs),
 //               tcgen05.commit frees smem slots / publishes finished accumulators
-//   warps 2-5   epilogue: tcgen05.ld 32x32b.x32 -> registers -> fused op -> global
+//   warps 2-9   epilogue (two warps per TMEM lane quadrant, one column half each):
+//               tcgen05.ld 32x32b.x32 -> registers -> fused op (packed f32x2 math) ->
+//               swizzled smem staging -> TMA bulk tensor store
 //   TMEM        2 x BN fp32 columns: the accumulator is double-buffered so the
 //               epilogue of tile i overlaps the main loop of tile i+1
+// The 2-SM variant (gemm_bf16_tc2_kernel, cta_group::2, 256 x 256 tiles) is used whenever
+// its tiles fill the 74 CTA pairs; ragged last waves are split along K (last-wave split).
+// D = rowsum(dO o O) of the attention backward can ride on the out-projection dgrad
+// epilogue (FB_EPI_BF16_ROWDOT).
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
