@@ -101,6 +101,7 @@ constexpr int kProducerWarp = 8, kMmaWarp = 9;
 template <int DH>
 __global__ void __launch_bounds__(320, 1)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tm,
+                       const __grid_constant__ CUtensorMap tmo,
                        __nv_bfloat16* __restrict__ out, float* __restrict__ lse2, uint8_t* __restrict__ live_map,
                        int T, int H, float scale_log2, int use_alibi) {
   using Cf = AttnTcCfg<DH>;
@@ -350,7 +351,9 @@ __global__ void __launch_bounds__(320, 1)
       mbar_wait(&o_done[g], 0);
       tc_fence_after();
       const float il = 1.0f / l;
-      __nv_bfloat16* orow = out + ((int64_t)row0 + qi) * d + h * DH;
+      // O staged in this group's Q tile (free once every PV_g, hence every S_g, completed) in
+      // the 128B-swizzled [chunk][row][64] layout it was loaded in, then one TMA bulk store
+      uint8_t* stg = smem + Cf::Q_OFF + g * Cf::QT;
 #pragma unroll
       for (int c = 0; c < DH / 32; ++c) {
         uint32_t o[32];
@@ -359,12 +362,20 @@ __global__ void __launch_bounds__(320, 1)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const float* f = reinterpret_cast<const float*>(o) + 8 * q;
-          uint4 pk = make_uint4(pack_bf16(f[0] * il, f[1] * il), pack_bf16(f[2] * il, f[3] * il),
-                                pack_bf16(f[4] * il, f[5] * il), pack_bf16(f[6] * il, f[7] * il));
-          *reinterpret_cast<uint4*>(orow + c * 32 + 8 * q) = pk;
+          const int jj = (c & 1) * 4 + q;
+          *reinterpret_cast<uint4*>(stg + (c >> 1) * (128 * 128) + r * 128 + ((jj ^ (r & 7)) << 4)) =
+              make_uint4(pack_bf16(f[0] * il, f[1] * il), pack_bf16(f[2] * il, f[3] * il),
+                         pack_bf16(f[4] * il, f[5] * il), pack_bf16(f[6] * il, f[7] * il));
         }
       }
       lse2[(int64_t)bh * T + qi] = m + log2f(l);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
+      if (quad == 0 && lane == 0) {
+        tma_store_3d(&tmo, stg, 0, row0 + q0 + 128 * g, (h * DH) / 64);
+        bulk_commit();
+        bulk_wait_read<0>();
+      }
     }
   }
   tc_fence_before();
@@ -406,10 +417,23 @@ int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, uint8_t* live, int 
       return FB_CUDA_ERROR;
     }
   }
+  CUtensorMap tmo;  // O store boxes: 128 rows x DH (DH / 64 chunks of 64 columns), 128B swizzle
+  {
+    cuuint64_t odims[3] = {64, (cuuint64_t)B * T, (cuuint64_t)(d / 64)};
+    cuuint64_t ostrides[2] = {(cuuint64_t)d * 2, 128};
+    cuuint32_t obox[3] = {64, 128, DH / 64};
+    CUresult r = g_enc_attn(&tmo, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, o, odims, ostrides, obox, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("attn output tensor map encode failed: %d", (int)r);
+      return FB_CUDA_ERROR;
+    }
+  }
   auto k = attn_fwd_tc_kernel<DH>;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)DH);
-  k<<<dim3((T + 255) / 256, B * H), 320, Cf::SMEM, st>>>(tmq, tm, (__nv_bfloat16*)o, lse, live, T, H, scale_log2,
+  k<<<dim3((T + 255) / 256, B * H), 320, Cf::SMEM, st>>>(tmq, tm, tmo, (__nv_bfloat16*)o, lse, live, T, H, scale_log2,
                                                           use_alibi);
   FB_LAUNCH_CHECK();
   return FB_OK;
