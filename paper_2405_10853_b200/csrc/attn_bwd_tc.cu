@@ -483,7 +483,7 @@ struct AttnBwdD64Cfg {
 
 __global__ void __launch_bounds__(320, 1)
     attn_bwd_tcd64_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                          const __grid_constant__ CUtensorMap tm_dq, const float* __restrict__ lse2,
+                          const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv, const float* __restrict__ lse2,
                           const uint8_t* __restrict__ live, const float* __restrict__ Dd,
                           __nv_bfloat16* __restrict__ dqkv, int T, int H,
                           float scale_log2, float scale, int use_alibi) {
@@ -745,10 +745,10 @@ __global__ void __launch_bounds__(320, 1)
       if (t > 0) drain(t - 1);
     }
     if (nlive > 0) drain(nlive - 1);
-    if (quad == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    const int64_t ld = 3 * (int64_t)d;
-    __nv_bfloat16* dkrow = dqkv + ((int64_t)row0 + kj) * ld + d + h * DH + 32 * g;
-    __nv_bfloat16* dvrow = dkrow + d;
+    if (quad == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    // dK / dV staged in the idle Q / dO buffers (128B-swizzled [key][64]), two TMA bulk stores
+    uint8_t* stK = smem + Cf::Q_OFF;
+    uint8_t* stV = smem + Cf::O_OFF;
     uint32_t kv[32], vv[32];
     tmem_ld_32x32b_x32(tmem + 384 + lane_off + 32 * g, kv);
     tmem_ld_32x32b_x32(tmem + 320 + lane_off + 32 * g, vv);
@@ -761,11 +761,21 @@ __global__ void __launch_bounds__(320, 1)
     for (int q = 0; q < 4; ++q) {
       const float* fk = reinterpret_cast<const float*>(kv) + 8 * q;
       const float* fv = reinterpret_cast<const float*>(vv) + 8 * q;
-      *reinterpret_cast<uint4*>(dkrow + 8 * q) =
+      const int jj = 4 * g + q;
+      const uint32_t off = r * 128 + ((jj ^ (r & 7)) << 4);
+      *reinterpret_cast<uint4*>(stK + off) =
           make_uint4(pack_bf16(fk[0] * scale, fk[1] * scale), pack_bf16(fk[2] * scale, fk[3] * scale),
                      pack_bf16(fk[4] * scale, fk[5] * scale), pack_bf16(fk[6] * scale, fk[7] * scale));
-      *reinterpret_cast<uint4*>(dvrow + 8 * q) = make_uint4(pack_bf16(fv[0], fv[1]), pack_bf16(fv[2], fv[3]),
-                                                            pack_bf16(fv[4], fv[5]), pack_bf16(fv[6], fv[7]));
+      *reinterpret_cast<uint4*>(stV + off) = make_uint4(pack_bf16(fv[0], fv[1]), pack_bf16(fv[2], fv[3]),
+                                                        pack_bf16(fv[4], fv[5]), pack_bf16(fv[6], fv[7]));
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (tid == 0) {
+      tma_store_3d(&tm_dkv, stK, 0, row0 + k0, (d + h * DH) / 64);
+      tma_store_3d(&tm_dkv, stV, 0, row0 + k0, (2 * d + h * DH) / 64);
+      bulk_commit();
+      bulk_wait_read<0>();
     }
   }
   tc_fence_before();
@@ -870,10 +880,13 @@ static int attn_bwd_tcd64_launch(const void* qkv, const void* dO, const float* l
       return FB_CUDA_ERROR;
     }
   }
+  CUtensorMap tdkv;  // dK / dV store boxes: 128 keys x 64 dh, 128B swizzle
+  rc = encode_box(&tdkv, dqkv, (int64_t)B * T, 3 * d, 128, 1);
+  if (rc) return rc;
   auto k = attn_bwd_tcd64_kernel;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale = 1.0f / sqrtf((float)DH);
-  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tq, to, tdq, lse, live, Dbuf, (__nv_bfloat16*)dqkv, T, H,
+  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tq, to, tdq, tdkv, lse, live, Dbuf, (__nv_bfloat16*)dqkv, T, H,
                                                  1.4426950408889634f * scale, scale, use_alibi);
   FB_LAUNCH_CHECK();
   return FB_OK;
