@@ -50,22 +50,29 @@ e1.record()
 torch.cuda.synchronize()
 ms = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-# (b) fused over NVLink peer memory
-peer = PeerAggregator(N, K)
-for k, t in mine.items():
-    peer.client_buffer(k).copy_(t)
-m_sh = m[peer.lo:peer.hi].contiguous()
-for _ in range(2):
-    w_peer, m_peer = peer.step(w, m_sh, nk, 0.7, 0.9, True)
-torch.cuda.synchronize()
-dist.barrier()
-e0.record()
-for _ in range(reps):
-    w_peer, m_peer = peer.step(w, m_sh, nk, 0.7, 0.9, True)
-e1.record()
-torch.cuda.synchronize()
-ms_peer = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
-dist.all_reduce(ms_peer, op=dist.ReduceOp.MAX)
+# (b) fused over NVLink peer memory: copy-engine staged pull (default) and direct SM pull
+res_peer = {}
+for mode in ("ce", "sm"):
+    peer = PeerAggregator(N, K, pull=mode, chunk=int(os.environ.get("CHK_CHUNK", str(1 << 25))))
+    for k, t in mine.items():
+        peer.client_buffer(k).copy_(t)
+    m_sh = m[peer.lo:peer.hi].contiguous()
+    for _ in range(2):
+        w_peer, m_peer = peer.step(w, m_sh, nk, 0.7, 0.9, True)
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    for _ in range(reps):
+        w_peer, m_peer = peer.step(w, m_sh, nk, 0.7, 0.9, True)
+    e1.record()
+    torch.cuda.synchronize()
+    t_ms = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
+    dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    res_peer[mode] = (float(t_ms), w_peer.clone(), m_peer.clone(), peer.stats.clone())
+    del peer
+    torch.cuda.empty_cache()
+ms_peer, w_peer, m_peer, _ = res_peer["ce"]
+ms_peer_sm, w_peer_sm, m_peer_sm, _ = res_peer["sm"]
 # single-GPU reference on every rank (all clients regenerated locally)
 allc = [client(k) for k in range(K)]
 ptrs = (C.c_void_p * K)(*[t.data_ptr() for t in allc])
@@ -77,16 +84,21 @@ torch.cuda.synchronize()
 ok_w = torch.equal(w_new.view(torch.int32), wr.view(torch.int32))
 ok_m = torch.equal(m_shard.view(torch.int32), mr[agg.lo:agg.hi].view(torch.int32))
 ok_pw = torch.equal(w_peer.view(torch.int32), wr.view(torch.int32))
-ok_pm = torch.equal(m_peer.view(torch.int32), mr[peer.lo:peer.hi].view(torch.int32))
-flags = torch.tensor([int(ok_w), int(ok_m), int(ok_pw), int(ok_pm)], device="cuda")
+ok_pm = torch.equal(m_peer.view(torch.int32), mr[agg.lo:agg.hi].view(torch.int32))
+ok_sm = torch.equal(w_peer_sm.view(torch.int32), wr.view(torch.int32)) and torch.equal(
+    m_peer_sm.view(torch.int32), mr[agg.lo:agg.hi].view(torch.int32))
+ok_st = torch.allclose(res_peer["ce"][3][:3], res_peer["sm"][3][:3], rtol=1e-12, atol=0)
+flags = torch.tensor([int(ok_w), int(ok_m), int(ok_pw), int(ok_pm), int(ok_sm), int(ok_st)], device="cuda")
 dist.all_reduce(flags, op=dist.ReduceOp.MIN)
 per_rank_bytes = 4 * N * len(mine) * (world - 1) / world + 4 * N * (world - 1) / world
 if rank == 0:
     print(json.dumps({"world": world, "N": N, "K": K, "bit_identical_w": bool(flags[0]), "bit_identical_m": bool(flags[1]),
                       "peer_bit_identical_w": bool(flags[2]), "peer_bit_identical_m": bool(flags[3]),
-                      "exchange_ms": round(float(ms), 3), "peer_fused_ms": round(float(ms_peer), 3),
+                      "peer_sm_bit_identical": bool(flags[4]), "peer_stats_ce_vs_sm_close": bool(flags[5]),
+                      "peer_sm_ms": round(ms_peer_sm, 3),
+                      "exchange_ms": round(float(ms), 3), "peer_fused_ms": round(ms_peer, 3),
                       "peer_nvlink_in_bytes_per_rank": int(4 * (N // world) * (K - len(mine))),
-                      "peer_nvlink_in_gbs_per_rank": round(4 * (N // world) * (K - len(mine)) / (float(ms_peer) / 1e3) / 1e9, 1),
+                      "peer_nvlink_in_gbs_per_rank": round(4 * (N // world) * (K - len(mine)) / (ms_peer / 1e3) / 1e9, 1),
                       "nvlink_bytes_per_rank_per_dir": int(per_rank_bytes),
                       "nvlink_gbs_per_rank": round(per_rank_bytes / (float(ms) / 1e3) / 1e9, 1)}), flush=True)
 dist.destroy_process_group()
