@@ -129,18 +129,18 @@ class PeerAggregator:
     written before w' is used). Momentum stays sharded. NVLink bytes per rank:
     in 4 (N/G) (K - K/G), out 4 (N/G) (G - 1).
 
-    pull="ce" (default): the remote slices are pulled by the copy engines into a
-    double-buffered local stage, chunk by chunk, overlapped with the kernel on the previous
-    chunk (SM loads of peer memory mixed into the reduction reach ~430 GB/s; the copy
-    engines 740 GB/s, tools/nvlink_pull.py). pull="sm": the kernel loads peer memory
-    directly (one launch, no stage)."""
+    pull="ce": the remote slices are pulled by the copy engines (one stream per peer) into
+    a double-buffered local stage, chunk by chunk, overlapped with the kernel on the
+    previous chunk (one peer alone: copy engines 740 GB/s, SM loads 670 GB/s per rank,
+    tools/nvlink_pull.py). pull="sm": the kernel loads peer memory directly (one launch,
+    no stage). pull="auto" (default) picks "ce" at G = 2 and "sm" above, as measured."""
 
-    def __init__(self, n: int, n_clients: int, group=None, device=None, pull: str = "ce", chunk: int = 1 << 25):
+    def __init__(self, n: int, n_clients: int, group=None, device=None, pull: str = "auto", chunk: int = 1 << 25):
         import torch
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm
-        if pull not in ("ce", "sm"):
-            raise ValueError(f"pull must be 'ce' or 'sm', got {pull!r}")
+        if pull not in ("auto", "ce", "sm"):
+            raise ValueError(f"pull must be 'auto', 'ce' or 'sm', got {pull!r}")
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.n = n
@@ -172,10 +172,14 @@ class PeerAggregator:
         self.width = width
         # peer views of every rank's client slots (for the copy-engine pull)
         self.peer_clients = [self.hc.get_buffer(r, (self.slots, width), torch.float32) for r in range(self.world)]
-        self.pull = pull
+        # measured at C4 (tools/multi_gpu_check.py): the staged copy-engine pull wins at G = 2
+        # (21.75 vs 24.6 ms), the direct SM pull at G = 4 (21.4 vs 28.5 ms: with every rank
+        # pulling from 3 peers the copy engines fall behind the SMs' loads)
+        self.pull = pull if pull != "auto" else ("ce" if self.world == 2 else "sm")
         self.chunk = int(chunk)
         self.stage = None
-        self.side = torch.cuda.Stream(device=dev)
+        # one copy stream per peer: pulls from different GPUs run on different copy engines
+        self.side = {r: torch.cuda.Stream(device=dev) for r in range(self.world) if r != self.rank}
 
     def exchange(self, local: dict):
         """Stage this rank's clients into their symmetric slots (a local copy; no transfer)."""
@@ -226,24 +230,29 @@ class PeerAggregator:
         ch = min(cnt, self.chunk)
         nch = (cnt + ch - 1) // ch
         if self.stage is None or self.stage.shape[1:] != (len(remote), ch):
-            self.stage = torch.empty(2, len(remote), ch, dtype=torch.float32, device=self.side.device)
-        stats = torch.empty(nch, 6, dtype=torch.float64, device=self.side.device)
-        bad = torch.empty(nch, dtype=torch.int64, device=self.side.device)
+            self.stage = torch.empty(2, len(remote), ch, dtype=torch.float32, device=m_shard.device)
+        stats = torch.empty(nch, 6, dtype=torch.float64, device=m_shard.device)
+        bad = torch.empty(nch, dtype=torch.int64, device=m_shard.device)
         main = torch.cuda.current_stream()
-        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        peers = sorted({k % self.world for k in remote})
+        ready = [{r: torch.cuda.Event() for r in peers} for _ in range(2)]
         done = [torch.cuda.Event(), torch.cuda.Event()]
-        self.side.wait_stream(main)  # after the barrier: the peers' clients are final
+        for r in peers:
+            self.side[r].wait_stream(main)  # after the barrier: the peers' clients are final
         slot = {k: i for i, k in enumerate(remote)}
         for c in range(nch):
             a, b, s = c * ch, min(cnt, (c + 1) * ch), c & 1
-            with torch.cuda.stream(self.side):
-                if c >= 2:
-                    self.side.wait_event(done[s])  # kernel c-2 has consumed this buffer
-                for k in remote:
-                    src = self.peer_clients[k % self.world][k // self.world, self.lo + a:self.lo + b]
-                    self.stage[s, slot[k], : b - a].copy_(src, non_blocking=True)
-                ready[s].record(self.side)
-            main.wait_event(ready[s])
+            for r in peers:
+                st = self.side[r]
+                with torch.cuda.stream(st):
+                    if c >= 2:
+                        st.wait_event(done[s])  # kernel c-2 has consumed this buffer
+                    for k in remote:
+                        if k % self.world == r:
+                            src = self.peer_clients[r][k // self.world, self.lo + a:self.lo + b]
+                            self.stage[s, slot[k], : b - a].copy_(src, non_blocking=True)
+                    ready[s][r].record(st)
+                main.wait_event(ready[s][r])
             srcs = [int(self.stage[s, slot[k]].data_ptr()) if k in slot
                     else self.cptr[self.rank] + 4 * ((k // self.world) * self.width + self.lo + a) for k in ids]
             self._launch(srcs, ids, n_k, deterministic, w, m_shard, m_new, reps, a, b, eta, mu, nesterov,

@@ -51,7 +51,7 @@ torch.cuda.synchronize()
 ms = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
 # (b) fused over NVLink peer memory: copy-engine staged pull (default) and direct SM pull
-res_peer = {}
+res_peer = {}  # both forms explicitly (the product default "auto" picks one per world size)
 for mode in ("ce", "sm"):
     peer = PeerAggregator(N, K, pull=mode, chunk=int(os.environ.get("CHK_CHUNK", str(1 << 25))))
     for k, t in mine.items():
