@@ -135,7 +135,8 @@ class PeerAggregator:
     tools/nvlink_pull.py). pull="sm": the kernel loads peer memory directly (one launch,
     no stage). pull="auto" (default) picks "ce" at G = 2 and "sm" above, as measured."""
 
-    def __init__(self, n: int, n_clients: int, group=None, device=None, pull: str = "auto", chunk: int = 1 << 25):
+    def __init__(self, n: int, n_clients: int, group=None, device=None, pull: str = "auto", chunk: int = 1 << 25,
+                 ce_clients: int | None = None):
         import torch
         import torch.distributed as dist
         import torch.distributed._symmetric_memory as symm
@@ -177,6 +178,8 @@ class PeerAggregator:
         # pulling from 3 peers the copy engines fall behind the SMs' loads)
         self.pull = pull if pull != "auto" else ("ce" if self.world == 2 else "sm")
         self.chunk = int(chunk)
+        self.ce_clients = ce_clients  # pull="ce": how many remote clients the copy engines stage (None = all;
+        # the rest are loaded by the kernel's SMs straight from peer memory, both in flight at once)
         self.stage = None
         # one copy stream per peer: pulls from different GPUs run on different copy engines
         self.side = {r: torch.cuda.Stream(device=dev) for r in range(self.world) if r != self.rank}
@@ -227,6 +230,8 @@ class PeerAggregator:
         client order: bit-identical to the direct pull and to one GPU."""
         import torch
         remote = [k for k in ids if k % self.world != self.rank]
+        if self.ce_clients is not None:
+            remote = remote[: self.ce_clients]
         ch = min(cnt, self.chunk)
         nch = (cnt + ch - 1) // ch
         if self.stage is None or self.stage.shape[1:] != (len(remote), ch):
@@ -254,7 +259,7 @@ class PeerAggregator:
                     ready[s][r].record(st)
                 main.wait_event(ready[s][r])
             srcs = [int(self.stage[s, slot[k]].data_ptr()) if k in slot
-                    else self.cptr[self.rank] + 4 * ((k // self.world) * self.width + self.lo + a) for k in ids]
+                    else self.cptr[k % self.world] + 4 * ((k // self.world) * self.width + self.lo + a) for k in ids]
             self._launch(srcs, ids, n_k, deterministic, w, m_shard, m_new, reps, a, b, eta, mu, nesterov,
                          stats[c], bad[c:c + 1])
             done[s].record(main)

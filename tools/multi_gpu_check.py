@@ -53,7 +53,8 @@ dist.all_reduce(ms, op=dist.ReduceOp.MAX)
 # (b) fused over NVLink peer memory: copy-engine staged pull (default) and direct SM pull
 res_peer = {}  # both forms explicitly (the product default "auto" picks one per world size)
 for mode in ("ce", "sm"):
-    peer = PeerAggregator(N, K, pull=mode, chunk=int(os.environ.get("CHK_CHUNK", str(1 << 25))))
+    peer = PeerAggregator(N, K, pull=mode, chunk=int(os.environ.get("CHK_CHUNK", str(1 << 25))),
+                          ce_clients=int(os.environ["CHK_CE"]) if "CHK_CE" in os.environ else None)
     for k, t in mine.items():
         peer.client_buffer(k).copy_(t)
     m_sh = m[peer.lo:peer.hi].contiguous()
