@@ -49,7 +49,9 @@ int fb_fedagg_step_f32(const float* const* d_client_w, const int64_t* n_k, int n
                        double* d_stats, int64_t* d_first_bad, double* d_pg_out, void* stream);
 /* Multi-GPU variant (one rank's shard): client pointers may be NVLink peer addresses and
  * w' is also stored to n_replicas peer copies of the global model, so the round-end
- * all-to-all, fused step and all-gather are one kernel. Bit-identical to the above. */
+ * all-to-all, fused step and all-gather are one kernel. Bit-identical to the above.
+ * d_stats (optional) here holds 6 doubles: the 3 above, then this shard's |w|^2,
+ * |sum p_k w_k|^2, |w - sum p_k w_k|^2 (summed over ranks -> compute_round_norms). */
 int fb_fedagg_step_f32_peers(const float* const* d_client_w, const int64_t* n_k, int n_clients,
                              int deterministic, const float* d_w, const float* d_m, float* d_w_out,
                              float* d_m_out, float* const* d_w_replicas, int n_replicas, int64_t n,
@@ -62,6 +64,12 @@ int fb_fedagg_round_norms_f32(const float* const* d_client_w, const int64_t* n_k
                               int deterministic, const float* d_w, const float* d_m, float* d_w_out,
                               float* d_m_out, int64_t n, double eta, double mu, int nesterov,
                               double* d_stats, int64_t* d_first_bad, void* stream);
+/* Both: the peer-memory round end with the 6 + K round-norm stats of this rank's shard. */
+int fb_fedagg_round_norms_f32_peers(const float* const* d_client_w, const int64_t* n_k, int n_clients,
+                                    int deterministic, const float* d_w, const float* d_m, float* d_w_out,
+                                    float* d_m_out, float* const* d_w_replicas, int n_replicas, int64_t n,
+                                    double eta, double mu, int nesterov, double* d_stats,
+                                    int64_t* d_first_bad, void* stream);
 /* Same contract for reference-format f64 deltas (ClientUpdate.delta, fedopt.py:26-46). */
 int fb_fedagg_step_f64delta(const double* const* d_deltas, const int64_t* n_k, int n_clients,
                             int deterministic, const float* d_w, const float* d_m, float* d_w_out,
@@ -144,8 +152,18 @@ int fb_gemm_bf16_rowdot(int M, int N, int K, const void* d_A, int64_t lda, int a
 /* ---- transformer pieces (model.py:75-150, :222-229) --------------------------------- */
 int fb_embed_fwd(const int32_t* d_tok, const float* d_emb, const float* d_pos, float* d_x,
                  int n_tok, int T, int d, void* stream);
+/* gemb[tok[r]] += dx[r] (and gpos[r % T] += dx[r]) with f32 atomics: arrival-order sums,
+ * not bitwise reproducible run to run. The runtime uses fb_embed_bwd_sorted. */
 int fb_embed_bwd(const int32_t* d_tok, const float* d_dx, float* d_gemb, float* d_gpos,
                  int n_tok, int T, int d, int vocab, void* stream);
+/* Deterministic embedding backward (model.py:109 / :145 grads): token ids are
+ * stably radix-sorted with their positions, each run of equal ids is summed in ascending
+ * position order by one owner and added once; positions are summed in ascending batch
+ * row. Bitwise reproducible. d_work: fb_embed_bwd_work_bytes(n_tok, vocab) bytes. */
+int64_t fb_embed_bwd_work_bytes(int n_tok, int vocab);
+int fb_embed_bwd_sorted(const int32_t* d_tok, const float* d_dx, float* d_gemb, float* d_gpos,
+                        int n_tok, int T, int d, int vocab, void* d_work, int64_t work_bytes,
+                        void* stream);
 /* LayerNorm eps 1e-5 (model.py:81,84,113): y(bf16) = LN(x), saves mean/rstd */
 int fb_ln_fwd(const float* d_x, const float* d_gamma, const float* d_beta, void* d_y_bf16,
               float* d_mean, float* d_rstd, int rows, int d, void* stream);
@@ -160,7 +178,8 @@ int fb_ln_bwd(const float* d_x, const float* d_gamma, const float* d_mean, const
  * block of 128 queries x 64 keys live (1) or dead (0: every softmax weight underflowed to
  * exactly 0, which ALiBi causes far from the diagonal) and skips the dead blocks' PV; the
  * backward skips the MMAs of blocks the map says are dead. Results are bit-identical with
- * and without the map. T % 128 == 0, dh in {64, 128}. */
+ * and without the map. tcgen05 kernels for T % 128 == 0 and dh in {64, 128}; any other
+ * shape (dh <= 256, any T) runs fixed-order CUDA-core kernels (d_live unused). */
 int fb_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, uint8_t* d_live, int B, int T, int H,
                 int dh, int use_alibi, void* stream);
 int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
@@ -172,6 +191,11 @@ enum { FB_ATTN_D_READY = 1 };
 int fb_attn_bwd_ex(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
                    const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh,
                    int use_alibi, int flags, void* stream);
+/* 1: bitwise-reproducible training (reference test_trainer.py:56-63 replay contract): the
+ * attention backward uses the fixed-order CUDA-core kernels instead of the tcgen05 kernel,
+ * whose dQ partials are TMA reduce-added in arrival order. Every other kernel is
+ * deterministic in both modes. Process-wide; 0 (default) = fastest. */
+int fb_set_deterministic(int enable);
 /* Mean next-token CE over B*(T-1) positions (model.py:226-229): logits f32 [rows][V]
  * for a chunk of rows [row0, row0+rows) of a B x T batch; writes dlogits(bf16) =
  * scale*(softmax - onehot) (0 on each sequence's last position) and adds the summed
@@ -188,8 +212,8 @@ int fb_gather_batch(const uint16_t* d_corpus, const int64_t* d_order, int64_t n_
 /* ---- native runtime: whole TinyLM micro-batch and whole local step ----------------
  * TinyLMConfig (model.py:28-43). Flat parameter layout = the reference manifest
  * order (model.py:184-190): embed, [pos_embed], per block {ln1.w, ln1.b, qkv, attn_proj,
- * ln2.w, ln2.b, mlp_fc, mlp_proj}, ln_f.w, ln_f.b, head. GPU path constraints:
- * d_model % 64 == 0, head dim in {64, 128}, vocab % 64 == 0, T % 64 == 0. */
+ * ln2.w, ln2.b, mlp_fc, mlp_proj}, ln_f.w, ln_f.b, head. GPU path constraints (TMA row
+ * pitch): d_model % 8 == 0, vocab % 8 == 0, head dim <= 256; any T in [2, ctx]. */
 typedef struct {
   int32_t vocab, ctx, n_layers, d_model, n_heads, use_alibi;
 } fb_model_cfg;

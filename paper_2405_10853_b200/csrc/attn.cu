@@ -10,7 +10,11 @@
 // o is [B*T][d] bf16 (the attn_proj GEMM operand), lse2 [B][H][T] f32 in base-2 units.
 // The kernels themselves are tcgen05/TMEM/TMA (attn_tc.cu forward, attn_bwd_tc.cu
 // backward); this file holds the D = rowsum(dO o O) pre-pass, the dQ f32 -> bf16
-// finalisation and the C-ABI dispatch. GPU path: T % 128 == 0, dh in {64, 128}.
+// finalisation and the C-ABI dispatch. Tensor-core path: T % 128 == 0, dh in {64, 128};
+// every other shape (the reference's desk configs: dh 4..32, short or ragged T) runs the
+// CUDA-core kernels of attn_generic.cu. Deterministic mode (fb_set_deterministic) routes
+// the backward to the fixed-order generic kernels as well (the tensor-core backward adds
+// dQ partials with TMA reduce-add in arrival order).
 #include "common.cuh"
 
 namespace fb {
@@ -54,6 +58,14 @@ __global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16*
   }
 }
 
+int attn_fwd_generic(const void* qkv, void* o, float* lse, int B, int T, int H, int dh, int use_alibi,
+                     cudaStream_t st);
+int attn_bwd_generic(const void* qkv, const void* o, const void* dO, const float* lse, void* dqkv, float* work, int B,
+                     int T, int H, int dh, int use_alibi, int d_ready, cudaStream_t st);
+int g_deterministic = 0;
+
+static bool tc_shape(int T, int dh) { return (dh == 64 || dh == 128) && T % 128 == 0; }
+
 template <int DH>
 int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, uint8_t* live, int B, int T, int H, int use_alibi,
                        cudaStream_t st);
@@ -88,18 +100,16 @@ using namespace fb;
 
 extern "C" int fb_attn_fwd(const void* d_qkv, void* d_o, float* d_lse, uint8_t* d_live, int B, int T, int H, int dh,
                            int use_alibi, void* stream) {
-  FB_REQUIRE(B > 0 && H > 0 && T > 0 && T % 128 == 0, "attn_fwd: T must be a positive multiple of 128 (T=%d)", T);
+  FB_REQUIRE(B > 0 && H > 0 && T > 0 && dh > 0, "attn_fwd: bad shape B=%d T=%d H=%d dh=%d", B, T, H, dh);
   cudaStream_t st = (cudaStream_t)stream;
+  if (!tc_shape(T, dh)) return attn_fwd_generic(d_qkv, d_o, d_lse, B, T, H, dh, use_alibi, st);
   // algorithmic flops: causal lower triangle, QK^T and PV (2*T*d per layer-token fwd)
   const double fl = 2.0 * 2.0 * B * H * (double)T * (T + 1) / 2.0 * dh;
   const int pi = prof_on() ? prof_start(1, st) : -1;
-  int rc = FB_UNSUPPORTED;
-  if (dh == 64) rc = attn_fwd_tc_launch<64>(d_qkv, d_o, d_lse, d_live, B, T, H, use_alibi, st);
-  else if (dh == 128) rc = attn_fwd_tc_launch<128>(d_qkv, d_o, d_lse, d_live, B, T, H, use_alibi, st);
+  int rc = dh == 64 ? attn_fwd_tc_launch<64>(d_qkv, d_o, d_lse, d_live, B, T, H, use_alibi, st)
+                    : attn_fwd_tc_launch<128>(d_qkv, d_o, d_lse, d_live, B, T, H, use_alibi, st);
   prof_stop(1, pi, st, fl);
-  if (rc != FB_UNSUPPORTED) return rc;
-  set_error("attn_fwd: head dim %d unsupported (64 or 128)", dh);
-  return FB_UNSUPPORTED;
+  return rc;
 }
 
 extern "C" int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
@@ -111,17 +121,22 @@ extern "C" int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do,
 extern "C" int fb_attn_bwd_ex(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
                               const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh,
                               int use_alibi, int flags, void* stream) {
-  FB_REQUIRE(B > 0 && H > 0 && T > 0 && T % 128 == 0, "attn_bwd: T must be a positive multiple of 128 (T=%d)", T);
+  FB_REQUIRE(B > 0 && H > 0 && T > 0 && dh > 0, "attn_bwd: bad shape B=%d T=%d H=%d dh=%d", B, T, H, dh);
   FB_REQUIRE(d_work != nullptr, "attn_bwd: needs a work buffer of B*H*T + B*T*H*dh floats");
   cudaStream_t st = (cudaStream_t)stream;
+  if (!tc_shape(T, dh) || g_deterministic)
+    return attn_bwd_generic(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, H, dh, use_alibi, flags & FB_ATTN_D_READY,
+                            st);
   const double fl = 2.0 * 2.0 * 2.0 * B * H * (double)T * (T + 1) / 2.0 * dh;  // bwd = 2x fwd
   const int pi = prof_on() ? prof_start(2, st) : -1;
-  int rc = FB_UNSUPPORTED;
-  if (dh == 64) rc = attn_bwd_launch<64>(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, use_alibi, flags, st);
-  else if (dh == 128)
-    rc = attn_bwd_launch<128>(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, use_alibi, flags, st);
+  int rc = dh == 64
+               ? attn_bwd_launch<64>(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, use_alibi, flags, st)
+               : attn_bwd_launch<128>(d_qkv, d_o, d_do, d_lse, d_live, d_dqkv, d_work, B, T, H, use_alibi, flags, st);
   prof_stop(2, pi, st, fl);
-  if (rc != FB_UNSUPPORTED) return rc;
-  set_error("attn_bwd: head dim %d unsupported (64 or 128)", dh);
-  return FB_UNSUPPORTED;
+  return rc;
+}
+
+extern "C" int fb_set_deterministic(int enable) {
+  fb::g_deterministic = enable ? 1 : 0;
+  return FB_OK;
 }

@@ -110,7 +110,8 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
                                                      float* __restrict__ m_out, int64_t n,
                                                      double eta, double mu, int nesterov,
                                                      double* stats, unsigned long long* first_bad,
-                                                     double* __restrict__ pg_out, int client_norms) {
+                                                     double* __restrict__ pg_out, int client_norms,
+                                                     int n_fixed) {
   __shared__ double red[kStatsFixed + FB_MAX_CLIENTS][8];
   double s_pg = 0.0, s_w = 0.0, s_m = 0.0, s_w0 = 0.0, s_avg = 0.0, s_dif = 0.0;
   const int lane_ = threadIdx.x & 31, wid_ = threadIdx.x >> 5;
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
       for (int e = 0; e < VEC; ++e) { wv[e] = w[j0 + e]; mv[e] = m[j0 + e]; }
     }
     double pg[VEC];
-    if constexpr (VEC >= 2 && sizeof(TIn) == 4) {
+    if constexpr (sizeof(TIn) == 4) {
       // all client loads of a batch of KB clients are issued before any f64 math; the launch
       // picks KB x VEC so that >= 128-256 B per thread are in flight (measured, C5 sweep)
       TreeAcc<D> acc[VEC];
@@ -153,9 +154,11 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
             if constexpr (VEC == 4) {
               float4 t = ld_stream_f4(src);
               c[j][0] = t.x; c[j][1] = t.y; c[j][2] = t.z; c[j][3] = t.w;
-            } else {
+            } else if constexpr (VEC == 2) {
               float2 t = __ldg(reinterpret_cast<const float2*>(src));
               c[j][0] = t.x; c[j][1] = t.y;
+            } else {  // unaligned inputs: scalar loads, same math (stats included)
+              c[j][0] = __ldg(src);
             }
           }
         }
@@ -320,7 +323,8 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
       if (lane_ == 0) red[i][wid_] = v[i];
     }
     __syncthreads();
-    const int nstat = kStatsFixed + (client_norms ? K : 0);
+    // only the entries the caller sized d_stats for: n_fixed (3 or 6) + K client norms
+    const int nstat = client_norms ? kStatsFixed + K : n_fixed;
     for (int i = threadIdx.x; i < nstat; i += blockDim.x) {
       double t = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[i][w];
@@ -365,8 +369,11 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
   }
   total = (double)itotal;
   for (int k = 0; k < K; ++k) P.pk[k] = (double)n_k[k] / total;
+  // stats_mode: 1 = 3 doubles (|pg|^2, |w'|^2, |m'|^2); 4 = the 6 fixed round-norm entries;
+  // 2 (with 1) = 6 fixed + K per-client entries
   const int client_norms = (stats_mode & 2) ? 1 : 0;
-  if (stats) FB_CUDA_TRY(cudaMemsetAsync(stats, 0, (kStatsFixed + (client_norms ? K : 0)) * sizeof(double), st));
+  const int n_fixed = (stats_mode & 6) ? kStatsFixed : 3;
+  if (stats) FB_CUDA_TRY(cudaMemsetAsync(stats, 0, (n_fixed + (client_norms ? K : 0)) * sizeof(double), st));
   if (first_bad) FB_CUDA_TRY(cudaMemsetAsync(first_bad, 0x7f, sizeof(int64_t), st));
   const int threads = 256;
   const int depth = K <= 1 ? 1 : K <= 3 ? 2 : K <= 7 ? 3 : K <= 15 ? 4 : K <= 31 ? 5 : K <= 63 ? 6 : 7;
@@ -378,12 +385,12 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
       fedagg_kernel<TIn, VEC_, D_, 1, KB_><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, \
                                                                m_out, n, eta, mu, nesterov, stats,         \
                                                                (unsigned long long*)first_bad, pg_out,     \
-                                                               client_norms);                              \
+                                                               client_norms, n_fixed);                     \
     else                                                                                                 \
     fedagg_kernel<TIn, VEC_, D_, 0, KB_><<<blocks, threads, 0, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, \
                                                              m_out, n, eta, mu, nesterov, stats,         \
                                                              (unsigned long long*)first_bad, pg_out,     \
-                                                             client_norms);                              \
+                                                             client_norms, n_fixed);                     \
   } while (0)
   if (aligned && sizeof(TIn) == 4) {
     switch (depth) {
@@ -423,7 +430,20 @@ extern "C" int fb_fedagg_step_f32_peers(const float* const* d_client_w, const in
                                         double eta, double mu, int nesterov, double* d_stats,
                                         int64_t* d_first_bad, void* stream) {
   return fb::launch_fedagg<float>(d_client_w, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n, eta, mu,
-                                  nesterov, d_stats, d_first_bad, nullptr, 1, (cudaStream_t)stream, d_w_replicas,
+                                  nesterov, d_stats, d_first_bad, nullptr, 4, (cudaStream_t)stream, d_w_replicas,
+                                  n_replicas);
+}
+
+// Peer-memory round end plus the per-client round telemetry: d_stats[6 + K] as in
+// fb_fedagg_round_norms_f32, each entry this rank's shard's contribution (sum over ranks).
+extern "C" int fb_fedagg_round_norms_f32_peers(const float* const* d_client_w, const int64_t* n_k, int n_clients,
+                                               int deterministic, const float* d_w, const float* d_m, float* d_w_out,
+                                               float* d_m_out, float* const* d_w_replicas, int n_replicas, int64_t n,
+                                               double eta, double mu, int nesterov, double* d_stats,
+                                               int64_t* d_first_bad, void* stream) {
+  FB_REQUIRE(d_stats != nullptr, "fb_fedagg_round_norms_f32_peers needs d_stats (6 + K doubles)");
+  return fb::launch_fedagg<float>(d_client_w, n_k, n_clients, deterministic, d_w, d_m, d_w_out, d_m_out, n, eta, mu,
+                                  nesterov, d_stats, d_first_bad, nullptr, 3, (cudaStream_t)stream, d_w_replicas,
                                   n_replicas);
 }
 

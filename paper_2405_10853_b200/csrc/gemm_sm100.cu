@@ -74,6 +74,10 @@ struct EpiArgs {
   int units;             // work units of the launch
   int group_m;           // raster group height (2-SM kernel)
   int rd_T, rd_dh;       // FB_EPI_BF16_ROWDOT: sequence length, head dim
+  // MN-major operand whose MN extent is not a multiple of 64 (1-SM kernel only): its map is
+  // 2-D {mn, K} and each 64-wide MN chunk of a stage is its own TMA, so the chunks past mn
+  // are zero-filled by the TMA bounds check instead of reading the next K row
+  int a_2d, b_2d;
 };
 
 // work unit -> (tile, first k-block, k-block count, tail piece or -1), 2-SM kernel
@@ -351,10 +355,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           uint8_t* sb = sa + Cfg::A_BYTES;
           mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
           const int k0 = kb * BK;
-          if (A_MN) tma_load_3d(sa, &tmA, &full_bar[stage], 0, k0, m0 / 64);
-          else      tma_load_2d(sa, &tmA, &full_bar[stage], k0, m0);
-          if (B_MN) tma_load_3d(sb, &tmB, &full_bar[stage], 0, k0, n0 / 64);
-          else      tma_load_2d(sb, &tmB, &full_bar[stage], k0, n0);
+          if (A_MN && ep.a_2d) {
+            for (int c = 0; c < BM / 64; ++c) tma_load_2d(sa + c * (64 * BK * 2), &tmA, &full_bar[stage], m0 + 64 * c, k0);
+          } else if (A_MN) {
+            tma_load_3d(sa, &tmA, &full_bar[stage], 0, k0, m0 / 64);
+          } else {
+            tma_load_2d(sa, &tmA, &full_bar[stage], k0, m0);
+          }
+          if (B_MN && ep.b_2d) {
+            for (int c = 0; c < BN / 64; ++c) tma_load_2d(sb + c * (64 * BK * 2), &tmB, &full_bar[stage], n0 + 64 * c, k0);
+          } else if (B_MN) {
+            tma_load_3d(sb, &tmB, &full_bar[stage], 0, k0, n0 / 64);
+          } else {
+            tma_load_2d(sb, &tmB, &full_bar[stage], k0, n0);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
@@ -832,6 +846,22 @@ static int make_map_mnmajor(CUtensorMap* m, const void* ptr, int mn, int K, int6
   return FB_OK;
 }
 
+// Ragged MN-major operand [K][ld] (mn % 64 != 0): 2-D {mn, K}, box {64 mn, 64 k}, one TMA per chunk
+static int make_map_mnmajor_2d(CUtensorMap* m, const void* ptr, int mn, int K, int64_t ld) {
+  cuuint64_t dims[2] = {(cuuint64_t)mn, (cuuint64_t)K};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)BK};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled(MN-major 2-D mn=%d K=%d ld=%lld) failed: %d", mn, K, (long long)ld, (int)r);
+    return FB_CUDA_ERROR;
+  }
+  return FB_OK;
+}
+
 template <int BN, int A_MN, int B_MN, int EPI>
 static int launch_gemm_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiArgs& ep,
                          cudaStream_t st) {
@@ -956,8 +986,6 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
              "gemm: operands must be 16-byte aligned");
   FB_REQUIRE(lda % 8 == 0 && ldb % 8 == 0, "gemm: lda/ldb must be multiples of 8 elements");
   FB_REQUIRE(ldc % 8 == 0, "gemm: ldc must be a multiple of 8 elements");
-  FB_REQUIRE(a_major == 0 || M % 64 == 0, "gemm: MN-major A needs M %% 64 == 0 (M=%d)", M);
-  FB_REQUIRE(b_major == 0 || N % 64 == 0, "gemm: MN-major B needs N %% 64 == 0 (N=%d)", N);
   const bool need_aux = epilogue == FB_EPI_RESID_F32 || epilogue == FB_EPI_DGELU || epilogue == FB_EPI_RESID_F32_BF16;
   const bool need_aux_out = epilogue == FB_EPI_GELU || epilogue == FB_EPI_RESID_F32_BF16;
   FB_REQUIRE(!need_aux || d_aux, "gemm: epilogue %d needs aux", epilogue);
@@ -969,21 +997,24 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   // 2-SM 256x256 tiles when they fill the 74 CTA pairs; else 1-SM 128x256, else 128x128
   const int tiles2 = ((M + 255) / 256) * ((N + 255) / 256);
   const int ks = g_split_ws ? g_split_n : 1;
-  const bool use2 = g_gemm_2sm && M >= 256 && N >= 256 && tiles2 * ks >= kNumSMs / 2;
+  const bool a_2d = a_major && M % 64, b_2d = b_major && N % 64;
+  const bool use2 = g_gemm_2sm && M >= 256 && N >= 256 && tiles2 * ks >= kNumSMs / 2 && !a_2d && !b_2d;
   const int tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256) * ks;
   const int BN = (use2 || (N >= 256 && tiles256 >= kNumSMs)) ? 256 : 128;
   CUtensorMap ta, tb;
-  rc = a_major ? make_map_mnmajor(&ta, d_A, M, K, lda, BM) : make_map_kmajor(&ta, d_A, M, K, lda, BM);
+  rc = a_2d ? make_map_mnmajor_2d(&ta, d_A, M, K, lda)
+     : a_major ? make_map_mnmajor(&ta, d_A, M, K, lda, BM) : make_map_kmajor(&ta, d_A, M, K, lda, BM);
   if (rc) return rc;
   const int bbox = use2 ? 128 : BN;  // 2-SM: each CTA stages 128 of the 256 B rows
-  rc = b_major ? make_map_mnmajor(&tb, d_B, N, K, ldb, bbox) : make_map_kmajor(&tb, d_B, N, K, ldb, bbox);
+  rc = b_2d ? make_map_mnmajor_2d(&tb, d_B, N, K, ldb)
+     : b_major ? make_map_mnmajor(&tb, d_B, N, K, ldb, bbox) : make_map_kmajor(&tb, d_B, N, K, ldb, bbox);
   if (rc) return rc;
   if (epilogue == FB_EPI_BF16_ROWDOT && (!use2 || g_rd_T <= 0)) {
     set_error("gemm: the row-dot epilogue needs the 2-SM kernel (fb_gemm_bf16_rowdot)");
     return FB_UNSUPPORTED;
   }
   EpiArgs ep{d_C, ldc, d_aux, d_aux_out, ld_aux, 1, 0, 0, 1, nullptr, 0, raster_group_m(K, (N + 255) / 256),
-             g_rd_T, g_rd_dh};
+             g_rd_T, g_rd_dh, (int)a_2d, (int)b_2d};
   if (g_tail_ws && use2) {  // set by fb_gemm_bf16_splitk for this call only
     ep.full_tiles = g_tail_full;
     ep.tail_split = g_tail_split;
@@ -1149,7 +1180,8 @@ extern "C" int fb_gemm_bf16_splitk(int M, int N, int K, const void* d_A, int64_t
   const int num_kb = (K + BK - 1) / BK;
   if (ksplit <= 0) {
     // 2-SM raster with a full first wave: split only the ragged last wave (tile-local partials)
-    if (g_gemm_2sm && M >= 256 && N >= 256 && tiles2 >= kNumSMs / 2 && d_ws) {
+    const bool ragged = (a_major && M % 64) || (b_major && N % 64);  // 1-SM kernel only
+    if (g_gemm_2sm && M >= 256 && N >= 256 && tiles2 >= kNumSMs / 2 && d_ws && !ragged) {
       int F = 0;
       const int S = plan_tail_split(tiles2, num_kb, (int)(ws_bytes / (65536 * 4)), F);
       if (S > 1) {

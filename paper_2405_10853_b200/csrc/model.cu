@@ -75,6 +75,8 @@ struct WS {
   std::vector<Acts> L;
   float *x_out, *meanf, *rstdf, *logits, *dx, *dln, *attn_work, *ln_work, *splitk;
   __nv_bfloat16 *lnf, *dlogits, *dxb, *dao, *dqkv, *dfc;
+  uint8_t* emb_work;  // sorted-token embedding backward (fb_embed_bwd_sorted)
+  int64_t emb_work_bytes;
   int chunk;
 };
 
@@ -90,7 +92,7 @@ static WS carve(const fb_model_cfg& c, int B, int T, Arena& A) {
     a.qkv = A.take<__nv_bfloat16>(M * 3 * d);
     a.ao = A.take<__nv_bfloat16>(M * d);
     a.lse = A.take<float>(B * H * T);
-    a.live = A.take<uint8_t>((int64_t)B * H * (T / 128) * (T / 64));
+    a.live = A.take<uint8_t>((int64_t)B * H * ((T + 127) / 128) * ((T + 63) / 64));
     a.x_mid = A.take<float>(M * d);
     a.mean2 = A.take<float>(M);
     a.rstd2 = A.take<float>(M);
@@ -115,25 +117,29 @@ static WS carve(const fb_model_cfg& c, int B, int T, Arena& A) {
   w.attn_work = A.take<float>(B * H * T + M * d);
   w.ln_work = A.take<float>(2 * 592 * d);
   w.splitk = A.take<float>(kSplitKFloats);
+  w.emb_work_bytes = fb_embed_bwd_work_bytes((int)M, (int)V);
+  w.emb_work = A.take<uint8_t>(w.emb_work_bytes);
   return w;
 }
 
+// The GEMM operands are read by TMA, whose row pitch must be a multiple of 16 bytes: every
+// bf16 activation / weight row is d, 3d, 4d or V elements wide and every manifest offset is a
+// multiple of d, so d % 8 == 0 and V % 8 == 0 are the only shape constraints. Attention runs
+// on tcgen05 for dh in {64, 128} with T % 128 == 0 and on the CUDA-core kernels otherwise.
 static int check_cfg(const fb_model_cfg& c, int B, int T) {
   FB_REQUIRE(c.vocab > 0 && c.n_layers >= 0 && c.d_model > 0 && c.n_heads > 0, "bad model config");
   FB_REQUIRE(c.d_model % c.n_heads == 0, "d_model=%d not divisible by n_heads=%d", c.d_model, c.n_heads);
   const int dh = c.d_model / c.n_heads;
-  if (c.d_model % 64 || (dh != 64 && dh != 128) || c.vocab % 64) {
-    set_error("GPU path needs d_model %% 64 == 0, head dim in {64,128}, vocab %% 64 == 0 (got d=%d dh=%d V=%d)",
+  if (c.d_model % 8 || c.vocab % 8 || dh > 256) {
+    set_error("GPU path needs d_model %% 8 == 0, vocab %% 8 == 0 and head dim <= 256 (got d=%d dh=%d V=%d)",
               c.d_model, dh, c.vocab);
     return FB_UNSUPPORTED;
   }
   FB_REQUIRE(B > 0 && T >= 2 && T <= c.ctx, "sequence length %d outside [2, context_len=%d]", T, c.ctx);
-  if (T % 128) {
-    set_error("GPU path needs T %% 128 == 0 (T=%d)", T);
-    return FB_UNSUPPORTED;
-  }
   return FB_OK;
 }
+
+static bool attn_tc_shape(int T, int dh) { return (dh == 64 || dh == 128) && T % 128 == 0; }
 
 }  // namespace fb
 
@@ -231,7 +237,9 @@ extern "C" int fb_model_fwd_bwd(const fb_model_cfg* cfgp, const float* P, const 
     // attention: x_mid = x_in + proj(attn(ln1(x_in)))
     // dO = dY W_proj; its epilogue also forms the attention backward's D = rowsum(dO o O)
     int aflags = FB_ATTN_D_READY;
-    int rc = fb_gemm_bf16_rowdot(M, d, d, w.dxb, d, 0, S + b.proj, d, 1, w.dao, d, a.ao, d, w.attn_work, T, dh, st);
+    int rc = attn_tc_shape(T, dh)
+                 ? fb_gemm_bf16_rowdot(M, d, d, w.dxb, d, 0, S + b.proj, d, 1, w.dao, d, a.ao, d, w.attn_work, T, dh, st)
+                 : FB_UNSUPPORTED;
     if (rc == FB_UNSUPPORTED) {
       aflags = 0;
       rc = fb_gemm_bf16(M, d, d, w.dxb, d, 0, S + b.proj, d, 1, w.dao, d, FB_EPI_BF16, nullptr, nullptr, 0, st);
@@ -244,7 +252,8 @@ extern "C" int fb_model_fwd_bwd(const fb_model_cfg* cfgp, const float* P, const 
     TRY(fb_ln_bwd(a.x_in, P + b.ln1_w, a.mean1, a.rstd1, w.dln, w.dx, w.dx, w.dxb, G + b.ln1_w, G + b.ln1_b,
                   w.ln_work, M, d, st));
   }
-  TRY(fb_embed_bwd(tok, w.dx, G + Lo.embed, Lo.pos >= 0 ? G + Lo.pos : nullptr, M, T, d, V, st));
+  TRY(fb_embed_bwd_sorted(tok, w.dx, G + Lo.embed, Lo.pos >= 0 ? G + Lo.pos : nullptr, M, T, d, V, w.emb_work,
+                          w.emb_work_bytes, st));
   return FB_OK;
 }
 

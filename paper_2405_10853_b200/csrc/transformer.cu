@@ -14,6 +14,8 @@
 // fixed order (no float atomics).
 #include <algorithm>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 
 namespace fb {
@@ -43,6 +45,77 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const float* _
     atomicAdd(e + c, v);
     if (p) atomicAdd(p + c, v);
   }
+}
+
+// Deterministic embedding backward (the atomics above add rows in arrival order, so the
+// f32 sums differ run to run): the token ids are stably sorted with their positions
+// (CUB radix sort, keys = ids), then each run of equal ids is owned by one CTA per column
+// block, which sums its dx rows in ascending position order and adds once into gemb.
+__global__ void iota_kernel(int32_t* __restrict__ v, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
+}
+
+constexpr int kEmbCols = 256;  // columns per CTA (64 threads x float4, or 256 scalar)
+
+__global__ void __launch_bounds__(64) embed_bwd_runs_kernel(const int32_t* __restrict__ skey,
+                                                            const int32_t* __restrict__ spos,
+                                                            const float* __restrict__ dx, float* __restrict__ gemb,
+                                                            int n_tok, int d) {
+  const int i0 = blockIdx.x;
+  const int v = skey[i0];
+  if (i0 > 0 && skey[i0 - 1] == v) return;  // not the head of a run
+  int i1 = i0 + 1;
+  while (i1 < n_tok && skey[i1] == v) ++i1;
+  const int c0 = blockIdx.y * kEmbCols;
+  float* out = gemb + (int64_t)v * d;
+  if ((d & 3) == 0) {
+    const int c = c0 + 4 * threadIdx.x;
+    if (c >= d) return;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    int i = i0;
+    for (; i + 4 <= i1; i += 4) {  // four rows in flight, summed in order
+      float4 r[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) r[u] = *reinterpret_cast<const float4*>(dx + (int64_t)spos[i + u] * d + c);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        acc.x += r[u].x; acc.y += r[u].y; acc.z += r[u].z; acc.w += r[u].w;
+      }
+    }
+    for (; i < i1; ++i) {
+      const float4 r = *reinterpret_cast<const float4*>(dx + (int64_t)spos[i] * d + c);
+      acc.x += r.x; acc.y += r.y; acc.z += r.z; acc.w += r.w;
+    }
+    float4* o = reinterpret_cast<float4*>(out + c);
+    float4 g = *o;
+    g.x += acc.x; g.y += acc.y; g.z += acc.z; g.w += acc.w;
+    *o = g;
+  } else {
+    for (int c = c0 + threadIdx.x; c < min(d, c0 + kEmbCols); c += blockDim.x) {
+      float acc = 0.f;
+      for (int i = i0; i < i1; ++i) acc += dx[(int64_t)spos[i] * d + c];
+      out[c] += acc;
+    }
+  }
+}
+
+// gpos[t] += sum_b dx[b*T + t] in ascending b (learned positions, use_alibi = false)
+__global__ void pos_bwd_kernel(const float* __restrict__ dx, float* __restrict__ gpos, int n_tok, int T, int d) {
+  const int64_t n = (int64_t)T * d;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    float acc = 0.f;
+    for (int64_t r = e; r < (int64_t)n_tok * d; r += n) acc += dx[r];
+    gpos[e] += acc;
+  }
+}
+
+static size_t embed_sort_temp_bytes(int n_tok, int vocab) {
+  size_t temp = 0;
+  int bits = 1;
+  while ((1 << bits) < vocab) ++bits;
+  cub::DeviceRadixSort::SortPairs(nullptr, temp, (const int32_t*)nullptr, (int32_t*)nullptr, (const int32_t*)nullptr,
+                                  (int32_t*)nullptr, n_tok, 0, bits);
+  return temp;
 }
 
 // ------------------------------------------------------------------ LayerNorm
@@ -418,6 +491,40 @@ extern "C" int fb_embed_bwd(const int32_t* d_tok, const float* d_dx, float* d_ge
   FB_REQUIRE(n_tok > 0 && T > 0 && d > 0 && vocab > 0, "embed_bwd: bad shape");
   embed_bwd_kernel<<<(n_tok + 7) / 8, 256, 0, (cudaStream_t)stream>>>(d_tok, d_dx, d_gemb, d_gpos, n_tok, T, d);
   FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
+extern "C" int64_t fb_embed_bwd_work_bytes(int n_tok, int vocab) {
+  if (n_tok <= 0 || vocab <= 0) return 0;
+  return 3 * (((int64_t)n_tok * 4 + 255) / 256 * 256) + (int64_t)embed_sort_temp_bytes(n_tok, vocab) + 256;
+}
+
+extern "C" int fb_embed_bwd_sorted(const int32_t* d_tok, const float* d_dx, float* d_gemb, float* d_gpos, int n_tok,
+                                   int T, int d, int vocab, void* d_work, int64_t work_bytes, void* stream) {
+  FB_REQUIRE(n_tok > 0 && T > 0 && d > 0 && vocab > 0, "embed_bwd: bad shape");
+  FB_REQUIRE(d_work && work_bytes >= fb_embed_bwd_work_bytes(n_tok, vocab), "embed_bwd: work buffer too small");
+  FB_REQUIRE((d & 3) != 0 || ((uintptr_t)d_dx % 16 == 0 && (uintptr_t)d_gemb % 16 == 0),
+             "embed_bwd: dx / gemb must be 16-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t slot = ((int64_t)n_tok * 4 + 255) / 256 * 256;
+  uint8_t* w = reinterpret_cast<uint8_t*>(d_work);
+  int32_t* skey = reinterpret_cast<int32_t*>(w);
+  int32_t* pos_in = reinterpret_cast<int32_t*>(w + slot);
+  int32_t* spos = reinterpret_cast<int32_t*>(w + 2 * slot);
+  void* temp = w + 3 * slot;
+  size_t temp_bytes = embed_sort_temp_bytes(n_tok, vocab);
+  int bits = 1;
+  while ((1 << bits) < vocab) ++bits;
+  iota_kernel<<<std::min((n_tok + 255) / 256, kNumSMs * 4), 256, 0, st>>>(pos_in, n_tok);
+  FB_LAUNCH_CHECK();
+  FB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, d_tok, skey, pos_in, spos, n_tok, 0, bits, st));
+  embed_bwd_runs_kernel<<<dim3(n_tok, (d + kEmbCols - 1) / kEmbCols), 64, 0, st>>>(skey, spos, d_dx, d_gemb, n_tok, d);
+  FB_LAUNCH_CHECK();
+  if (d_gpos) {
+    pos_bwd_kernel<<<std::min<int64_t>(((int64_t)T * d + 255) / 256, kNumSMs * 8), 256, 0, st>>>(d_dx, d_gpos, n_tok,
+                                                                                                T, d);
+    FB_LAUNCH_CHECK();
+  }
   return FB_OK;
 }
 

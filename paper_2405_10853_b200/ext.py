@@ -37,6 +37,8 @@ SIGNATURES = {
     "fb_device_check": [],
     "fb_fedagg_step_f32": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _i64, _d, _d, _i, _vp, _vp, _vp, _vp],
     "fb_fedagg_step_f32_peers": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _i64, _d, _d, _i, _vp, _vp, _vp],
+    "fb_fedagg_round_norms_f32_peers": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _i64, _d, _d, _i, _vp, _vp,
+                                        _vp],
     "fb_fedagg_round_norms_f32": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _i64, _d, _d, _i, _vp, _vp, _vp],
     "fb_fedagg_step_f64delta": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _i64, _d, _d, _i, _vp, _vp, _vp, _vp],
     "fb_sumsq_partials": [_vp, _i64, _vp, _vp],
@@ -48,6 +50,8 @@ SIGNATURES = {
     "fb_gemm_bf16_splitk": [_i, _i, _i, _vp, _i64, _i, _vp, _i64, _i, _vp, _i64, _i, _i, _vp, _i64, _vp],
     "fb_embed_fwd": [_vp, _vp, _vp, _vp, _i, _i, _i, _vp],
     "fb_embed_bwd": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp],
+    "fb_embed_bwd_sorted": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _vp, _i64, _vp],
+    "fb_set_deterministic": [_i],
     "fb_ln_fwd": [_vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp],
     "fb_ln_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _vp],
     "fb_attn_fwd": [_vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
@@ -101,6 +105,8 @@ def lib(require_device: bool = True):
                 getattr(L, name).restype = C.c_int64
             L.fb_model_workspace_bytes.argtypes = [C.POINTER(ModelCfg), _i, _i]
             L.fb_model_workspace_bytes.restype = C.c_int64
+            L.fb_embed_bwd_work_bytes.argtypes = [_i, _i]
+            L.fb_embed_bwd_work_bytes.restype = C.c_int64
             L.fb_last_error.argtypes = []
             L.fb_last_error.restype = C.c_char_p
             _lib = L

@@ -72,18 +72,25 @@ def init_params_host(cfg: TinyLMConfig) -> np.ndarray:
 
 
 def check_gpu_shape(cfg: TinyLMConfig, T: int | None = None) -> None:
+    """The kernels' only shape limits: TMA row pitches (d_model, vocab multiples of 8) and a
+    head dim <= 256. Attention runs on tcgen05 for dh in {64, 128} with T % 128 == 0 and on
+    the fixed-order CUDA-core kernels for every other shape (the reference's desk configs)."""
     dh = cfg.d_model // cfg.n_heads
     why = []
-    if cfg.d_model % 64:
-        why.append(f"d_model={cfg.d_model} not a multiple of 64")
-    if dh not in (64, 128):
-        why.append(f"head dim {dh} not in {{64, 128}}")
-    if cfg.vocab_size % 64:
-        why.append(f"vocab_size={cfg.vocab_size} not a multiple of 64")
-    if T is not None and T % 128:
-        why.append(f"sequence length {T} not a multiple of 128")
+    if cfg.d_model % 8:
+        why.append(f"d_model={cfg.d_model} not a multiple of 8")
+    if dh > 256:
+        why.append(f"head dim {dh} above 256")
+    if cfg.vocab_size % 8:
+        why.append(f"vocab_size={cfg.vocab_size} not a multiple of 8")
     if why:
         raise UnsupportedShapeError("sm_100a kernels do not implement this shape: " + "; ".join(why))
+
+
+def set_deterministic(enable: bool = True) -> None:
+    """Bitwise-reproducible training (reference tests/test_trainer.py:56-63): route the
+    attention backward to the fixed-order kernels (fb_set_deterministic). Process-wide."""
+    ext.call("fb_set_deterministic", int(bool(enable)))
 
 
 def model_cfg_struct(cfg: TinyLMConfig) -> ext.ModelCfg:

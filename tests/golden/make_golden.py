@@ -176,7 +176,7 @@ def gen_round():
 
 
 def gen_c1():
-    """C1: 2 clients x 4 steps x 16x128, FedAvg; 2 rounds of telemetry."""
+    """C1: 2 clients x 4 steps x 16x128, FedAvg; 3 rounds of telemetry."""
     cfg = rmodel.TinyLMConfig(vocab_size=256, context_len=128, n_layers=2, d_model=512, n_heads=8, seed=1234)
     text = rdata.synth_corpus(99, 400_000, "markov")
     corpus = rdata.tokenize_bytes(text, 128, 256)
@@ -188,7 +188,7 @@ def gen_c1():
     opt = rfed.ServerOptState.fresh(len(w), 1.0, 0.0, True)
     its = [rdata.BatchIterator(corpus, s, 16, 99) for s in split.shards]
     tele_all, wsub, mean_losses = [], [], []
-    for rnd in (1, 2):
+    for rnd in (1, 2, 3):
         agg = rfed.AggregatorState(rnd, len(w), deterministic=True)
         for k, s in enumerate(split.shards):
             task = TrainTask(rnd, k, 4, (rnd - 1) * 4, 16, 1, {"data": 99}, "k")

@@ -39,7 +39,12 @@ def attn_ref(qkv, B, T, H, dh, use_alibi):
 
 @pytest.mark.parametrize("B,T,H,dh,alibi", [(2, 128, 2, 64, 1), (1, 256, 3, 64, 1), (2, 128, 2, 128, 1),
                                              (1, 512, 4, 128, 1), (2, 128, 2, 64, 0), (1, 1024, 12, 64, 1),
-                                             (1, 384, 2, 128, 1), (2, 640, 3, 64, 0)])
+                                             (1, 384, 2, 128, 1), (2, 640, 3, 64, 0),
+                                             # the C3 / C4 context length (T = 2048), dead-block map on
+                                             (1, 2048, 16, 128, 1), (1, 2048, 12, 64, 1),
+                                             # CUDA-core path: the reference's desk shapes and ragged T
+                                             (3, 64, 4, 16, 1), (2, 16, 2, 8, 1), (2, 8, 2, 4, 0), (1, 16, 3, 8, 1),
+                                             (2, 200, 2, 64, 1), (1, 130, 2, 128, 0), (2, 96, 3, 32, 1)])
 def test_attention_fwd_bwd(fb, B, T, H, dh, alibi):
     torch.manual_seed(0)
     dev = torch.device("cuda")
@@ -47,7 +52,7 @@ def test_attention_fwd_bwd(fb, B, T, H, dh, alibi):
     qkv = torch.randn(B * T, 3 * d, device=dev).to(torch.bfloat16)
     o = torch.empty(B * T, d, dtype=torch.bfloat16, device=dev)
     lse2 = torch.empty(B * H * T, dtype=torch.float32, device=dev)
-    live = torch.empty(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device=dev)
+    live = torch.empty(B * H * ((T + 127) // 128) * ((T + 63) // 64), dtype=torch.uint8, device=dev)
     fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), live.data_ptr(), B, T, H, dh, alibi,
             fb.stream_handle())
     q32 = qkv.float().requires_grad_()
@@ -192,6 +197,43 @@ def test_embedding(fb):
     torch.cuda.synchronize()
     torch.testing.assert_close(ge, ref, atol=1e-4, rtol=1e-5)
     torch.testing.assert_close(gp, dx.view(B, T, d).sum(0), atol=1e-4, rtol=1e-5)
+
+
+@pytest.mark.parametrize("V,d,B,T,skew", [(300, 256, 4, 64, False), (32000, 2048, 8, 2048, True), (64, 16, 4, 16, False),
+                                          (48, 24, 3, 16, True)])
+def test_embedding_bwd_sorted_is_deterministic(fb, V, d, B, T, skew):
+    """the sorted-token segment sum gives the same bits on every run and equals
+    the fixed-order (ascending position) sum of the rows of each token."""
+    torch.manual_seed(3)
+    dev = torch.device("cuda")
+    n = B * T
+    tok = torch.randint(0, V, (n,), device=dev, dtype=torch.int32)
+    if skew:  # one dominant id, as in real text
+        tok[torch.rand(n, device=dev) < 0.3] = 7
+    dx = torch.randn(n, d, device=dev)
+    wb = int(fb.lib().fb_embed_bwd_work_bytes(n, V))
+    work = torch.empty(wb, dtype=torch.uint8, device=dev)
+    outs = []
+    for _ in range(3):
+        ge = torch.full((V, d), 0.5, device=dev)
+        gp = torch.full((T, d), 0.25, device=dev)
+        fb.call("fb_embed_bwd_sorted", tok.data_ptr(), dx.data_ptr(), ge.data_ptr(), gp.data_ptr(), n, T, d, V,
+                work.data_ptr(), wb, fb.stream_handle())
+        outs.append((ge.clone(), gp.clone()))
+    torch.cuda.synchronize()
+    for ge, gp in outs[1:]:
+        assert torch.equal(ge, outs[0][0]) and torch.equal(gp, outs[0][1])
+    ge, gp = outs[0]
+    ref = torch.zeros(V, d, dtype=torch.float64, device=dev).index_add_(0, tok.long(), dx.double()) + 0.5
+    torch.testing.assert_close(ge.double(), ref, atol=1e-3 * (n / V) ** 0.5 + 1e-4, rtol=1e-5)
+    torch.testing.assert_close(gp.double(), dx.double().view(B, T, d).sum(0) + 0.25, atol=1e-4, rtol=1e-5)
+    # the exact fixed-order f32 sum for a few ids
+    t_cpu, dx_cpu = tok.cpu().numpy(), dx.cpu().numpy()
+    for v in np.unique(t_cpu)[:3]:
+        acc = np.zeros(d, np.float32)
+        for r in np.nonzero(t_cpu == v)[0]:
+            acc += dx_cpu[r]
+        assert np.array_equal(ge[v].cpu().numpy(), acc + np.float32(0.5)), v
 
 
 @pytest.mark.parametrize("V", [256, 32000])

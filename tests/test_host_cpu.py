@@ -31,7 +31,8 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     assert L.fb_abi_version() == 1
     # every declared entry has a ctypes signature in the binding
-    bound = set(ext.SIGNATURES) | {"fb_last_error", "fb_model_n_params", "fb_model_workspace_bytes"}
+    bound = set(ext.SIGNATURES) | {"fb_last_error", "fb_model_n_params", "fb_model_workspace_bytes",
+                                     "fb_embed_bwd_work_bytes"}
     assert set(syms) <= bound, set(syms) - bound
 
 
@@ -61,8 +62,13 @@ def test_unsupported_shape_is_loud():
     from paper_2405_10853_b200.config import TinyLMConfig
     from paper_2405_10853_b200.errors import UnsupportedShapeError
     from paper_2405_10853_b200.model import check_gpu_shape
-    with pytest.raises(UnsupportedShapeError):
-        check_gpu_shape(TinyLMConfig(vocab_size=32, context_len=8, n_layers=2, d_model=8, n_heads=2))
+    with pytest.raises(UnsupportedShapeError, match="d_model=12"):
+        check_gpu_shape(TinyLMConfig(vocab_size=32, context_len=8, n_layers=2, d_model=12, n_heads=2))
+    with pytest.raises(UnsupportedShapeError, match="vocab_size=30"):
+        check_gpu_shape(TinyLMConfig(vocab_size=30, context_len=8, n_layers=2, d_model=16, n_heads=2))
+    # every shape the reference's own goldens and shipped configs use is accepted
+    check_gpu_shape(TinyLMConfig(vocab_size=32, context_len=8, n_layers=2, d_model=8, n_heads=2), 8)
+    check_gpu_shape(TinyLMConfig(vocab_size=48, context_len=16, n_layers=1, d_model=24, n_heads=3), 16)
     check_gpu_shape(TinyLMConfig(vocab_size=32000, context_len=2048, n_layers=24, d_model=2048, n_heads=16), 2048)
 
 

@@ -120,3 +120,40 @@ def test_train_round_vs_reference():
     delta = g["params"].astype(np.float64) - w.astype(np.float64)
     np.testing.assert_allclose(delta, g["delta"], rtol=1e-4, atol=1e-9)
     np.testing.assert_allclose(np.array(tele), g["tele"], rtol=1e-5)
+
+
+def test_c1_three_rounds_and_round2_is_chaotic():
+    """The oracle reproduces the reference's 3-round C1 run (c1.npz) and, from start weights
+    perturbed by 1e-4 relative (40x below bf16 resolution), its own round-2 round-mean loss
+    moves by > 0.3: the reference algorithm is chaotic at the round-2 grad-norm spikes, which
+    is why free-running GPU rounds 2-3 are bounded by this envelope and the strict 2e-2 bound
+    is applied from a common start model (tests/test_gpu_round_parity.py)."""
+    import torch
+    from oracle import fedopt_ref
+    torch.set_num_threads(min(8, os.cpu_count() or 1))
+    g = golden("c1.npz")
+    tok = data_ref.tokens_of(data_ref.markov_bytes(99, 400_000))
+    _, shards = data_ref.split(data_ref.n_samples(tok, 128), 2, 99, 0.05)
+    orders = [data_ref.client_order(s, k, 99) for k, s in enumerate(shards)]
+    opt = dict(beta1=0.9, beta2=0.95, eps=1e-8, weight_decay=1e-5, clip_norm=1.0)
+
+    def run(w):
+        m = np.zeros_like(w)
+        means = []
+        for rnd in (1, 2, 3):
+            ws = []
+            for k, s in enumerate(shards):
+                wk, tele = round_ref.train_round(w, tok, 128, orders[k], s.size, (256, 128, 2, 512, 8, True), opt,
+                                                 (1e-3, 2, 1000, 0.1), local_steps=4, schedule_offset=(rnd - 1) * 4,
+                                                 batch_size=16, micro_batches=1)
+                ws.append(wk)
+                means.append(np.mean([t[1] for t in tele]))
+            w, m = fedopt_ref.fed_round(w, m, ws, [s.size for s in shards], 1.0, 0.0, True)
+        return np.array(means)
+
+    w0 = model_ref.init_flat(256, 128, 2, 512, 1234)
+    np.testing.assert_allclose(run(w0), g["mean_losses"], atol=2e-3)
+    pert = (w0 * (1 + 1e-4 * np.random.default_rng(1).standard_normal(w0.size))).astype(np.float32)
+    d = np.abs(run(pert) - g["mean_losses"])
+    assert d[:2].max() < 2e-3          # round 1: insensitive
+    assert d[2] > 0.3                  # round 2, client 0: the spike moves the round mean by ~0.35
