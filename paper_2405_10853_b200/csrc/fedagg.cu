@@ -121,8 +121,13 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
   }
   unsigned long long bad = ~0ull;
   const int64_t nvec = n / VEC;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec;
-       v += (int64_t)gridDim.x * blockDim.x) {
+  // With STATS the per-client norms are reduced across the warp (warp_sum), so every lane of a
+  // warp runs the same trip count: lanes past the end recompute the last vector (valid reads)
+  // and neither store nor count it. Without STATS the loop is the plain grid-stride one.
+  for (int64_t v0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; STATS ? (v0 - lane_ < nvec) : (v0 < nvec);
+       v0 += (int64_t)gridDim.x * blockDim.x) {
+    const bool act = !STATS || v0 < nvec;
+    const int64_t v = act ? v0 : nvec - 1;
     const int64_t j0 = v * VEC;
     float wv[VEC], mv[VEC];
     if constexpr (VEC == 4) {
@@ -175,7 +180,7 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
                 ck += (double)cv[e] * (double)cv[e];
               }
               if (client_norms) {
-                ck = warp_sum(ck);
+                ck = warp_sum(act ? ck : 0.0);
                 if (lane_ == 0) red[kStatsFixed + k][wid_] += ck;
               }
             }
@@ -196,7 +201,7 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
 #pragma unroll
       for (int e = 0; e < VEC; ++e) {
         pg[e] = (K == 1) ? sum[e] : __ddiv_rn(deterministic ? acc[e].result(K) : sum[e], total);
-        if (STATS) {
+        if (STATS && act) {
           const double w0 = (double)wv[e];
           s_w0 += w0 * w0;
           s_avg += avg[e] * avg[e];
@@ -226,12 +231,12 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
 #pragma unroll
       for (int e = 0; e < VEC; ++e) pg[e] = __ddiv_rn(sum[e], total);
     }
-    if (pg_out) {
+    if (pg_out && act) {
 #pragma unroll
       for (int e = 0; e < VEC; ++e) pg_out[j0 + e] = pg[e];
     }
     if (!w_out) {
-      if (STATS) {
+      if (STATS && act) {
 #pragma unroll
         for (int e = 0; e < VEC; ++e) s_pg += pg[e] * pg[e];
       }
@@ -243,14 +248,15 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
       StepOut o = outer_step(wv[e], mv[e], pg[e], eta, mu, nesterov);
       wo[e] = o.w;
       mo[e] = o.m;
-      if (STATS) {
+      if (STATS && act) {
         s_pg += pg[e] * pg[e];
         s_w += (double)o.w * (double)o.w;
         s_m += (double)o.m * (double)o.m;
       }
-      if (!(isfinite(o.w) && isfinite(o.m)) && (unsigned long long)(j0 + e) < bad)
+      if (act && !(isfinite(o.w) && isfinite(o.m)) && (unsigned long long)(j0 + e) < bad)
         bad = (unsigned long long)(j0 + e);
     }
+    if (!act) continue;
     if constexpr (VEC == 4) {
       st_stream_f4(w_out + j0, make_float4(wo[0], wo[1], wo[2], wo[3]));
       st_stream_f4(m_out + j0, make_float4(mo[0], mo[1], mo[2], mo[3]));

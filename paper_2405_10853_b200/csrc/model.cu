@@ -165,7 +165,7 @@ extern "C" int64_t fb_model_n_params(const fb_model_cfg* cfg) { return layout_of
 extern "C" int64_t fb_model_workspace_bytes(const fb_model_cfg* cfg, int batch, int T) {
   Arena A{nullptr};
   carve(*cfg, batch, T, A);
-  return A.off + 256;
+  return (A.off + 256 + 255) & ~int64_t(255);
 }
 
 extern "C" int fb_model_fwd_bwd(const fb_model_cfg* cfgp, const float* P, const void* shadow, float* G,

@@ -29,6 +29,50 @@ def clients_of(rank: int, world: int, n_clients: int):
     return [k for k in range(n_clients) if k % world == rank]
 
 
+NO_BAD = 1 << 62  # "no non-finite index" (any value >= n means none)
+
+
+def gather_vector(shard, n: int, group=None):
+    """All ranks' contiguous shards (shard_bounds layout) -> the full [n] vector on every rank.
+    Used for the server momentum before a checkpoint (restore_server, server.py:164, needs
+    the full-length vector)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    lo, hi, per = shard_bounds(n, world, rank)
+    mine = torch.zeros(per, dtype=shard.dtype, device=shard.device)
+    mine[: hi - lo].copy_(shard[: hi - lo])
+    if dist.get_backend(group) == "nccl":
+        full = torch.empty(per * world, dtype=shard.dtype, device=shard.device)
+        dist.all_gather_into_tensor(full, mine, group=group)
+    else:
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine, group=group)
+        full = torch.cat(parts)
+    return full[:n]
+
+
+def reduce_round_end(stats, bad, group=None):
+    """Sum the per-shard telemetry side reductions and take the global first non-finite index
+    (min over ranks) in one host round trip: (stats f64 numpy, first_bad int)."""
+    import torch
+    import torch.distributed as dist
+    s = stats.clone()
+    b = bad.clone()
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(s, group=group)
+        dist.all_reduce(b, op=dist.ReduceOp.MIN, group=group)
+    return s.cpu().numpy(), int(b.item())
+
+
+def _global_bad(local_bad, count: int, offset: int):
+    """A kernel's first-bad index (relative to its launch of `count` elements, >= count when
+    none) -> a global index, or NO_BAD."""
+    import torch
+    return torch.where(local_bad < count, local_bad + offset, torch.full_like(local_bad, NO_BAD))
+
+
 class ShardedAggregator:
     """Round-end aggregation + outer step across `world` ranks (torch.distributed / NCCL).
 
@@ -54,9 +98,10 @@ class ShardedAggregator:
         self.recv = torch.empty(self.K if self.world > 1 else 0, self.per, dtype=torch.float32, device=dev)
         self.src = {}
         self.w_full = torch.empty(self.per * self.world, dtype=torch.float32, device=dev)
-        # fb_fedagg_* write kStatsFixed = 6 side reductions (||pg||^2, ||w'||^2, ||m'||^2, ...)
-        self.stats = torch.zeros(6, dtype=torch.float64, device=dev)
-        self.bad = torch.empty(1, dtype=torch.int64, device=dev)
+        # round-norm side reductions of this shard (fb_fedagg_round_norms_f32): 6 fixed + K clients
+        self.stats = torch.zeros(6 + n_clients, dtype=torch.float64, device=dev)
+        self.bad = torch.full((1,), NO_BAD, dtype=torch.int64, device=dev)  # global index after step()
+        self.ids = list(range(n_clients))
 
     def exchange(self, local: dict):
         """all-to-all: every client's slice r lands on rank r (grouped send/recv)."""
@@ -90,9 +135,13 @@ class ShardedAggregator:
         w_slice = w[self.lo:self.hi]
         m_new = torch.empty_like(m_shard)
         wo = self.w_full[self.rank * self.per: self.rank * self.per + cnt]
+        self.ids = ids
+        self.stats.zero_()
+        self.bad.fill_(NO_BAD)
         if cnt > 0:
             self.kernel([self.src[k][:cnt] for k in ids], [int(n_k[k]) for k in ids], deterministic, w_slice,
                         m_shard, wo, m_new, eta, mu, nesterov, self)
+            self.bad.copy_(_global_bad(self.bad, cnt, self.lo))
         if self.world > 1:
             mine = self.w_full[self.rank * self.per:(self.rank + 1) * self.per]
             if self.dist.get_backend(self.group) == "nccl":
@@ -106,12 +155,13 @@ class ShardedAggregator:
 
 
 def fused_kernel(srcs, nks, deterministic, w_slice, m_slice, w_out, m_out, eta, mu, nesterov, agg):
-    """fb_fedagg_step_f32 on one rank's slice (clients already in reduction order)."""
+    """fb_fedagg_round_norms_f32 on one rank's slice (clients already in reduction order):
+    the fused step plus this shard's share of every round norm (agg.stats[6 + K])."""
     ptrs = (C.c_void_p * len(srcs))(*[t.data_ptr() for t in srcs])
     nk = (C.c_int64 * len(srcs))(*nks)
-    ext.call("fb_fedagg_step_f32", ptrs, nk, len(srcs), int(deterministic), w_slice.data_ptr(), m_slice.data_ptr(),
-             w_out.data_ptr(), m_out.data_ptr(), w_slice.numel(), float(eta), float(mu), int(nesterov),
-             agg.stats.data_ptr(), agg.bad.data_ptr(), None, ext.stream_handle())
+    ext.call("fb_fedagg_round_norms_f32", ptrs, nk, len(srcs), int(deterministic), w_slice.data_ptr(),
+             m_slice.data_ptr(), w_out.data_ptr(), m_out.data_ptr(), w_slice.numel(), float(eta), float(mu),
+             int(nesterov), agg.stats.data_ptr(), agg.bad.data_ptr(), ext.stream_handle())
 
 
 class PeerAggregator:
@@ -167,9 +217,10 @@ class PeerAggregator:
         self.hw = symm.rendezvous(self.wbuf, grp)
         self.cptr = [int(p) for p in self.hc.buffer_ptrs]
         self.wptr = [int(p) for p in self.hw.buffer_ptrs]
-        # fb_fedagg_* write kStatsFixed = 6 side reductions (||pg||^2, ||w'||^2, ||m'||^2, ...)
-        self.stats = torch.zeros(6, dtype=torch.float64, device=dev)
-        self.bad = torch.empty(1, dtype=torch.int64, device=dev)
+        # round-norm side reductions of this shard (fb_fedagg_round_norms_f32_peers): 6 fixed + K clients
+        self.stats = torch.zeros(6 + n_clients, dtype=torch.float64, device=dev)
+        self.bad = torch.full((1,), NO_BAD, dtype=torch.int64, device=dev)  # global index after step()
+        self.ids = list(range(n_clients))
         self.width = width
         # peer views of every rank's client slots (for the copy-engine pull)
         self.peer_clients = [self.hc.get_buffer(r, (self.slots, width), torch.float32) for r in range(self.world)]
@@ -202,11 +253,15 @@ class PeerAggregator:
         ids = sorted(n_k) if deterministic else list(n_k)
         reps = [self.wptr[r] + 4 * self.lo for r in range(self.world) if r != self.rank]
         m_new = torch.empty_like(m_shard)
+        self.ids = ids
+        self.stats.zero_()
+        self.bad.fill_(NO_BAD)
         self.hc.barrier(channel=0)  # every rank's clients are final
         if cnt > 0 and self.pull == "sm":
             srcs = [self.cptr[k % self.world] + 4 * ((k // self.world) * self.width + self.lo) for k in ids]
             self._launch(srcs, ids, n_k, deterministic, w, m_shard, m_new, reps, 0, cnt, eta, mu, nesterov,
                          self.stats, self.bad)
+            self.bad.copy_(_global_bad(self.bad, cnt, self.lo))
         elif cnt > 0:
             self._staged(ids, n_k, deterministic, w, m_shard, m_new, reps, cnt, eta, mu, nesterov)
         self.hc.barrier(channel=1)  # every shard of w' has landed in every replica
@@ -216,7 +271,7 @@ class PeerAggregator:
 
     def _launch(self, srcs, ids, n_k, deterministic, w, m_shard, m_new, reps, a, b, eta, mu, nesterov, stats, bad):
         wo = self.wbuf[self.lo + a:self.lo + b]
-        ext.call("fb_fedagg_step_f32_peers", (C.c_void_p * len(ids))(*srcs),
+        ext.call("fb_fedagg_round_norms_f32_peers", (C.c_void_p * len(ids))(*srcs),
                  (C.c_int64 * len(ids))(*[int(n_k[k]) for k in ids]), len(ids), int(deterministic),
                  w[self.lo + a:self.lo + b].data_ptr(), m_shard[a:b].data_ptr(), wo.data_ptr(), m_new[a:b].data_ptr(),
                  (C.c_void_p * max(1, len(reps)))(*[p + 4 * a for p in reps]), len(reps), b - a, float(eta),
@@ -236,7 +291,7 @@ class PeerAggregator:
         nch = (cnt + ch - 1) // ch
         if self.stage is None or self.stage.shape[1:] != (len(remote), ch):
             self.stage = torch.empty(2, len(remote), ch, dtype=torch.float32, device=m_shard.device)
-        stats = torch.empty(nch, 6, dtype=torch.float64, device=m_shard.device)
+        stats = torch.empty(nch, 6 + len(ids), dtype=torch.float64, device=m_shard.device)
         bad = torch.empty(nch, dtype=torch.int64, device=m_shard.device)
         main = torch.cuda.current_stream()
         peers = sorted({k % self.world for k in remote})
@@ -264,3 +319,8 @@ class PeerAggregator:
                          stats[c], bad[c:c + 1])
             done[s].record(main)
         torch.sum(stats, 0, out=self.stats)
+        # per-chunk first-bad indices are relative to each launch: offset, then the minimum
+        starts = torch.arange(nch, dtype=torch.int64, device=bad.device) * ch
+        counts = torch.clamp(cnt - starts, max=ch)
+        glob = torch.where(bad < counts, bad + starts + self.lo, torch.full_like(bad, NO_BAD))
+        self.bad.copy_(glob.min().reshape(1))

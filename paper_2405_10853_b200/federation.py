@@ -18,13 +18,14 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import ext
-from .checkpoint import write_checkpoint
+from .checkpoint import write_checkpoint_async
 from .config import AdamWConfig, ScheduleConfig, TinyLMConfig, TrainTask
 from .data import BatchIterator, DataSplit, TokenizedCorpus
-from .dist import PeerAggregator, ShardedAggregator, clients_of
+from .dist import PeerAggregator, ShardedAggregator, clients_of, gather_vector, reduce_round_end
+from .errors import ParamError
 from .fedopt import AggregatorState, DeviceVector, ServerOptState, server_step_with_norms
 from .model import LossEvaluator, init_params_host
-from .telemetry import RoundNorms, norms_from_stats
+from .telemetry import RoundNorms, norms_from_stats  # noqa: F401
 from .trainer import evaluate_mean_ce, train_round
 
 
@@ -37,6 +38,7 @@ class RoundResult:
     client_metrics: dict = field(default_factory=dict)
     telemetry: dict = field(default_factory=dict)
     val_loss: float | None = None
+    checkpoint: object | None = None  # AsyncCheckpointWrite on rank 0 (wait() before reading the file)
 
 
 class Federation:
@@ -61,6 +63,7 @@ class Federation:
         self.iters = {k: BatchIterator(corpus, split.shards[k], batch_size, data_seed) for k in self.mine}
         self.n_k = {k: split.shards[k].n_k for k in range(self.K)}
         self.agg = None
+        self._ckpt = None
         if self.world > 1:  # fused peer-memory round end where NVLink peers map; NCCL exchange otherwise
             try:
                 if dist.get_backend() != "nccl":
@@ -99,17 +102,27 @@ class Federation:
             w_full, m_new = self.agg.step(w.tensor, opt.momentum.tensor, self.n_k, self.eta, self.mu, self.nesterov,
                                           deterministic=self.det, w_out=w_out)
             w_new, opt_new = DeviceVector(w_full), ServerOptState(DeviceVector(m_new), self.eta, self.mu, self.nesterov)
-            stats = self.agg.stats.clone()
-            dist.all_reduce(stats)
-            s = stats.cpu().numpy()
-            norms = RoundNorms(global_norm=float("nan"), per_client_norms={},
-                               avg_client_norm=float("nan"), momentum_norm=math.sqrt(s[2]),
-                               pseudograd_norm=math.sqrt(s[0]))
+            # every shard's side reductions summed, the first non-finite index min-reduced: the same
+            # telemetry and the same failure check as one GPU (fedopt.server_step_with_norms)
+            s, first_bad = reduce_round_end(self.agg.stats, self.agg.bad)
+            if first_bad < len(w):
+                raise ParamError(f"non-finite global model after server step in round {round_num} "
+                                 f"(first bad index {first_bad})")
+            norms = norms_from_stats(s, self.agg.ids, math.sqrt(s[2]))
         val = None
         if self.eval_batches and self.rank == 0 and self.split.validation.size:
             val = evaluate_mean_ce(self.ev, w_new, self.corpus, self.split.validation, self.B, self.eval_batches)
-        if checkpoint_path is not None and self.rank == 0:
-            write_checkpoint({"round": round_num, "global": w_new, "momentum": opt_new.momentum,
-                              "server_opt": {"eta": self.eta, "mu": self.mu, "nesterov": self.nesterov}},
-                             checkpoint_path)
-        return RoundResult(round_num, w_new, opt_new, norms, metrics, tele, val)
+        if checkpoint_path is not None:
+            momentum = opt_new.momentum
+            if self.agg is not None:  # momentum is sharded: the checkpoint holds the full [N] vector
+                momentum = DeviceVector(gather_vector(opt_new.momentum.tensor, len(w_new)))
+            if self.rank == 0:
+                if self._ckpt is not None:  # at most one checkpoint in flight
+                    self._ckpt.wait()
+                # D2H copies ordered behind this round on a side stream; CRC32 + file write on a host
+                # thread: the next round's first steps overlap the checkpoint (server.py:100-132)
+                self._ckpt = write_checkpoint_async(
+                    {"round": round_num, "global": w_new, "momentum": momentum,
+                     "server_opt": {"eta": self.eta, "mu": self.mu, "nesterov": self.nesterov}}, checkpoint_path)
+        return RoundResult(round_num, w_new, opt_new, norms, metrics, tele, val,
+                           self._ckpt if checkpoint_path is not None else None)

@@ -10,6 +10,7 @@ back in a single device->host copy at the end of the round.
 """
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import math
 
@@ -56,8 +57,14 @@ class ClientSession:
     """One client's round on the device, step by step (train_round is a thin loop over it).
 
     begin() places the received global in HBM (no copy if it already is), resets the
-    AdamW moments and positions the data cursor; step() enqueues one whole local step
-    (no host sync); finish() does the round's single device->host copy of telemetry."""
+    AdamW moments and positions the data cursor; step() enqueues one whole local step.
+    Failure detection (trainer.py:89-95, localopt.py:87-88) is asynchronous: each step's
+    telemetry row (64 B) is copied to pinned host memory behind the step and checked once
+    its event has fired; the host never runs more than `max_lag` steps ahead of the last
+    checked one, so a non-finite loss or parameter stops the round within max_lag steps
+    and the error names the local step. finish() only waits for the last rows."""
+
+    max_lag = 2
 
     def __init__(self, evaluator: LossEvaluator, batches: BatchIterator, adamw_cfg: AdamWConfig,
                  sched: ScheduleConfig):
@@ -98,11 +105,34 @@ class ClientSession:
         self.rb = rb
         self.row_loss = rb.rows(task.micro_batches * B * T, ev.device)
         self.tele = torch.zeros(task.local_steps * N_TELE, dtype=torch.float64, device=ev.device)
+        self.tele_host = torch.zeros(task.local_steps, N_TELE, dtype=torch.float64, pin_memory=True)
+        self.pending = collections.deque()
         self.lrs = []
         self.batches.seek(task.schedule_offset * task.micro_batches * B)
         return self
 
+    def _check_row(self, s: int) -> None:
+        row = self.tele_host[s].numpy()
+        if not math.isfinite(float(row[0])):
+            raise RoundFailedError(self.task.client_id,
+                                   f"non-finite loss in round {self.task.round} at local step {s}")
+        if row[5] >= 0:
+            raise ParamError(f"non-finite parameters after AdamW step (local step {s}, index {int(row[5])})")
+
+    def poll(self, block_through: int = -1) -> None:
+        """Check every finished step's telemetry; wait for the steps <= block_through."""
+        while self.pending:
+            s, ev = self.pending[0]
+            if s <= block_through:
+                ev.synchronize()
+            elif not ev.query():
+                break
+            self.pending.popleft()
+            self._check_row(s)
+
     def step(self, s: int) -> None:
+        import torch
+        self.poll(s - 1 - self.max_lag)
         task, B = self.task, self.task.batch_size
         lr = lr_at(self.sched, task.schedule_offset + s)
         self.lrs.append(lr)
@@ -115,18 +145,20 @@ class ClientSession:
                  self.tele[(s % self.task.local_steps) * N_TELE:].data_ptr(), self.rb.scratch.data_ptr(),
                  self.row_loss.data_ptr(), self.ws.data_ptr(), self.ws.numel(), self.st)
         self.batches.cursor += task.micro_batches * B
+        r = s % self.task.local_steps
+        self.tele_host[r].copy_(self.tele[r * N_TELE:(r + 1) * N_TELE], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self.pending.append((s, ev))
 
     def finish(self):
         task = self.task
         S = len(self.lrs)
-        tv = self.tele.view(-1, N_TELE)[:S].cpu().numpy()  # the round's single device->host copy
+        self.poll(S)
+        tv = self.tele_host.numpy()
         telemetry = []
         for s in range(S):
             loss = float(tv[s, 0])
-            if not math.isfinite(loss):
-                raise RoundFailedError(task.client_id, f"non-finite loss in round {task.round}")
-            if tv[s, 5] >= 0:
-                raise ParamError("non-finite parameters after AdamW step")
             telemetry.append(StepTelemetry(task.schedule_offset + s, loss, math.sqrt(tv[s, 1]),
                                            math.sqrt(tv[s, 2]), self.lrs[s], math.sqrt(tv[s, 3])))
         update = DeviceClientUpdate(
@@ -176,7 +208,8 @@ def evaluate_mean_ce(evaluator: LossEvaluator, params, corpus, indices: np.ndarr
         rows = min(batch_size, n - start)
         ws = evaluator.workspace(rows, T, extra=rows * T * 4 + 512)
         need = int(ext.lib().fb_model_workspace_bytes(C.byref(evaluator._mcfg), rows, T))
-        tok = ws[((need + 255) // 256) * 256:].view(torch.int32)
+        off = ((need + 255) // 256) * 256
+        tok = ws[off:off + rows * T * 4].view(torch.int32)
         ext.call("fb_gather_batch", dc.tokens.data_ptr(), order[start:].data_ptr(), rows, 0, rows, T,
                  tok.data_ptr(), st)
         rl = torch.empty(rows * T, dtype=torch.float64, device=evaluator.device)

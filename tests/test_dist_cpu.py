@@ -81,3 +81,40 @@ def test_shard_bounds_cover():
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
             assert all(lo % 4 == 0 for lo, hi in spans if hi > lo)
     assert clients_of(1, 4, 8) == [1, 5]
+
+
+def _worker_round_end(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2405_10853_b200.dist import NO_BAD, gather_vector, reduce_round_end, shard_bounds
+    full = torch.arange(n, dtype=torch.float32) * 0.5 - 3.0
+    lo, hi, _ = shard_bounds(n, world, rank)
+    m_full = gather_vector(full[lo:hi].clone(), n)        # the checkpoint's momentum (federation.py)
+    stats = torch.full((6 + 3,), float(rank + 1), dtype=torch.float64)
+    bad = torch.tensor([NO_BAD if rank != 1 else lo + 5], dtype=torch.int64)
+    s, first_bad = reduce_round_end(stats, bad)
+    q.put((rank, m_full.numpy(), s, first_bad, lo))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 1001), (3, 10)])
+def test_round_end_gather_and_reduce(world, n):
+    """G > 1 round end (federation.py): the sharded momentum gathers to the full [N] vector
+    (so a checkpoint is restorable, server.py:164), the per-shard norm statistics sum, and
+    the first non-finite index is the minimum over ranks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_round_end, args=(r, world, port, n, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in ps:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = np.arange(n, dtype=np.float32) * 0.5 - 3.0
+    lo1 = res[1][4]
+    for rank, m_full, s, first_bad, _ in res:
+        assert m_full.shape == (n,) and np.array_equal(m_full, want)
+        assert np.allclose(s, sum(range(1, world + 1)))
+        assert first_bad == lo1 + 5

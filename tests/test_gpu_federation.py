@@ -31,6 +31,7 @@ def test_federation_round1_vs_reference(tmp_path):
     assert np.median(err) <= 5e-4
     assert res.norms.pseudograd_norm > 0 and len(res.norms.per_client_norms) == 2
     assert np.isfinite(res.val_loss) and res.val_loss < 5.6
+    assert res.checkpoint.wait() > 0
     ck = read_checkpoint(tmp_path / "r1.fedp")
     assert ck["round"] == 1 and ck["global"].bitwise_equal(res.params.to_param_vector())
     res2 = fed.run_round(res.params, res.opt, 2)
@@ -52,3 +53,26 @@ def test_flower_facade_fit_and_aggregate():
     assert len(new_params) == len(params) and metrics["n_contributors"] == 2
     assert abs(sum(metrics["weights"].values()) - 1.0) < 1e-12
     assert all(np.isfinite(a).all() for a in new_params)
+
+
+def test_async_checkpoint_of_device_vectors(tmp_path):
+    """(f)4: the round-boundary checkpoint snapshots device vectors with async D2H copies on a
+    side stream (the caller continues at once) and writes the same bytes as the host encoder."""
+    from paper_2405_10853_b200.checkpoint import decode_sections, encode_sections, write_checkpoint_async
+    from paper_2405_10853_b200.fedopt import DeviceVector
+    from paper_2405_10853_b200.params import ParamVector
+    n = 10_000_019
+    w = torch.randn(n, device="cuda")
+    m = torch.randn(n, device="cuda") * 1e-3
+    w2 = w * 2  # produced on the current stream right before the snapshot
+    h = write_checkpoint_async({"round": 7, "global": DeviceVector(w2), "momentum": DeviceVector(m),
+                                "server_opt": {"eta": 0.7, "mu": 0.9, "nesterov": True}}, tmp_path / "a.fedp")
+    nbytes = h.wait()
+    raw = open(tmp_path / "a.fedp", "rb").read()
+    assert nbytes == len(raw)
+    want = encode_sections({"round": 7, "global": ParamVector(w2.cpu().numpy()),
+                            "momentum": ParamVector(m.cpu().numpy()),
+                            "server_opt": {"eta": 0.7, "mu": 0.9, "nesterov": True}})
+    assert raw == want
+    dec = decode_sections(raw)
+    assert dec["global"].bitwise_equal(ParamVector(w2.cpu().numpy())) and dec["round"] == 7

@@ -8,6 +8,8 @@ import os
 import subprocess
 import sys
 
+import numpy as np
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -26,10 +28,37 @@ def test_peer_round_end_bit_identical(n, chunk):
     env = dict(os.environ, CHK_N=str(n), CHK_CHUNK=str(chunk), CHK_K="8")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29541", os.path.join(ROOT, "tools", "multi_gpu_check.py")]
-    out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     line = [x for x in out.stdout.splitlines() if x.startswith("{")][-1]
     r = json.loads(line)
     for key in ("bit_identical_w", "bit_identical_m", "peer_bit_identical_w", "peer_bit_identical_m",
-                "peer_sm_bit_identical", "peer_stats_ce_vs_sm_close"):
+                "peer_sm_bit_identical", "peer_stats_ce_vs_sm_close", "round_norms_match_1gpu",
+                "first_bad_global_index"):
         assert r[key], (key, r)
+
+
+def _fed(nproc, port):
+    env = dict(os.environ)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(nproc),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tools", "fed_multi.py")]
+    out = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    return json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+
+
+@pytest.mark.gpu
+def test_federation_two_gpus_matches_one():
+    """The round driver on 2 GPUs (clients sharded, peer-memory round end) against 1 GPU:
+    same round-2 client losses, the full round telemetry (was NaN / empty on G > 1)
+    and a checkpoint whose momentum is the full [N] vector (restore_server, server.py:164)."""
+    if _gpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    one, two = _fed(1, 29551), _fed(2, 29553)
+    assert two["aggregator"] == "PeerAggregator" and two["finite"]
+    assert two["ckpt_momentum_len"] == two["ckpt_global_len"] == one["ckpt_global_len"]
+    np.testing.assert_allclose(two["round2_client_mean_losses"], one["round2_client_mean_losses"], atol=2e-3)
+    for key in ("global", "avg_client", "pseudograd", "momentum"):
+        np.testing.assert_allclose(two["norms"][key], one["norms"][key], rtol=2e-3)
+    np.testing.assert_allclose(two["norms"]["per_client"], one["norms"]["per_client"], rtol=2e-3)
+    np.testing.assert_allclose(two["ckpt_momentum_norm"], two["norms"]["momentum"], rtol=1e-6)

@@ -26,7 +26,8 @@ kw = dict(batch_size=16, micro_batches=1, local_steps=4, server_eta=0.7, server_
 fed = Federation(cfg, AdamWConfig(), ScheduleConfig(1e-3, 2, 1000, 0.1), corpus, split, **kw)
 w, opt = fed.init_state()
 res = fed.run_round(w, opt, 1)
-res = fed.run_round(res.params, res.opt, 2)
+ck_path = os.environ.get("FED_CKPT", "/tmp/fed_multi_r2.fedp")
+res = fed.run_round(res.params, res.opt, 2, checkpoint_path=ck_path)
 losses = torch.zeros(K, dtype=torch.float64, device="cuda")
 for k, mtr in res.client_metrics.items():
     losses[k] = mtr["mean_loss"]
@@ -34,7 +35,16 @@ dist.all_reduce(losses)
 w_multi = res.params.tensor.clone()
 kind = type(fed.agg).__name__
 if rank == 0:
+    from paper_2405_10853_b200.checkpoint import read_checkpoint
+    res.checkpoint.wait()
+    ck = read_checkpoint(ck_path)
+    n = res.norms
     print(json.dumps({"world": world, "aggregator": kind, "round2_client_mean_losses": [round(float(x), 5) for x in
-                      losses.tolist()], "w_norm": float(w_multi.double().norm()), "finite": bool(torch.isfinite(w_multi).all())}),
+                      losses.tolist()], "w_norm": float(w_multi.double().norm()), "finite": bool(torch.isfinite(w_multi).all()),
+                      "ckpt_momentum_len": len(ck["momentum"]), "ckpt_global_len": len(ck["global"]),
+                      "ckpt_momentum_norm": float(np.linalg.norm(np.asarray(ck["momentum"].data, np.float64))),
+                      "norms": {"global": n.global_norm, "avg_client": n.avg_client_norm, "pseudograd": n.pseudograd_norm,
+                                "momentum": n.momentum_norm,
+                                "per_client": [n.per_client_norms[k] for k in sorted(n.per_client_norms)]}}),
           flush=True)
 dist.destroy_process_group()

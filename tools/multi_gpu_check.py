@@ -13,7 +13,8 @@ import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_10853_b200 import ext  # noqa: E402
-from paper_2405_10853_b200.dist import PeerAggregator, ShardedAggregator, clients_of  # noqa: E402
+from paper_2405_10853_b200.dist import (PeerAggregator, ShardedAggregator, clients_of,  # noqa: E402
+                                        reduce_round_end)
 
 N = int(os.environ.get("CHK_N", "70542336"))
 K = int(os.environ.get("CHK_K", "8"))
@@ -50,6 +51,7 @@ e1.record()
 torch.cuda.synchronize()
 ms = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
 dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+stats_nccl, bad_nccl = reduce_round_end(agg.stats, agg.bad)
 # (b) fused over NVLink peer memory: copy-engine staged pull (default) and direct SM pull
 res_peer = {}  # both forms explicitly (the product default "auto" picks one per world size)
 for mode in ("ce", "sm"):
@@ -69,33 +71,48 @@ for mode in ("ce", "sm"):
     torch.cuda.synchronize()
     t_ms = torch.tensor([e0.elapsed_time(e1) / reps], device="cuda")
     dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
-    res_peer[mode] = (float(t_ms), w_peer.clone(), m_peer.clone(), peer.stats.clone())
+    st_sum, bad_sum = reduce_round_end(peer.stats, peer.bad)
+    # an injected NaN in the last client's last-shard element must surface as that global index
+    kn = K - 1
+    if kn % world == rank:
+        peer.client_buffer(kn)[N - 3] = float("nan")
+    w_nan, _ = peer.step(w, m_sh, nk, 0.7, 0.9, True)
+    _, bad_nan = reduce_round_end(peer.stats, peer.bad)
+    res_peer[mode] = (float(t_ms), w_peer.clone(), m_peer.clone(), st_sum, bad_sum, bad_nan)
     del peer
     torch.cuda.empty_cache()
-ms_peer, w_peer, m_peer, _ = res_peer["ce"]
-ms_peer_sm, w_peer_sm, m_peer_sm, _ = res_peer["sm"]
+ms_peer, w_peer, m_peer = res_peer["ce"][:3]
+ms_peer_sm, w_peer_sm, m_peer_sm = res_peer["sm"][:3]
 # single-GPU reference on every rank (all clients regenerated locally)
 allc = [client(k) for k in range(K)]
 ptrs = (C.c_void_p * K)(*[t.data_ptr() for t in allc])
 nks = (C.c_int64 * K)(*[nk[k] for k in range(K)])
 wr, mr = torch.empty_like(w), torch.empty_like(m)
-ext.call("fb_fedagg_step_f32", ptrs, nks, K, 1, w.data_ptr(), m.data_ptr(), wr.data_ptr(), mr.data_ptr(), N, 0.7, 0.9, 1,
-         None, None, None, ext.stream_handle())
+stats1 = torch.zeros(6 + K, dtype=torch.float64, device="cuda")
+ext.call("fb_fedagg_round_norms_f32", ptrs, nks, K, 1, w.data_ptr(), m.data_ptr(), wr.data_ptr(), mr.data_ptr(), N, 0.7,
+         0.9, 1, stats1.data_ptr(), None, ext.stream_handle())
 torch.cuda.synchronize()
+s1 = stats1.cpu().numpy()
+import numpy as np  # noqa: E402
+norms_ok = all(np.allclose(x, s1, rtol=1e-9, atol=0) for x in (stats_nccl, res_peer["ce"][3], res_peer["sm"][3]))
+bad_ok = bad_nccl >= N and res_peer["ce"][4] >= N and res_peer["sm"][4] >= N and \
+    res_peer["ce"][5] == N - 3 and res_peer["sm"][5] == N - 3
 ok_w = torch.equal(w_new.view(torch.int32), wr.view(torch.int32))
 ok_m = torch.equal(m_shard.view(torch.int32), mr[agg.lo:agg.hi].view(torch.int32))
 ok_pw = torch.equal(w_peer.view(torch.int32), wr.view(torch.int32))
 ok_pm = torch.equal(m_peer.view(torch.int32), mr[agg.lo:agg.hi].view(torch.int32))
 ok_sm = torch.equal(w_peer_sm.view(torch.int32), wr.view(torch.int32)) and torch.equal(
     m_peer_sm.view(torch.int32), mr[agg.lo:agg.hi].view(torch.int32))
-ok_st = torch.allclose(res_peer["ce"][3][:3], res_peer["sm"][3][:3], rtol=1e-12, atol=0)
-flags = torch.tensor([int(ok_w), int(ok_m), int(ok_pw), int(ok_pm), int(ok_sm), int(ok_st)], device="cuda")
+ok_st = bool(np.allclose(res_peer["ce"][3][:3], res_peer["sm"][3][:3], rtol=1e-12, atol=0))
+flags = torch.tensor([int(ok_w), int(ok_m), int(ok_pw), int(ok_pm), int(ok_sm), int(ok_st), int(norms_ok),
+                      int(bad_ok)], device="cuda")
 dist.all_reduce(flags, op=dist.ReduceOp.MIN)
 per_rank_bytes = 4 * N * len(mine) * (world - 1) / world + 4 * N * (world - 1) / world
 if rank == 0:
     print(json.dumps({"world": world, "N": N, "K": K, "bit_identical_w": bool(flags[0]), "bit_identical_m": bool(flags[1]),
                       "peer_bit_identical_w": bool(flags[2]), "peer_bit_identical_m": bool(flags[3]),
                       "peer_sm_bit_identical": bool(flags[4]), "peer_stats_ce_vs_sm_close": bool(flags[5]),
+                      "round_norms_match_1gpu": bool(flags[6]), "first_bad_global_index": bool(flags[7]),
                       "peer_sm_ms": round(ms_peer_sm, 3),
                       "exchange_ms": round(float(ms), 3), "peer_fused_ms": round(ms_peer, 3),
                       "peer_nvlink_in_bytes_per_rank": int(4 * (N // world) * (K - len(mine))),
