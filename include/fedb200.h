@@ -76,6 +76,12 @@ int fb_fedagg_step_f64delta(const double* const* d_deltas, const int64_t* n_k, i
                             float* d_m_out, int64_t n, double eta, double mu, int nesterov,
                             double* d_stats, int64_t* d_first_bad, double* d_pg_out, void* stream);
 
+/* AggregatorState.weighted_sum (fedopt.py:95): d_out[n] (f64) = sum_k n_k * delta_k in the
+ * given (arrival) order, delta_k = f64(w) - f64(w_k) for f32 client weights (src_is_f64_delta
+ * = 0, d_w needed) or the f64 deltas themselves (1). Bitwise the reference's running sum. */
+int fb_fedagg_weighted_sum(const void* const* d_src, int src_is_f64_delta, const int64_t* n_k,
+                           int n_clients, const float* d_w, int64_t n, double* d_out, void* stream);
+
 /* ---- client optimizer (K10-K12) --------------------------------------------------- */
 /* d_partials[FB_RED_BLOCKS] = per-block sum of x^2 (f64). l2_norm: params.py:126-133 */
 int fb_sumsq_partials(const float* d_x, int64_t n, double* d_partials, void* stream);

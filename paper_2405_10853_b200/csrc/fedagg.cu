@@ -18,6 +18,8 @@
 // loads and no extra traffic. Algorithmic bytes: (4K + 16) N. The client loads
 // are issued in batches of KB before any f64 math, with KB x VEC chosen per tree
 // depth so that 128-256 B per thread are in flight: 73-82% of HBM for K = 8..64.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace fb {
@@ -413,7 +415,46 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
   return FB_OK;
 }
 
+// AggregatorState.weighted_sum (fedopt.py:95): sum_k n_k * (w - w_k) in arrival order, f64,
+// the reference's running accumulator itself (no division, no tree).
+template <typename TIn>
+__global__ void weighted_sum_kernel(AggParams<TIn> P, int K, const float* __restrict__ w, int64_t n,
+                                    double* __restrict__ out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    const double wg = (double)w[j];
+    double s = 0.0;
+    for (int k = 0; k < K; ++k) s = __dadd_rn(s, __dmul_rn(P.nk[k], delta_of<TIn>(P.src[k], j, wg)));
+    out[j] = s;
+  }
+}
+
+template <typename TIn>
+static int launch_weighted_sum(const void* const* src, const int64_t* n_k, int K, const float* w, int64_t n,
+                               double* out, cudaStream_t st) {
+  FB_REQUIRE(K >= 1 && K <= FB_MAX_CLIENTS, "n_clients=%d outside [1, %d]", K, FB_MAX_CLIENTS);
+  FB_REQUIRE(n > 0 && out && (w || sizeof(TIn) == 8), "weighted_sum: bad args");
+  AggParams<TIn> P;
+  P.nrep = 0;
+  for (int k = 0; k < K; ++k) {
+    FB_REQUIRE(src[k] != nullptr && n_k[k] >= 1, "client %d: null pointer or n_k < 1", k);
+    P.src[k] = reinterpret_cast<const TIn*>(src[k]);
+    P.nk[k] = (double)n_k[k];
+    P.pk[k] = 0.0;
+  }
+  const int64_t blocks = std::min<int64_t>((n + 255) / 256, kNumSMs * 8);
+  weighted_sum_kernel<TIn><<<(int)blocks, 256, 0, st>>>(P, K, w, n, out);
+  FB_LAUNCH_CHECK();
+  return FB_OK;
+}
+
 }  // namespace fb
+
+extern "C" int fb_fedagg_weighted_sum(const void* const* d_src, int src_is_f64_delta, const int64_t* n_k,
+                                      int n_clients, const float* d_w, int64_t n, double* d_out, void* stream) {
+  return src_is_f64_delta
+             ? fb::launch_weighted_sum<double>(d_src, n_k, n_clients, d_w, n, d_out, (cudaStream_t)stream)
+             : fb::launch_weighted_sum<float>(d_src, n_k, n_clients, d_w, n, d_out, (cudaStream_t)stream);
+}
 
 extern "C" int fb_fedagg_step_f32(const float* const* d_client_w, const int64_t* n_k, int n_clients,
                                   int deterministic, const float* d_w, const float* d_m, float* d_w_out,

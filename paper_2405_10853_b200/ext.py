@@ -40,6 +40,7 @@ SIGNATURES = {
     "fb_fedagg_round_norms_f32_peers": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _vp, _i, _i64, _d, _d, _i, _vp, _vp,
                                         _vp],
     "fb_fedagg_round_norms_f32": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _i64, _d, _d, _i, _vp, _vp, _vp],
+    "fb_fedagg_weighted_sum": [_vp, _i, _vp, _i, _vp, _i64, _vp, _vp],
     "fb_fedagg_step_f64delta": [_vp, _vp, _i, _i, _vp, _vp, _vp, _vp, _i64, _d, _d, _i, _vp, _vp, _vp, _vp],
     "fb_sumsq_partials": [_vp, _i64, _vp, _vp],
     "fb_sum_partials": [_vp, _i, _vp, _vp],

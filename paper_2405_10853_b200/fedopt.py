@@ -211,10 +211,23 @@ class AggregatorState:
 
     @property
     def weighted_sum(self) -> np.ndarray:
-        """sum_k n_k * delta_k (f64), as the reference keeps it."""
+        """sum_k n_k * delta_k (f64) in arrival order: bitwise the reference's running sum
+        (fedopt.py:95), evaluated on the device (fb_fedagg_weighted_sum)."""
         if not self._updates:
             return np.zeros(self.model_len)
-        return np.asarray(self._pg_device(raw_sum=True))
+        t = _torch()
+        ext.lib()
+        ups = list(self._updates)  # arrival order, whatever the finalize mode
+        dev = [u for u in ups if isinstance(u, DeviceClientUpdate)]
+        if len(dev) == len(ups) and len({u.w_start.data_ptr() for u in ups}) == 1:
+            srcs, f64, w = [u.w_end for u in ups], 0, ups[0].w_start
+        else:
+            srcs, f64, w = [t.from_numpy(u.delta).cuda() for u in ups], 1, None
+        out = t.empty(self.model_len, dtype=t.float64, device="cuda")
+        ext.call("fb_fedagg_weighted_sum", (C.c_void_p * len(srcs))(*[x.data_ptr() for x in srcs]), f64,
+                 (C.c_int64 * len(ups))(*[u.n_k for u in ups]), len(ups), ext.ptr(w), self.model_len,
+                 out.data_ptr(), ext.stream_handle())
+        return out.cpu().numpy()
 
     def weights(self) -> dict:
         if not self.contributors:
@@ -261,16 +274,13 @@ class AggregatorState:
                  ext.ptr(stats), ext.ptr(bad), ext.ptr(pg_out), ext.stream_handle())
         return srcs  # keep alive until the stream has consumed them
 
-    def _pg_device(self, raw_sum=False):
+    def _pg_device(self):
         t = _torch()
         ext.lib()
         pg = t.empty(self.model_len, dtype=t.float64, device="cuda")
         srcs = self._launch(None, None, None, None, 1.0, 0.0, False, pg_out=pg)
         t.cuda.current_stream().synchronize()
         del srcs
-        if raw_sum:
-            return (pg * float(self.total_weight)).cpu().numpy() if len(self._updates) > 1 else \
-                (pg * float(self._updates[0].n_k)).cpu().numpy()
         return pg
 
     def _materialize(self) -> np.ndarray:

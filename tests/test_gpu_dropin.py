@@ -58,6 +58,25 @@ def test_device_updates_bitwise():
     assert np.array_equal(opt2.momentum.data.view(np.uint32), g["k8_det_0.7_0.9_1_m"].view(np.uint32))
 
 
+@pytest.mark.parametrize("device_updates", [True, False])
+def test_weighted_sum_is_the_reference_running_sum(device_updates):
+    """AggregatorState.weighted_sum (fedopt.py:95): the f64 running sum of n_k * delta_k in
+    arrival order, bitwise — for device end weights and for host f64 deltas."""
+    f, P = api()
+    g = golden("agg.npz")
+    w, wk, nk, arr = g["k13_w"], g["k13_wk"], g["k13_nk"], g["k13_arrival"]
+    W = torch.from_numpy(w).cuda()
+    agg = f.AggregatorState(1, w.size, deterministic=True)
+    ref = np.zeros(w.size)
+    for k in arr:
+        delta = w.astype(np.float64) - wk[k].astype(np.float64)
+        ref += int(nk[k]) * delta
+        u = (f.DeviceClientUpdate(int(k), 1, int(nk[k]), torch.from_numpy(wk[k]).cuda(), W) if device_updates
+             else f.ClientUpdate(int(k), 1, int(nk[k]), delta))
+        agg.accumulate(u)
+    assert np.array_equal(agg.weighted_sum.view(np.uint64), ref.view(np.uint64))
+
+
 class TestReferenceAggregatorTests:
     def test_first_contribution(self):
         f, _ = api()
