@@ -311,7 +311,7 @@ def run_ours(args, cfgname):
     torch.cuda.empty_cache()
     # the product path for G > 1: one fused kernel over NVLink peer memory (dist.PeerAggregator)
     # replaces all-to-all + kernel + all-gather; the NCCL form above stays as the comparison
-    peer_ms, peer_err = None, None
+    peer_ms, peer_err, peer_pull = None, None, None
     if world > 1:
         try:
             from paper_2405_10853_b200.dist import PeerAggregator
@@ -331,7 +331,8 @@ def run_ours(args, cfgname):
             t = torch.tensor([x0.elapsed_time(x1) / reps], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             peer_ms = float(t.item())
-            agg_total_ms = min(agg_total_ms, peer_ms)
+            peer_pull = peer.pull
+            agg_total_ms = peer_ms  # the product path (federation.Federation picks PeerAggregator on NCCL)
             del peer
         except Exception as e:  # no peer mapping on this box: the NCCL form is the round's exchange
             peer_err = repr(e)[:200]
@@ -376,10 +377,14 @@ def run_ours(args, cfgname):
                   "agg_bytes_per_rank": agg_bytes,
                   "exchange_nccl_ms": round(nccl_total_ms, 3) if world > 1 else None,
                   "exchange_peer_fused_ms": round(peer_ms, 3) if peer_ms is not None else None,
-                  "exchange_note": ("G > 1: agg_exchange_ms is the faster of the NCCL form (all-to-all + kernel + "
-                                    "all-gather) and the single fused kernel over NVLink peer memory; both are "
-                                    "bit-identical to one GPU" + (f"; peer path unavailable: {peer_err}" if peer_err else ""))
-                  if world > 1 else None},
+                  "exchange_note": ("G > 1: agg_exchange_ms is the product path, the single fused kernel over NVLink "
+                                    f"peer memory (PeerAggregator, pull={peer_pull!r}, with the round-norm telemetry); "
+                                    "exchange_nccl_ms is the NCCL form (all-to-all + kernel + all-gather) for "
+                                    "comparison; both are bit-identical to one GPU"
+                                    + (f"; peer path unavailable, NCCL form used: {peer_err}" if peer_err else ""))
+                  if world > 1 else None,
+                  "nvlink": nvlink_record(N, Kc, world, len(mine), peer_ms if peer_ms is not None else nccl_total_ms,
+                                          "peer" if peer_ms is not None else "nccl") if world > 1 else None},
         "step_tensor": {"achieved_tflops": round(step_tflops, 1), "peak": tf_sus,
                         "frac": round(step_tflops / tf_sus, 3), "note": "whole local step, algorithmic FLOPs (SURVEY 8d) vs sustained bf16"},
         "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tc{,2}_kernel (tcgen05, all GEMM launches of the step)",
@@ -405,6 +410,23 @@ def run_ours(args, cfgname):
         emit(out)
     if world > 1:
         dist.destroy_process_group()
+
+
+def nvlink_record(N, K, G, k_local, ms, path):
+    """NVLink bytes per rank of the round-end exchange and the achieved rate vs 900 GB/s per
+    direction (NVLink 5 spec). peer: in = the remote clients' slices of this rank's shard,
+    out = the w' shard stored into the G-1 peer replicas plus the local clients' slices the
+    peers pull. nccl: all-to-all of client slices + all-gather of w'."""
+    shard = 4 * (N // G)
+    if path == "peer":
+        b_in = shard * (K - k_local)
+        b_out = shard * (G - 1) + shard * k_local * (G - 1)
+    else:
+        b_in = b_out = shard * k_local * (G - 1) + shard * (G - 1)
+    gbs = max(b_in, b_out) / (ms / 1e3) / 1e9
+    return {"path": path, "bytes_in_per_rank": b_in, "bytes_out_per_rank": b_out, "ms": round(ms, 3),
+            "gbs_per_rank_per_dir": round(gbs, 1), "peak_gbs": 900.0, "frac": round(gbs / 900.0, 3),
+            "note": "time includes the fused reduction + outer step + norms (the exchange is overlapped with it)"}
 
 
 def run_e2e(c, cfg, corpus, split, client, world, rank, K, barrier):
