@@ -484,23 +484,43 @@ def run_e2e(c, cfg, corpus, split, client, world, rank, K, barrier):
 
 
 # ------------------------------------------------------------------------------ CPU baseline
+def host_info():
+    """CPU model, logical cores and RAM of the box the CPU baseline ran on."""
+    model, mem_gb = None, None
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemTotal"):
+                    mem_gb = round(int(line.split()[1]) / 2**20, 1)
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "logical_cores": os.cpu_count(), "ram_gb": mem_gb}
+
+
 def cpu_baseline(c, budget_s=20.0, sample_tokens=None):
     """The reference's CPU path (oracle port: torch-CPU fp32 fwd/bwd + numpy f64
     optimizer, all host cores) on a bounded sample at the workload's exact shapes,
     extrapolated linearly to one local step:
-      fwd/bwd: a 1-layer and a 3-layer model at the exact width/vocab/context on
-      1 x `tokens` tokens -> per-layer and embedding/head cost -> L layers, per token;
+      fwd/bwd: a 1-layer and a 2-layer model at the exact width / vocab on ONE full-length
+      sequence (T tokens, so attention is timed at its true T x T cost) -> per-layer and
+      embedding/head cost -> L layers; a step is B x micro such sequences (exactly linear);
       optimizer: micro-accumulate / clip / AdamW / l2 on a 4M-param slice, per param."""
     import torch
     from oracle import localopt_ref, model_ref
     cores = os.cpu_count() or 1
     torch.set_num_threads(cores)
     V, d, L, H, T = c["V"], c["d"], c["L"], c["H"], c["T"]
-    tokens = min(sample_tokens or 128, T)
+    tokens = min(sample_tokens or T, T)
     rng = np.random.default_rng(0)
     batch = rng.integers(33, 97, size=(1, tokens))
     times = {}
-    for nl in (1, 3):  # one timed call each, after an untimed warm-up call
+    for nl in (1, 2):  # one timed call each, after an untimed warm-up call
         n = V * d + nl * (12 * d * d + 4 * d) + 2 * d + d * V
         w = np.asarray(rng.normal(0, 0.02, n), dtype=np.float32)
         model_ref.loss_and_grad(w, batch[:, :8], V, T, nl, d, H)  # warm-up: allocator + cached ALiBi buffer
@@ -508,11 +528,11 @@ def cpu_baseline(c, budget_s=20.0, sample_tokens=None):
         model_ref.loss_and_grad(w, batch, V, T, nl, d, H)
         times[nl] = time.perf_counter() - t0
         del w
-    # per-layer cost from the 1- vs 3-layer difference; floored by the layer's FLOP share of the
+    # per-layer cost from the 1- vs 2-layer difference; floored by the layer's FLOP share of the
     # 1-layer time so timing noise cannot make the extrapolation optimistic
     fl_layer = 24.0 * d * d + 4.0 * tokens * d
     fl_rest = 4.0 * V * d
-    per_layer = max((times[3] - times[1]) / 2, times[1] * fl_layer / (fl_layer + fl_rest))
+    per_layer = max(times[2] - times[1], times[1] * fl_layer / (fl_layer + fl_rest))
     base = max(times[1] - per_layer, 0.0)
     t_fb = base + L * per_layer
     n_s = 4_000_000
@@ -532,13 +552,15 @@ def cpu_baseline(c, budget_s=20.0, sample_tokens=None):
     localopt_ref.l2_norm(p2)
     t_opt = time.perf_counter() - t0
     N = n_params(c)
-    tokens_step = c["B"] * c["micro"] * T
-    step_s = t_fb / tokens * tokens_step + (c["micro"] * t_acc + t_opt) / n_s * N
+    seqs_step = c["B"] * c["micro"]
+    tokens_step = seqs_step * T
+    step_s = t_fb * seqs_step * (T / tokens) + (c["micro"] * t_acc + t_opt) / n_s * N
     return {"value": round(tokens_step / step_s, 3), "unit": "tokens/s", "cores": cores, "kind": "port",
-            "sample": f"oracle loss_and_grad on 1x{tokens} tokens with 1 and 3 layers at the exact d={d}/V={V}/"
-                      f"ctx={T} shape ({times[1]:.1f}s, {times[3]:.1f}s -> {L} layers) + accumulate/clip/AdamW on a "
-                      f"{n_s // 10**6}M-param slice ({t_acc + t_opt:.2f}s), extrapolated to one local step "
-                      f"({tokens_step} tokens, {N} params)"}
+            "host": host_info(),
+            "sample": f"oracle loss_and_grad on 1 sequence x {tokens} tokens with 1 and 2 layers at the exact "
+                      f"d={d}/V={V}/ctx={T} shape ({times[1]:.1f}s, {times[2]:.1f}s -> {L} layers) + "
+                      f"accumulate/clip/AdamW on a {n_s // 10**6}M-param slice ({t_acc + t_opt:.2f}s), extrapolated "
+                      f"to one local step ({seqs_step} sequences = {tokens_step} tokens, {N} params)"}
 
 
 def run_reference(args, cfgname):
