@@ -76,3 +76,27 @@ def test_async_checkpoint_of_device_vectors(tmp_path):
     assert raw == want
     dec = decode_sections(raw)
     assert dec["global"].bitwise_equal(ParamVector(w2.cpu().numpy())) and dec["round"] == 7
+
+
+def test_concurrent_clients_match_sequential():
+    """Federation(concurrent_clients=2): this GPU's clients train two at a time on their own
+    streams; with the deterministic kernels the round's global model is bitwise the
+    sequential one (same per-client computations, same fused round end)."""
+    from paper_2405_10853_b200.federation import Federation
+    from paper_2405_10853_b200.model import set_deterministic
+    cfg, corpus, split, adamw, sched = _c1()
+    kw = dict(batch_size=16, micro_batches=2, local_steps=3, server_eta=0.7, server_mu=0.9)
+    set_deterministic(True)
+    try:
+        outs = []
+        for P in (1, 2):
+            fed = Federation(cfg, adamw, sched, corpus, split, concurrent_clients=P, **kw)
+            w, opt = fed.init_state()
+            res = fed.run_round(w, opt, 1)
+            res = fed.run_round(res.params, res.opt, 2)
+            outs.append((res.params.tensor.cpu().numpy(), res.opt.momentum.tensor.cpu().numpy(), res.client_metrics))
+    finally:
+        set_deterministic(False)
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))
+    assert outs[0][2] == outs[1][2]
