@@ -127,7 +127,10 @@ enum fb_epilogue {
   FB_EPI_GELU = 4,       /* C(bf16) = gelu_erf(acc); aux_out(bf16) = acc (pre-activation) */
   FB_EPI_DGELU = 5,      /* C(bf16) = acc * gelu_erf'(aux(bf16)) */
   FB_EPI_RESID_F32_BF16 = 6, /* C(f32) = aux(f32) + acc and aux_out(bf16) = same */
-  FB_EPI_BF16_ROWDOT = 7     /* C(bf16) = acc and per-head row dots with aux: fb_gemm_bf16_rowdot only */
+  FB_EPI_BF16_ROWDOT = 7,    /* C(bf16) = acc and per-head row dots with aux: fb_gemm_bf16_rowdot only */
+  FB_EPI_CE_EXP = 8          /* LM head for fb_lmhead_ce: C(bf16) = exp(acc - m_c) per 32-column chunk c,
+                                aux_out(float2)[c * ld_aux + row] = (m_c, sum of the chunk's exps);
+                                K-major operands only */
 };
 /* 1 (default): use the 2-SM cta_group::2 256x256-tile kernel where the tile count fills the
  * 74 CTA pairs; 0: 1-SM kernels only (A/B comparison and tests) */
@@ -202,12 +205,18 @@ int fb_attn_bwd_ex(const void* d_qkv, const void* d_o, const void* d_do, const f
  * whose dQ partials are TMA reduce-added in arrival order. Every other kernel is
  * deterministic in both modes. Process-wide; 0 (default) = fastest. */
 int fb_set_deterministic(int enable);
-/* Mean next-token CE over B*(T-1) positions (model.py:226-229): logits f32 [rows][V]
- * for a chunk of rows [row0, row0+rows) of a B x T batch; writes dlogits(bf16) =
- * scale*(softmax - onehot) (0 on each sequence's last position) and adds the summed
- * loss of the chunk into d_loss_sum (f64). */
-int fb_ce_fwd_bwd(const float* d_logits, const int32_t* d_tok, void* d_dlogits, int row0,
-                  int rows, int T, int V, float scale, double* d_loss_sum, void* stream);
+/* Fused LM head + mean next-token cross-entropy (model.py:114, :150, :226-229) for
+ * rows [row0, row0 + rows) of a B x T batch: logits = x W^T on tcgen05 with the FB_EPI_CE_EXP
+ * epilogue (no f32 logits in HBM: bf16 e = exp(x - m_chunk) plus (m, sum) per 32-column chunk),
+ * then per row lse and loss = lse - x[target] (target logit recomputed in f32 from the same bf16
+ * operands; 0 on each sequence's last position, which is not scored) -> d_row_loss[row0 + r]
+ * (f64), and, when want_grad, dlogits(bf16) = scale * (softmax - onehot) written in place of e
+ * (the target entry from the f32 target logit). d_x: [rows][d] bf16; d_w: [V][d] bf16;
+ * d_work: fb_lmhead_ce_work_floats(rows, V) floats. V % 8 == 0, d % 8 == 0. */
+int64_t fb_lmhead_ce_work_floats(int rows, int V);
+int fb_lmhead_ce(const void* d_x, const void* d_w, const int32_t* d_tok, int row0, int rows, int T, int V, int d,
+                 float scale, int want_grad, void* d_dlogits, float* d_work, int64_t work_floats,
+                 double* d_row_loss, void* stream);
 
 /* ---- data feed: BatchIterator.next_batch on device (data.py:152-161) ----------------
  * rows = order[(cursor + i) mod n_order]; tok[i][t] = corpus[rows[i]*T + t] */

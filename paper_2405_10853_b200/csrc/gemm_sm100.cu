@@ -196,6 +196,27 @@ __device__ __forceinline__ float2 gelu_erf_grad2(float2 x) {
   return f2_fma(x, make_float2(ex2_approx(a.x), ex2_approx(a.y)), norm_cdf2(x, xx));
 }
 
+// FB_EPI_CE_EXP (LM head + cross-entropy, model.py:226-229): the 32 logits of this chunk
+// become e = exp(x - m) with m the chunk max (so e in (0, 1] keeps bf16 precision), and the
+// chunk's (m, sum e) pair goes to aux_out[(col / 32) * M + row] (a warp's 32 rows are
+// contiguous). The f32 logits never reach HBM; fb_lmhead_ce turns the pairs into the row's
+// log-sum-exp and rescales e into the gradient in place.
+__device__ __forceinline__ void ce_exp_chunk(const EpiArgs& e, int64_t row, bool in, int col, int N, float (&v)[32]) {
+  constexpr float kL2e = 1.4426950408889634f;
+  float m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) m = (col + i < N) ? fmaxf(m, v[i]) : m;
+  const float ml = m * kL2e;
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const float x = (col + i < N) ? ex2_approx(fmaf(v[i], kL2e, -ml)) : 0.f;
+    v[i] = x;
+    s += x;
+  }
+  if (in) reinterpret_cast<float2*>(e.aux_out)[(int64_t)(col >> 5) * e.ld_aux + row] = make_float2(m, s);
+}
+
 // Process 32 consecutive columns [col, col+32) of one row held in registers.
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int64_t row, int col, int N, const uint32_t (&r)[32]) {
@@ -203,7 +224,8 @@ __device__ __forceinline__ void epilogue_chunk(const EpiArgs& e, int64_t row, in
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
   const bool full = col + 32 <= N;
-  if constexpr (EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU) {
+  if constexpr (EPI == FB_EPI_CE_EXP) ce_exp_chunk(e, row, true, col, N, v);
+  if constexpr (EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU || EPI == FB_EPI_CE_EXP) {
     __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(e.C) + row * e.ldc + col;
     float o[32];
     if constexpr (EPI == FB_EPI_GELU) {
@@ -420,7 +442,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int tile, kb0, nkb;
       unit_coords(u, num_tiles, num_kb, ep.ksplit, tile, kb0, nkb);
       EpiArgs eu = ep;
-      eu.C = (char*)ep.C + (u / num_tiles) * ep.split_stride * (EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU ? 2 : 4);
+      eu.C = (char*)ep.C + (u / num_tiles) * ep.split_stride *
+                               (EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU || EPI == FB_EPI_CE_EXP ? 2 : 4);
       int mb, nb;
       tile_coords(tile, num_m, num_n, mb, nb);
       const int m0 = mb * BM;
@@ -519,6 +542,7 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& e, const EpiMa
       _Pragma("unroll") for (int i = 0; i < 32; ++i) if (col + i < N) v[i] += R[i];
     }
   }
+  if constexpr (EPI == FB_EPI_CE_EXP) ce_exp_chunk(e, row, in, col, N, v);
   uint32_t pre[16];  // GELU: bf16 pre-activation pairs (stored as aux_out; gelu sees the rounded value)
   if constexpr (EPI == FB_EPI_GELU) {
 #pragma unroll
@@ -577,7 +601,8 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& e, const EpiMa
   // ---- staging (the previous chunk's bulk store must have read the tile) ----
   if (lane == 0) bulk_wait_read<0>();
   __syncwarp();
-  constexpr bool kBf16Out = EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU || EPI == FB_EPI_BF16_ROWDOT;
+  constexpr bool kBf16Out = EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU || EPI == FB_EPI_BF16_ROWDOT ||
+                            EPI == FB_EPI_CE_EXP;
   if constexpr (kBf16Out) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) stg_put_bf16(stg, lane, j, v + 8 * j);
@@ -901,7 +926,8 @@ static int make_out_map(CUtensorMap* m, void* ptr, bool bf16, int M, int N, int6
 template <int A_MN, int B_MN, int EPI>
 static int launch_gemm2_t(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, const EpiArgs& ep,
                           cudaStream_t st) {
-  constexpr bool kBf16Out = EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU || EPI == FB_EPI_BF16_ROWDOT;
+  constexpr bool kBf16Out = EPI == FB_EPI_BF16 || EPI == FB_EPI_GELU || EPI == FB_EPI_DGELU || EPI == FB_EPI_BF16_ROWDOT ||
+                            EPI == FB_EPI_CE_EXP;
   EpiMaps maps;
   int rc = make_out_map(&maps.C, ep.C, kBf16Out, M, N, ep.ldc, ep.ksplit, ep.split_stride);
   if (rc) return rc;
@@ -945,6 +971,9 @@ static int dispatch_epi2(int epi, const CUtensorMap& ta, const CUtensorMap& tb, 
     case FB_EPI_DGELU: return launch_gemm2_t<A_MN, B_MN, FB_EPI_DGELU>(ta, tb, M, N, K, ep, st);
     case FB_EPI_RESID_F32_BF16: return launch_gemm2_t<A_MN, B_MN, FB_EPI_RESID_F32_BF16>(ta, tb, M, N, K, ep, st);
     case FB_EPI_BF16_ROWDOT: return launch_gemm2_t<A_MN, B_MN, FB_EPI_BF16_ROWDOT>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_CE_EXP:
+      if constexpr (A_MN == 0 && B_MN == 0) return launch_gemm2_t<0, 0, FB_EPI_CE_EXP>(ta, tb, M, N, K, ep, st);
+      break;
   }
   set_error("unknown epilogue %d", epi);
   return FB_BAD_ARG;
@@ -961,6 +990,9 @@ static int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, i
     case FB_EPI_GELU: return launch_gemm_t<BN, A_MN, B_MN, FB_EPI_GELU>(ta, tb, M, N, K, ep, st);
     case FB_EPI_DGELU: return launch_gemm_t<BN, A_MN, B_MN, FB_EPI_DGELU>(ta, tb, M, N, K, ep, st);
     case FB_EPI_RESID_F32_BF16: return launch_gemm_t<BN, A_MN, B_MN, FB_EPI_RESID_F32_BF16>(ta, tb, M, N, K, ep, st);
+    case FB_EPI_CE_EXP:
+      if constexpr (A_MN == 0 && B_MN == 0) return launch_gemm_t<BN, 0, 0, FB_EPI_CE_EXP>(ta, tb, M, N, K, ep, st);
+      break;
   }
   set_error("unknown epilogue %d", epi);
   return FB_BAD_ARG;
@@ -987,10 +1019,12 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   FB_REQUIRE(lda % 8 == 0 && ldb % 8 == 0, "gemm: lda/ldb must be multiples of 8 elements");
   FB_REQUIRE(ldc % 8 == 0, "gemm: ldc must be a multiple of 8 elements");
   const bool need_aux = epilogue == FB_EPI_RESID_F32 || epilogue == FB_EPI_DGELU || epilogue == FB_EPI_RESID_F32_BF16;
-  const bool need_aux_out = epilogue == FB_EPI_GELU || epilogue == FB_EPI_RESID_F32_BF16;
+  const bool need_aux_out = epilogue == FB_EPI_GELU || epilogue == FB_EPI_RESID_F32_BF16 || epilogue == FB_EPI_CE_EXP;
+  FB_REQUIRE(epilogue != FB_EPI_CE_EXP || (a_major == 0 && b_major == 0 && ld_aux >= M),
+             "gemm: the CE epilogue needs K-major operands and ld_aux >= M (stats row stride)");
   FB_REQUIRE(!need_aux || d_aux, "gemm: epilogue %d needs aux", epilogue);
   FB_REQUIRE(!need_aux_out || d_aux_out, "gemm: epilogue %d needs aux_out", epilogue);
-  FB_REQUIRE(!need_aux_out || ((uintptr_t)d_aux_out % 16 == 0 && (epilogue != FB_EPI_GELU || ld_aux % 8 == 0)),
+  FB_REQUIRE(!need_aux_out || ((uintptr_t)d_aux_out % 8 == 0 && (epilogue != FB_EPI_GELU || ld_aux % 8 == 0)),
              "gemm: aux_out must be 16-byte aligned with ld_aux %% 8 == 0");
   int rc = get_encoder();
   if (rc) return rc;

@@ -73,7 +73,7 @@ constexpr int64_t kSplitKFloats = 16ll << 20;
 
 struct WS {
   std::vector<Acts> L;
-  float *x_out, *meanf, *rstdf, *logits, *dx, *dln, *attn_work, *ln_work, *splitk;
+  float *x_out, *meanf, *rstdf, *ce_work, *dx, *dln, *attn_work, *ln_work, *splitk;
   __nv_bfloat16 *lnf, *dlogits, *dxb, *dao, *dqkv, *dfc;
   uint8_t* emb_work;  // sorted-token embedding backward (fb_embed_bwd_sorted)
   int64_t emb_work_bytes;
@@ -106,7 +106,7 @@ static WS carve(const fb_model_cfg& c, int B, int T, Arena& A) {
   w.rstdf = A.take<float>(M);
   w.lnf = A.take<__nv_bfloat16>(M * d);
   w.chunk = (int)std::min<int64_t>(M, 8192);
-  w.logits = A.take<float>((int64_t)w.chunk * V);
+  w.ce_work = A.take<float>(fb_lmhead_ce_work_floats(w.chunk, (int)V));  // chunk (max, sum) pairs + lse
   w.dlogits = A.take<__nv_bfloat16>((int64_t)w.chunk * V);
   w.dx = A.take<float>(M * d);
   w.dxb = A.take<__nv_bfloat16>(M * d);
@@ -199,12 +199,11 @@ extern "C" int fb_model_fwd_bwd(const fb_model_cfg* cfgp, const float* P, const 
                      nullptr, d, st));
   }
   TRY(fb_ln_fwd(w.x_out, P + Lo.lnf_w, P + Lo.lnf_b, w.lnf, w.meanf, w.rstdf, M, d, st));
-  // LM head + CE (+ head backward) in row chunks so logits stay L2-friendly
+  // LM head + CE fused (no f32 logits): dlogits(bf16) of each row chunk, then the head backward
   for (int r0 = 0; r0 < M; r0 += w.chunk) {
     const int rows = std::min(w.chunk, M - r0);
-    TRY(fb_gemm_bf16(rows, V, d, w.lnf + (int64_t)r0 * d, d, 0, S + Lo.head, d, 0, w.logits, V, FB_EPI_F32, nullptr,
-                     nullptr, 0, st));
-    TRY(fb_ce_fwd_bwd(w.logits, tok, w.dlogits, r0, rows, T, V, grad_scale, row_loss, st));
+    TRY(fb_lmhead_ce(w.lnf + (int64_t)r0 * d, S + Lo.head, tok, r0, rows, T, V, d, grad_scale, want_grad, w.dlogits,
+                     w.ce_work, fb_lmhead_ce_work_floats(w.chunk, V), row_loss, st));
     if (want_grad) {
       // d(lnf) = dlogits . W_head ; dW_head += dlogits^T . lnf
       TRY(fb_gemm_bf16_splitk(rows, d, V, w.dlogits, V, 0, S + Lo.head, d, 1, w.dln + (int64_t)r0 * d, d,

@@ -1,17 +1,18 @@
 // Non-GEMM transformer pieces of the reference TinyLM (fedforge/model.py):
 //   embedding gather / scatter-add      model.py:109, :145 (+ pos_embed :111, :147)
 //   LayerNorm eps=1e-5 fwd / bwd        model.py:81, :84, :113 (applied :90, :100, :150)
-//   mean next-token cross-entropy       model.py:226-229  (logits[:, :-1] vs tokens[:, 1:])
+//   LM head + mean next-token CE       model.py:114, :150, :226-229 (logits[:, :-1] vs tokens[:, 1:])
 //
 // B200 design: all row kernels are one warp per row with coalesced 32-lane
 // strides (HBM-bound; the fp32 residual stream is read once per kernel). LN
 // keeps the row in registers for a two-pass mean/variance (same formula torch
 // uses), writes the bf16 GEMM operand and saves mean/rstd for the backward.
 // dgamma/dbeta use per-CTA partial rows plus a fixed-order second pass, so they
-// are deterministic. CE reads each f32 logits row twice (max/sum pass, then the
-// softmax-minus-onehot pass) while it is L2-resident and writes bf16 dlogits for
-// the head dgrad/wgrad GEMMs; per-row losses go to a buffer that is reduced in
-// fixed order (no float atomics).
+// are deterministic. The cross-entropy is fused with the LM head (fb_lmhead_ce): the
+// head GEMM's epilogue writes bf16 exp(x - chunk max) and per-chunk (max, sum) pairs, so
+// no f32 logits tensor exists; two light kernels turn the pairs into the row lse / loss
+// (per-row losses to a buffer reduced in fixed order, no float atomics) and rescale the
+// exps in place into bf16 dlogits for the head dgrad/wgrad GEMMs.
 #include <algorithm>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -397,81 +398,120 @@ __global__ void __launch_bounds__(256) ln_bwd_reduce_kernel(const float* __restr
 constexpr int kLnBwdBlocks = 592;  // 148 SMs x 4
 
 // ------------------------------------------------------------------ cross-entropy
-// One CTA (256 threads) per logits row. Row r of the chunk is position t = (row0+r) % T.
-// Pass 1: online max / sum-exp with 128-bit loads; pass 2 (row is L2-resident): bf16 dlogits.
-__global__ void __launch_bounds__(256) ce_kernel(const float* __restrict__ logits, const int32_t* __restrict__ tok,
-                                                 __nv_bfloat16* __restrict__ dlogits, int row0, int T, int V,
-                                                 float scale, double* __restrict__ row_loss) {
-  __shared__ float red_m[8], red_s[8];
+// After the head GEMM's FB_EPI_CE_EXP epilogue: stats[c][r] = (m_c, s_c) per 32-column chunk c
+// of row r, e[r][col] = bf16(exp(x - m_c)).
+// ce_lse_kernel: 32 rows per CTA, lane = row; the 8 warps split the chunks (coalesced: the 32
+// rows of a chunk are contiguous), then warp 0 merges the 8 partial (max, sum) pairs. The
+// target logit is a warp dot product of the same bf16 operands in f32.
+constexpr float kCeL2e = 1.4426950408889634f;
+
+__global__ void __launch_bounds__(256) ce_lse_kernel(const float2* __restrict__ stats, int nch, int rows,
+                                                     const __nv_bfloat16* __restrict__ x,
+                                                     const __nv_bfloat16* __restrict__ w, int d,
+                                                     const int32_t* __restrict__ tok, int row0, int T,
+                                                     float* __restrict__ lse_out, float* __restrict__ xt_out,
+                                                     double* __restrict__ row_loss) {
+  __shared__ float pm[8][32], ps[8][32], sl[32], sx[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int r = blockIdx.x * 32 + lane;
+  auto merge = [](float& m, float& s, float2 ms) {
+    if (ms.x > m) {
+      s = s * exp2f((m - ms.x) * kCeL2e) + ms.y;
+      m = ms.x;
+    } else {
+      s += ms.y * exp2f((ms.x - m) * kCeL2e);
+    }
+  };
+  float m = -INFINITY, s = 0.f;
+  if (r < rows) {
+    // four independent (max, sum) streams keep four loads in flight per thread
+    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, s4[4] = {0.f, 0.f, 0.f, 0.f};
+    int c = wid;
+    for (; c + 24 < nch; c += 32) {
+      float2 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = stats[(int64_t)(c + 8 * u) * rows + r];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) merge(m4[u], s4[u], v[u]);
+    }
+    for (; c < nch; c += 8) merge(m4[0], s4[0], stats[(int64_t)c * rows + r]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (m4[u] != -INFINITY) merge(m, s, make_float2(m4[u], s4[u]));
+  }
+  pm[wid][lane] = m;
+  ps[wid][lane] = s;
+  __syncthreads();
+  if (wid == 0) {
+    float mm = pm[0][lane];
+    for (int i = 1; i < 8; ++i) mm = fmaxf(mm, pm[i][lane]);
+    float ss = 0.f;
+    for (int i = 0; i < 8; ++i) ss += (pm[i][lane] == -INFINITY) ? 0.f : ps[i][lane] * exp2f((pm[i][lane] - mm) * kCeL2e);
+    sl[lane] = mm + logf(ss);
+  }
+  // target logits: warp w handles rows 4w .. 4w+3 of this block
+  for (int k = 0; k < 4; ++k) {
+    const int rr = wid * 4 + k, row = blockIdx.x * 32 + rr;
+    float acc = 0.f;
+    const int grow = row0 + row;
+    const bool scored = row < rows && (grow % T) != T - 1;
+    if (scored) {
+      const int target = tok[grow + 1];
+      const __nv_bfloat16* xr = x + (int64_t)row * d;
+      const __nv_bfloat16* wr = w + (int64_t)target * d;
+      for (int c = 2 * lane; c < d; c += 64) {
+        const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(xr + c));
+        const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(wr + c));
+        acc = fmaf(a.x, b.x, acc);
+        acc = fmaf(a.y, b.y, acc);
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) sx[rr] = acc;
+  }
+  __syncthreads();
+  if (wid == 0 && r < rows) {
+    const int grow = row0 + r;
+    const bool scored = (grow % T) != T - 1;
+    lse_out[r] = sl[lane];
+    xt_out[r] = sx[lane];
+    row_loss[grow] = scored ? (double)(sl[lane] - sx[lane]) : 0.0;
+  }
+}
+
+// dlogits = scale * (e * exp(m_c - lse) - onehot), in place over e. One CTA per row (row
+// scalars loaded once, no 64-bit index division), 8 columns per thread per step.
+// The target entry uses the f32 target logit (softmax near 1 would lose the (p - 1) to
+// cancellation on the bf16 e); a sequence's last position gets 0 (not scored).
+__global__ void __launch_bounds__(256) ce_grad_kernel(const float2* __restrict__ stats, int rows, int V,
+                                                      const float* __restrict__ lse, const float* __restrict__ xt,
+                                                      const int32_t* __restrict__ tok, int row0, int T, float scale,
+                                                      __nv_bfloat16* __restrict__ e) {
   const int r = blockIdx.x;
   const int grow = row0 + r;
-  const int t = grow % T;
-  const float* lr = logits + (int64_t)r * V;
-  __nv_bfloat16* dr = dlogits + (int64_t)r * V;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const bool vec = (V % 8 == 0);
-  if (t == T - 1) {  // last position: not scored (logits[:, :-1])
-    if (vec) {
-      for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) *reinterpret_cast<uint4*>(dr + c) = make_uint4(0, 0, 0, 0);
-    } else {
-      for (int c = threadIdx.x; c < V; c += blockDim.x) dr[c] = __float2bfloat16_rn(0.f);
-    }
-    if (threadIdx.x == 0) row_loss[grow] = 0.0;
+  uint4* p = reinterpret_cast<uint4*>(e + (int64_t)r * V);
+  const int nv = V / 8;
+  if ((grow % T) == T - 1) {
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) p[i] = make_uint4(0u, 0u, 0u, 0u);
     return;
   }
+  const float L = lse[r] * kCeL2e;
   const int target = tok[grow + 1];
-  float m = -INFINITY, s = 0.f;
-  auto upd = [&](float x) {
-    if (x > m) { s = s * __expf(m - x) + 1.f; m = x; }
-    else s += __expf(x - m);
-  };
-  if (vec) {
-    for (int c = threadIdx.x * 4; c < V; c += blockDim.x * 4) {
-      const float4 a = *reinterpret_cast<const float4*>(lr + c);
-      upd(a.x); upd(a.y); upd(a.z); upd(a.w);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+    const int col = 8 * i;
+    const float f = exp2f(fmaf(stats[(int64_t)(col >> 5) * rows + r].x, kCeL2e, -L)) * scale;
+    uint4 v = p[i];
+    __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+    float o[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 a = __bfloat1622float2(h[k]);
+      o[2 * k] = a.x * f;
+      o[2 * k + 1] = a.y * f;
     }
-  } else {
-    for (int c = threadIdx.x; c < V; c += blockDim.x) upd(lr[c]);
+    if (target >= col && target < col + 8) o[target - col] = (exp2f(fmaf(xt[r], kCeL2e, -L)) - 1.0f) * scale;
+    p[i] = make_uint4(pack_bf16(o[0], o[1]), pack_bf16(o[2], o[3]), pack_bf16(o[4], o[5]), pack_bf16(o[6], o[7]));
   }
-  // combine (m, s) pairs: warp then CTA
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
-    const float mn = fmaxf(m, m2);
-    s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
-    m = mn;
-  }
-  if (lane == 0) { red_m[wid] = m; red_s[wid] = s; }
-  __syncthreads();
-  float mx = red_m[0];
-#pragma unroll
-  for (int i = 1; i < 8; ++i) mx = fmaxf(mx, red_m[i]);
-  float sum = 0.f;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) sum += red_s[i] * __expf(red_m[i] - mx);
-  const float lse = mx + logf(sum);
-  const float inv = 1.0f / sum;
-  if (vec) {
-    for (int c = threadIdx.x * 8; c < V; c += blockDim.x * 8) {
-      const float4 a = *reinterpret_cast<const float4*>(lr + c), b = *reinterpret_cast<const float4*>(lr + c + 4);
-      float p[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        p[i] = __expf(p[i] - mx) * inv;
-        if (c + i == target) p[i] -= 1.0f;
-        p[i] *= scale;
-      }
-      *reinterpret_cast<uint4*>(dr + c) = make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]),
-                                                     pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
-    }
-  } else {
-    for (int c = threadIdx.x; c < V; c += blockDim.x) {
-      float p = __expf(lr[c] - mx) * inv;
-      if (c == target) p -= 1.0f;
-      dr[c] = __float2bfloat16_rn(p * scale);
-    }
-  }
-  if (threadIdx.x == 0) row_loss[grow] = (double)(lse - lr[target]);
 }
 
 }  // namespace fb
@@ -585,11 +625,34 @@ extern "C" int fb_ln_bwd(const float* d_x, const float* d_gamma, const float* d_
   return FB_OK;
 }
 
-extern "C" int fb_ce_fwd_bwd(const float* d_logits, const int32_t* d_tok, void* d_dlogits, int row0, int rows, int T,
-                             int V, float scale, double* d_row_loss, void* stream) {
-  FB_REQUIRE(rows > 0 && T >= 2 && V > 0 && row0 >= 0, "ce: bad shape");
-  ce_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(d_logits, d_tok, (__nv_bfloat16*)d_dlogits, row0, T, V, scale,
-                                                     d_row_loss);
+extern "C" int fb_gemm_bf16(int, int, int, const void*, int64_t, int, const void*, int64_t, int, void*, int64_t, int,
+                            const void*, void*, int64_t, void*);
+
+extern "C" int64_t fb_lmhead_ce_work_floats(int rows, int V) {
+  if (rows <= 0 || V <= 0) return 0;
+  return 2 * (int64_t)((V + 31) / 32) * rows + 2 * (int64_t)rows;
+}
+
+extern "C" int fb_lmhead_ce(const void* d_x, const void* d_w, const int32_t* d_tok, int row0, int rows, int T, int V,
+                            int d, float scale, int want_grad, void* d_dlogits, float* d_work, int64_t work_floats,
+                            double* d_row_loss, void* stream) {
+  FB_REQUIRE(rows > 0 && T >= 2 && V > 0 && d > 0 && row0 >= 0, "lmhead_ce: bad shape");
+  FB_REQUIRE(V % 8 == 0 && d % 8 == 0, "lmhead_ce: V and d must be multiples of 8 (V=%d d=%d)", V, d);
+  FB_REQUIRE(d_work && work_floats >= fb_lmhead_ce_work_floats(rows, V), "lmhead_ce: work buffer too small");
+  FB_REQUIRE((uintptr_t)d_work % 16 == 0 && (uintptr_t)d_dlogits % 16 == 0, "lmhead_ce: buffers must be 16-byte aligned");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int nch = (V + 31) / 32;
+  float2* stats = reinterpret_cast<float2*>(d_work);
+  float* lse = d_work + 2 * (int64_t)nch * rows;
+  float* xt = lse + rows;
+  int rc = fb_gemm_bf16(rows, V, d, d_x, d, 0, d_w, d, 0, d_dlogits, V, FB_EPI_CE_EXP, nullptr, stats, rows, stream);
+  if (rc) return rc;
+  ce_lse_kernel<<<(rows + 31) / 32, 256, 0, st>>>(stats, nch, rows, (const __nv_bfloat16*)d_x,
+                                                 (const __nv_bfloat16*)d_w, d, d_tok, row0, T, lse, xt, d_row_loss);
   FB_LAUNCH_CHECK();
+  if (want_grad) {
+    ce_grad_kernel<<<rows, 256, 0, st>>>(stats, rows, V, lse, xt, d_tok, row0, T, scale, (__nv_bfloat16*)d_dlogits);
+    FB_LAUNCH_CHECK();
+  }
   return FB_OK;
 }

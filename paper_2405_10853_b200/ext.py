@@ -17,7 +17,8 @@ FB_OK, FB_BAD_ARG, FB_CUDA_ERROR, FB_NONFINITE, FB_UNSUPPORTED = 0, 1, 2, 3, 4
 FB_RED_BLOCKS = 1184
 FB_MAX_CLIENTS = 64
 
-EPI = {"bf16": 0, "f32": 1, "acc_f32": 2, "resid_f32": 3, "gelu": 4, "dgelu": 5, "resid_f32_bf16": 6, "bf16_rowdot": 7}
+EPI = {"bf16": 0, "f32": 1, "acc_f32": 2, "resid_f32": 3, "gelu": 4, "dgelu": 5, "resid_f32_bf16": 6, "bf16_rowdot": 7,
+       "ce_exp": 8}
 
 _vp, _i, _i64, _d = C.c_void_p, C.c_int, C.c_int64, C.c_double
 
@@ -59,7 +60,7 @@ SIGNATURES = {
     "fb_attn_bwd": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _vp],
     "fb_attn_bwd_ex": [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _i, _i, _i, _i, _i, _i, _vp],
     "fb_gemm_bf16_rowdot": [_i, _i, _i, _vp, _i64, _i, _vp, _i64, _i, _vp, _i64, _vp, _i64, _vp, _i, _i, _vp],
-    "fb_ce_fwd_bwd": [_vp, _vp, _vp, _i, _i, _i, _i, C.c_float, _vp, _vp],
+    "fb_lmhead_ce": [_vp, _vp, _vp, _i, _i, _i, _i, _i, C.c_float, _i, _vp, _vp, _i64, _vp, _vp],
     "fb_gather_batch": [_vp, _vp, _i64, _i64, _i, _i, _vp, _vp],
     "fb_profile_begin": [_i],
     "fb_gemm_set_2sm": [_i],
@@ -108,6 +109,8 @@ def lib(require_device: bool = True):
             L.fb_model_workspace_bytes.restype = C.c_int64
             L.fb_embed_bwd_work_bytes.argtypes = [_i, _i]
             L.fb_embed_bwd_work_bytes.restype = C.c_int64
+            L.fb_lmhead_ce_work_floats.argtypes = [_i, _i]
+            L.fb_lmhead_ce_work_floats.restype = C.c_int64
             L.fb_last_error.argtypes = []
             L.fb_last_error.restype = C.c_char_p
             _lib = L
