@@ -207,43 +207,82 @@ def run_ours(args, cfgname):
     sched = ScheduleConfig(*c["sched"])
     adamw = AdamWConfig()
     W, K = args.warmup, args.steps
+    P = max(1, args.concurrent)  # clients trained concurrently on this GPU (own stream + evaluator each)
     task = TrainTask(1, client, W + K, 0, c["B"], c["micro"], {"data": 99}, "bench")
     sess = ClientSession(ev, it, adamw, sched).begin(w0, task)
     tokens_step = c["B"] * c["micro"] * c["T"]
+    extra = []  # (session, stream) of the concurrent clients beyond the first
+    for i in range(1, P):
+        k2 = (client + world * i) % c["K"]
+        st_i = torch.cuda.Stream()
+        with torch.cuda.stream(st_i):
+            it_i = data.BatchIterator(corpus, split.shards[k2], c["B"], 99)
+            s_i = ClientSession(LossEvaluator(cfg), it_i, adamw, sched).begin(
+                w0, TrainTask(1, k2, W + K, 0, c["B"], c["micro"], {"data": 99}, "bench"))
+        extra.append((s_i, st_i))
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    for s in range(W):
-        sess.step(s)
+    def run_steps(lo, hi):
+        """Steps [lo, hi) of every client: the first on the current stream, the others on their
+        own streams from their own host threads (ctypes releases the GIL)."""
+        if not extra:
+            for s in range(lo, hi):
+                sess.step(s)
+            return
+        main = torch.cuda.current_stream()
+
+        def worker(si, sti):
+            with torch.cuda.stream(sti):
+                if sti is not main:
+                    sti.wait_stream(main)
+                for s in range(lo, hi):
+                    si.step(s)
+
+        # every client (the first too, on the main stream) runs in its own thread; the main thread only joins
+        ths = [threading.Thread(target=worker, args=x) for x in [(sess, main)] + extra]
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        for _, sti in extra:
+            main.wait_stream(sti)
+
+    run_steps(0, W)
     torch.cuda.synchronize()
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ext.check(ext.lib().fb_profile_begin(20000), "profile")
+    if not extra:  # the live per-launch profiler is single-stream
+        ext.check(ext.lib().fb_profile_begin(20000), "profile")
     torch.cuda.synchronize()
     barrier()
     e0.record(st)
-    for s in range(W, W + K):
-        sess.step(s)
+    run_steps(W, W + K)
     e1.record(st)
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
     prof = (C.c_double * 12)()
-    ext.check(ext.lib().fb_profile_end(prof), "profile")
+    if not extra:
+        ext.check(ext.lib().fb_profile_end(prof), "profile")
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     upd, tele = sess.finish()
+    for s_i, st_i in extra:
+        with torch.cuda.stream(st_i):
+            s_i.finish()
+    extra.clear()
     losses = [x.loss for x in tele]
     ms_step = ms / K
-    value = world * tokens_step / (ms_step / 1e3)
+    value = world * P * tokens_step / (ms_step / 1e3)
 
     # ---------------- round-end aggregation: K clients x N params ----------------
     del sess, ev
@@ -345,11 +384,11 @@ def run_ours(args, cfgname):
     # ---------------- compose ----------------
     traffic, traffic_alg, traffic_kernel = ncu_traffic()
     clients_per_gpu = math.ceil(Kc / world)
-    round_s = clients_per_gpu * c["S"] * ms_step / 1e3 + agg_total_ms / 1e3
+    round_s = math.ceil(clients_per_gpu / P) * c["S"] * ms_step / 1e3 + agg_total_ms / 1e3
     round_tokens = Kc * c["S"] * tokens_step
     gemm_avg_ms = gemm_ms / max(gemm_n, 1)
     gemm_tflops = gemm_fl / max(gemm_ms, 1e-9) / 1e9
-    step_tflops = flops_per_token(c) * tokens_step / (ms_step / 1e3) / 1e12
+    step_tflops = flops_per_token(c) * P * tokens_step / (ms_step / 1e3) / 1e12
     out = {
         "metric": METRIC,
         "value": round(value, 1),
@@ -365,7 +404,9 @@ def run_ours(args, cfgname):
         "data": "synthetic (reference Markov corpus seed 99, 32 MB; seeded reference init)",
         "config": {"workload": f"{cfgname}: {c['label']}", "params": N, "tokens_per_step_per_gpu": tokens_step,
                    "global_batch_seqs": c["B"] * c["micro"], "seq_len": c["T"], "clients": Kc,
-                   "clients_per_gpu": clients_per_gpu, "parallelism": f"clients sharded over {world} GPU(s)",
+                   "clients_per_gpu": clients_per_gpu, "concurrent_clients_per_gpu": P,
+                   "parallelism": f"clients sharded over {world} GPU(s)" + (f", {P} trained concurrently per GPU"
+                                                                          if P > 1 else ""),
                    "l2": "inputs > L2 (126 MB): every step streams 5.4 GB params/state and GB-scale activations"},
         "gpu_launches": None,
         "loss": [round(x, 4) for x in losses[-K:]],
@@ -402,8 +443,14 @@ def run_ours(args, cfgname):
         "clocks": clk,
         "e2e": e2e,
     }
+    if P > 1:  # the per-launch profiler is single-stream: report the whole step against the tensor roofline
+        out["roofline"] = {"bound": "tensor", "kernel": f"whole local step of {P} concurrent clients",
+                           "achieved": round(step_tflops, 1), "peak": tf_sus, "unit": "TFLOP/s",
+                           "frac": round(step_tflops / tf_sus, 3), "traffic": None,
+                           "peak_note": "sustained bf16; per-kernel timing is off with concurrent clients"}
+        out["attention"] = None
     # GPU launches of our kernels inside the timed region (per step, counted from the runtime's schedule)
-    out["gpu_launches"] = launches_per_step(c) * K
+    out["gpu_launches"] = launches_per_step(c) * K * P
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(c, args.cpu_budget)
     if rank == 0:
@@ -619,6 +666,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--concurrent", type=int, default=1,
+                    help="clients trained concurrently per GPU (own stream + evaluator each; small configs)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     with _StdoutToStderr():
