@@ -59,9 +59,12 @@ def n_params(c):
 
 def ncu_traffic():
     """DRAM bytes per launch of the dominant kernel from the committed `ncu --set full` capture
-    (profiles/r01_ncu_summary.json, tcgen05 2-SM GEMM, C4 qkv fwd: M=16384 N=6144 K=2048, bf16 out)."""
+    (profiles/r02_ncu_summary.json, tcgen05 2-SM GEMM, C4 qkv fwd: M=16384 N=6144 K=2048, bf16 out)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_summary.json")) as fh:
+        path = os.path.join(ROOT, "profiles", "r02_ncu_summary.json")
+        if not os.path.exists(path):
+            path = os.path.join(ROOT, "profiles", "r01_ncu_summary.json")
+        with open(path) as fh:
             s = json.load(fh)
         for k, v in s.items():
             if k.startswith("gemmqkv:"):

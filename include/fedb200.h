@@ -166,9 +166,10 @@ int fb_embed_fwd(const int32_t* d_tok, const float* d_emb, const float* d_pos, f
 int fb_embed_bwd(const int32_t* d_tok, const float* d_dx, float* d_gemb, float* d_gpos,
                  int n_tok, int T, int d, int vocab, void* stream);
 /* Deterministic embedding backward (model.py:109 / :145 grads): token ids are
- * stably radix-sorted with their positions, each run of equal ids is summed in ascending
- * position order by one owner and added once; positions are summed in ascending batch
- * row. Bitwise reproducible. d_work: fb_embed_bwd_work_bytes(n_tok, vocab) bytes. */
+ * stably radix-sorted with their positions; a run of equal ids is cut into 8 contiguous
+ * ranges of ascending positions, each summed in order, the range sums added in order and
+ * once into gemb (one thread per column when d % 8 != 0); positions are summed in ascending
+ * batch row. Bitwise reproducible. d_work: fb_embed_bwd_work_bytes(n_tok, vocab) bytes. */
 int64_t fb_embed_bwd_work_bytes(int n_tok, int vocab);
 int fb_embed_bwd_sorted(const int32_t* d_tok, const float* d_dx, float* d_gemb, float* d_gpos,
                         int n_tok, int T, int d, int vocab, void* d_work, int64_t work_bytes,

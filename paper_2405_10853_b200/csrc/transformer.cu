@@ -16,6 +16,7 @@
 #include <algorithm>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "common.cuh"
 
@@ -51,51 +52,101 @@ __global__ void embed_bwd_kernel(const int32_t* __restrict__ tok, const float* _
 // Deterministic embedding backward (the atomics above add rows in arrival order, so the
 // f32 sums differ run to run): the token ids are stably sorted with their positions
 // (CUB radix sort, keys = ids), then each run of equal ids is owned by one CTA per column
-// block, which sums its dx rows in ascending position order and adds once into gemb.
+// block, which sums its dx rows in a fixed order (below) and adds once into gemb.
 __global__ void iota_kernel(int32_t* __restrict__ v, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
 }
 
-constexpr int kEmbCols = 256;  // columns per CTA (64 threads x float4, or 256 scalar)
+constexpr int kEmbCols = 256;  // columns per work item
 
-__global__ void __launch_bounds__(64) embed_bwd_runs_kernel(const int32_t* __restrict__ skey,
-                                                            const int32_t* __restrict__ spos,
-                                                            const float* __restrict__ dx, float* __restrict__ gemb,
-                                                            int n_tok, int d) {
-  const int i0 = blockIdx.x;
-  const int v = skey[i0];
-  if (i0 > 0 && skey[i0 - 1] == v) return;  // not the head of a run
-  int i1 = i0 + 1;
-  while (i1 < n_tok && skey[i1] == v) ++i1;
-  const int c0 = blockIdx.y * kEmbCols;
-  float* out = gemb + (int64_t)v * d;
-  if ((d & 3) == 0) {
-    const int c = c0 + 4 * threadIdx.x;
-    if (c >= d) return;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    int i = i0;
-    for (; i + 4 <= i1; i += 4) {  // four rows in flight, summed in order
-      float4 r[4];
+// run boundaries of the sorted ids: flags[i] = 1 at the head of each run of equal ids
+__global__ void run_flags_kernel(const int32_t* __restrict__ skey, int n, int32_t* __restrict__ flags) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    flags[i] = (i == 0 || skey[i] != skey[i - 1]) ? 1 : 0;
+}
+// run_idx = inclusive scan of flags (1-based run number): starts[run] = head position,
+// starts[n_runs] = n, nruns[0] = n_runs
+__global__ void run_bounds_kernel(const int32_t* __restrict__ flags, const int32_t* __restrict__ run_idx, int n,
+                                  int32_t* __restrict__ starts, int32_t* __restrict__ nruns) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (flags[i]) starts[run_idx[i] - 1] = i;
+    if (i == n - 1) {
+      starts[run_idx[i]] = n;
+      nruns[0] = run_idx[i];
+    }
+  }
+}
+
+// Persistent CTAs (8 warps) over (run, 256-column block) work items. The run's rows are split
+// into 8 contiguous ranges; warp w sums range w in ascending position order (lane = 8 columns,
+// 8 rows in flight), then the range sums are added in range order and once into gemb. Fixed
+// order for a given token sequence: bitwise reproducible. d % 8 == 0.
+__global__ void __launch_bounds__(256) embed_bwd_runs_kernel(const int32_t* __restrict__ skey,
+                                                             const int32_t* __restrict__ spos,
+                                                             const int32_t* __restrict__ starts,
+                                                             const int32_t* __restrict__ nruns,
+                                                             const float* __restrict__ dx, float* __restrict__ gemb,
+                                                             int d) {
+  __shared__ float part[8][kEmbCols];
+  const int ncb = (d + kEmbCols - 1) / kEmbCols;
+  const int items = nruns[0] * ncb;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int run = item / ncb, cb = item % ncb;
+    const int i0 = starts[run], i1 = starts[run + 1];
+    const int v = skey[i0];
+    const int len = i1 - i0;
+    const int c0 = cb * kEmbCols, c = c0 + 8 * lane;
+    const int a = i0 + (int)((int64_t)len * w / 8), b = i0 + (int)((int64_t)len * (w + 1) / 8);
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    if (c < d) {
+      int i = a;
+      for (; i + 8 <= b; i += 8) {
+        float4 r[8][2];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) r[u] = *reinterpret_cast<const float4*>(dx + (int64_t)spos[i + u] * d + c);
+        for (int u = 0; u < 8; ++u) {
+          const float4* src = reinterpret_cast<const float4*>(dx + (int64_t)spos[i + u] * d + c);
+          r[u][0] = src[0];
+          r[u][1] = src[1];
+        }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        acc.x += r[u].x; acc.y += r[u].y; acc.z += r[u].z; acc.w += r[u].w;
+        for (int u = 0; u < 8; ++u) {
+          acc[0] += r[u][0].x; acc[1] += r[u][0].y; acc[2] += r[u][0].z; acc[3] += r[u][0].w;
+          acc[4] += r[u][1].x; acc[5] += r[u][1].y; acc[6] += r[u][1].z; acc[7] += r[u][1].w;
+        }
+      }
+      for (; i < b; ++i) {
+        const float4* src = reinterpret_cast<const float4*>(dx + (int64_t)spos[i] * d + c);
+        const float4 r0 = src[0], r1 = src[1];
+        acc[0] += r0.x; acc[1] += r0.y; acc[2] += r0.z; acc[3] += r0.w;
+        acc[4] += r1.x; acc[5] += r1.y; acc[6] += r1.z; acc[7] += r1.w;
       }
     }
-    for (; i < i1; ++i) {
-      const float4 r = *reinterpret_cast<const float4*>(dx + (int64_t)spos[i] * d + c);
-      acc.x += r.x; acc.y += r.y; acc.z += r.z; acc.w += r.w;
+    __syncthreads();  // part[] reuse across items
+#pragma unroll
+    for (int k = 0; k < 8; ++k) part[w][8 * lane + k] = acc[k];
+    __syncthreads();
+    const int col = c0 + threadIdx.x;
+    if (col < d) {
+      float t = part[0][threadIdx.x];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) t += part[k][threadIdx.x];
+      gemb[(int64_t)v * d + col] += t;
     }
-    float4* o = reinterpret_cast<float4*>(out + c);
-    float4 g = *o;
-    g.x += acc.x; g.y += acc.y; g.z += acc.z; g.w += acc.w;
-    *o = g;
-  } else {
-    for (int c = c0 + threadIdx.x; c < min(d, c0 + kEmbCols); c += blockDim.x) {
+  }
+}
+
+// d % 8 != 0 (tiny desk shapes): one thread per column walks the run in order
+__global__ void embed_bwd_runs_scalar_kernel(const int32_t* __restrict__ skey, const int32_t* __restrict__ spos,
+                                             const int32_t* __restrict__ starts, const int32_t* __restrict__ nruns,
+                                             const float* __restrict__ dx, float* __restrict__ gemb, int d) {
+  for (int run = blockIdx.x; run < nruns[0]; run += gridDim.x) {
+    const int i0 = starts[run], i1 = starts[run + 1];
+    const int v = skey[i0];
+    for (int c = threadIdx.x; c < d; c += blockDim.x) {
       float acc = 0.f;
       for (int i = i0; i < i1; ++i) acc += dx[(int64_t)spos[i] * d + c];
-      out[c] += acc;
+      gemb[(int64_t)v * d + c] += acc;
     }
   }
 }
@@ -111,12 +162,13 @@ __global__ void pos_bwd_kernel(const float* __restrict__ dx, float* __restrict__
 }
 
 static size_t embed_sort_temp_bytes(int n_tok, int vocab) {
-  size_t temp = 0;
+  size_t temp = 0, scan = 0;
   int bits = 1;
   while ((1 << bits) < vocab) ++bits;
   cub::DeviceRadixSort::SortPairs(nullptr, temp, (const int32_t*)nullptr, (int32_t*)nullptr, (const int32_t*)nullptr,
                                   (int32_t*)nullptr, n_tok, 0, bits);
-  return temp;
+  cub::DeviceScan::InclusiveSum(nullptr, scan, (const int32_t*)nullptr, (int32_t*)nullptr, n_tok);
+  return temp > scan ? temp : scan;
 }
 
 // ------------------------------------------------------------------ LayerNorm
@@ -534,31 +586,43 @@ extern "C" int fb_embed_bwd(const int32_t* d_tok, const float* d_dx, float* d_ge
   return FB_OK;
 }
 
+// workspace slots of the sorted embedding backward (each n_tok + 1 int32, 256-byte aligned)
+enum { kSlotKey, kSlotPosIn, kSlotPos, kSlotFlag, kSlotRun, kSlotStart, kSlotCount, kNumSlots };
+
 extern "C" int64_t fb_embed_bwd_work_bytes(int n_tok, int vocab) {
   if (n_tok <= 0 || vocab <= 0) return 0;
-  return 3 * (((int64_t)n_tok * 4 + 255) / 256 * 256) + (int64_t)embed_sort_temp_bytes(n_tok, vocab) + 256;
+  const int64_t slot = ((int64_t)(n_tok + 1) * 4 + 255) / 256 * 256;
+  return kNumSlots * slot + (int64_t)embed_sort_temp_bytes(n_tok, vocab) + 256;
 }
 
 extern "C" int fb_embed_bwd_sorted(const int32_t* d_tok, const float* d_dx, float* d_gemb, float* d_gpos, int n_tok,
                                    int T, int d, int vocab, void* d_work, int64_t work_bytes, void* stream) {
   FB_REQUIRE(n_tok > 0 && T > 0 && d > 0 && vocab > 0, "embed_bwd: bad shape");
   FB_REQUIRE(d_work && work_bytes >= fb_embed_bwd_work_bytes(n_tok, vocab), "embed_bwd: work buffer too small");
-  FB_REQUIRE((d & 3) != 0 || ((uintptr_t)d_dx % 16 == 0 && (uintptr_t)d_gemb % 16 == 0),
-             "embed_bwd: dx / gemb must be 16-byte aligned");
+  FB_REQUIRE((d & 7) != 0 || (uintptr_t)d_dx % 16 == 0, "embed_bwd: dx must be 16-byte aligned");
   cudaStream_t st = (cudaStream_t)stream;
-  const int64_t slot = ((int64_t)n_tok * 4 + 255) / 256 * 256;
+  const int64_t slot = ((int64_t)(n_tok + 1) * 4 + 255) / 256 * 256;
   uint8_t* w = reinterpret_cast<uint8_t*>(d_work);
-  int32_t* skey = reinterpret_cast<int32_t*>(w);
-  int32_t* pos_in = reinterpret_cast<int32_t*>(w + slot);
-  int32_t* spos = reinterpret_cast<int32_t*>(w + 2 * slot);
-  void* temp = w + 3 * slot;
+  auto sl = [&](int k) { return reinterpret_cast<int32_t*>(w + k * slot); };
+  int32_t *skey = sl(kSlotKey), *pos_in = sl(kSlotPosIn), *spos = sl(kSlotPos), *flags = sl(kSlotFlag),
+          *run_idx = sl(kSlotRun), *starts = sl(kSlotStart), *nruns = sl(kSlotCount);
+  void* temp = w + kNumSlots * slot;
   size_t temp_bytes = embed_sort_temp_bytes(n_tok, vocab);
   int bits = 1;
   while ((1 << bits) < vocab) ++bits;
-  iota_kernel<<<std::min((n_tok + 255) / 256, kNumSMs * 4), 256, 0, st>>>(pos_in, n_tok);
+  const int g = std::min((n_tok + 255) / 256, kNumSMs * 4);
+  iota_kernel<<<g, 256, 0, st>>>(pos_in, n_tok);
   FB_LAUNCH_CHECK();
   FB_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, d_tok, skey, pos_in, spos, n_tok, 0, bits, st));
-  embed_bwd_runs_kernel<<<dim3(n_tok, (d + kEmbCols - 1) / kEmbCols), 64, 0, st>>>(skey, spos, d_dx, d_gemb, n_tok, d);
+  run_flags_kernel<<<g, 256, 0, st>>>(skey, n_tok, flags);
+  FB_LAUNCH_CHECK();
+  FB_CUDA_TRY(cub::DeviceScan::InclusiveSum(temp, temp_bytes, flags, run_idx, n_tok, st));
+  run_bounds_kernel<<<g, 256, 0, st>>>(flags, run_idx, n_tok, starts, nruns);
+  FB_LAUNCH_CHECK();
+  if (d % 8 == 0)
+    embed_bwd_runs_kernel<<<kNumSMs * 4, 256, 0, st>>>(skey, spos, starts, nruns, d_dx, d_gemb, d);
+  else
+    embed_bwd_runs_scalar_kernel<<<kNumSMs * 4, 64, 0, st>>>(skey, spos, starts, nruns, d_dx, d_gemb, d);
   FB_LAUNCH_CHECK();
   if (d_gpos) {
     pos_bwd_kernel<<<std::min<int64_t>(((int64_t)T * d + 255) / 256, kNumSMs * 8), 256, 0, st>>>(d_dx, d_gpos, n_tok,

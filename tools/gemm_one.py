@@ -14,7 +14,7 @@ am, bm = int(os.environ.get("GAM", "0")), int(os.environ.get("GBM", "0"))
 epi = os.environ.get("GE", "bf16")
 A = torch.randn((K, M) if am else (M, K), device="cuda").to(torch.bfloat16)
 B = torch.randn((K, N) if bm else (N, K), device="cuda").to(torch.bfloat16)
-cdt = torch.bfloat16 if epi in ("bf16", "gelu", "dgelu") else torch.float32
+cdt = torch.bfloat16 if epi in ("bf16", "gelu", "dgelu", "ce_exp") else torch.float32
 C = torch.zeros(M, N, dtype=cdt, device="cuda")
 aux = torch.randn(M, N, device="cuda").to(torch.bfloat16 if epi in ("gelu", "dgelu") else torch.float32)
 for _ in range(4):
