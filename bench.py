@@ -110,22 +110,25 @@ def tail_split(M, N, K):
     return best if best_t <= 0.96 * base else 1
 
 
-def launches_per_step(c):
-    """Kernel launches of our library per local step (fb_train_step), from the runtime's schedule."""
-    L, d, M = c["L"], c["d"], c["B"] * c["T"]
+def launches_per_step(c, fuse=1):
+    """Kernel launches of our library per local step (fb_train_step), from the runtime's schedule
+    (`fuse` micro-batches per forward/backward pass, ClientSession.fuse)."""
+    L, d, M = c["L"], c["d"], c["B"] * fuse * c["T"]
     chunks = math.ceil(M / 8192)
-    # forward: gather + embed + L x (ln, qkv, attn, proj, ln, fc, proj2) + ln_f + chunks x (logits, ce, dgrad, wgrad)
+    # forward: gather + embed + L x (ln, qkv, attn, proj, ln, fc, proj2) + ln_f
+    # + chunks x (head GEMM with the CE epilogue, ce_lse, ce_grad, head dgrad, head wgrad)
     hd = min(M, 8192)  # head-dgrad rows per chunk: a last-wave split or a classic split-K adds one reduction
-    fwd = 1 + 1 + 7 * L + 1 + 4 * chunks + chunks * (tail_split(hd, d, c["V"]) > 1 or splitk_splits(hd, d, c["V"]) > 1)
+    fwd = 1 + 1 + 7 * L + 1 + 5 * chunks + chunks * (tail_split(hd, d, c["V"]) > 1 or splitk_splits(hd, d, c["V"]) > 1)
     # backward: ln_f bwd(2) + L x (dgelu, wgrad, dgrad, wgrad, ln bwd(2), dgrad, wgrad, attn bwd(3), dgrad, wgrad,
-    # ln bwd(2)) + split-K reduction launches + embed bwd
+    # ln bwd(2)) + split-K reduction launches + sorted embedding bwd (iota, CUB sort ~4, run flags,
+    # CUB scan ~2, run bounds, runs: ~10)
     wg = [(d, 4 * d), (4 * d, d), (d, d), (3 * d, d)]
     red = sum(1 for (mm, nn) in wg if splitk_splits(mm, nn, M) > 1 or tail_split(mm, nn, M) > 1)
     # attention bwd: 3 launches (D pre-pass, kernel, dQ finalize); 2 when the out-projection dgrad
     # forms D in its epilogue (fb_gemm_bf16_rowdot: 2-SM raster, i.e. >= 74 256x256 tiles)
     rowdot = M >= 256 and d >= 256 and (M // 256) * (d // 256) >= 74
-    bwd = 2 + L * (15 - rowdot + red) + 1
-    return c["micro"] * (fwd + bwd) + 4  # + sumsq, step_prepare, adamw, telemetry
+    bwd = 2 + L * (15 - rowdot + red) + 10
+    return c["micro"] // fuse * (fwd + bwd) + 4  # + sumsq, step_prepare, adamw, telemetry
 
 
 def peaks():
@@ -213,6 +216,7 @@ def run_ours(args, cfgname):
     P = max(1, args.concurrent)  # clients trained concurrently on this GPU (own stream + evaluator each)
     task = TrainTask(1, client, W + K, 0, c["B"], c["micro"], {"data": 99}, "bench")
     sess = ClientSession(ev, it, adamw, sched).begin(w0, task)
+    fuse = sess.fuse
     tokens_step = c["B"] * c["micro"] * c["T"]
     extra = []  # (session, stream) of the concurrent clients beyond the first
     for i in range(1, P):
@@ -407,6 +411,7 @@ def run_ours(args, cfgname):
         "data": "synthetic (reference Markov corpus seed 99, 32 MB; seeded reference init)",
         "config": {"workload": f"{cfgname}: {c['label']}", "params": N, "tokens_per_step_per_gpu": tokens_step,
                    "global_batch_seqs": c["B"] * c["micro"], "seq_len": c["T"], "clients": Kc,
+                   "micro_batches_per_pass": fuse,
                    "clients_per_gpu": clients_per_gpu, "concurrent_clients_per_gpu": P,
                    "parallelism": f"clients sharded over {world} GPU(s)" + (f", {P} trained concurrently per GPU"
                                                                           if P > 1 else ""),
@@ -453,7 +458,7 @@ def run_ours(args, cfgname):
                            "peak_note": "sustained bf16; per-kernel timing is off with concurrent clients"}
         out["attention"] = None
     # GPU launches of our kernels inside the timed region (per step, counted from the runtime's schedule)
-    out["gpu_launches"] = launches_per_step(c) * K * P
+    out["gpu_launches"] = launches_per_step(c, fuse) * K * P
     if rank == 0 and world == 1 and not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(c, args.cpu_budget)
     if rank == 0:

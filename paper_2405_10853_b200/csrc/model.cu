@@ -286,8 +286,12 @@ extern "C" int fb_train_step(const fb_model_cfg* cfgp, float* P, void* shadow, f
   const fb_model_cfg& c = *cfgp;
   const fb_data_desc& D = *data;
   cudaStream_t st = (cudaStream_t)stream;
-  const int B = D.batch, T = D.seq_len, M = B * T;
-  FB_REQUIRE(D.micro >= 1 && B >= 1, "micro_batches and batch_size must be >= 1");
+  const int fuse = D.fuse > 1 ? D.fuse : 1;
+  FB_REQUIRE(D.micro >= 1 && D.batch >= 1, "micro_batches and batch_size must be >= 1");
+  FB_REQUIRE(D.micro % fuse == 0, "fuse=%d must divide micro_batches=%d", fuse, D.micro);
+  // one forward/backward pass covers `fuse` consecutive micro-batches: micro-batch i's rows are
+  // order[cursor + i*B + r], so pass j is the contiguous cursor range [cursor + j*fuse*B, +fuse*B)
+  const int B = D.batch * fuse, T = D.seq_len, M = B * T, passes = D.micro / fuse;
   const int64_t n = layout_of(c).total;
   double* part_g = scratch;
   double* part_u = scratch + FB_RED_BLOCKS;
@@ -299,16 +303,16 @@ extern "C" int fb_train_step(const fb_model_cfg* cfgp, float* P, void* shadow, f
   FB_REQUIRE(ws_bytes >= need + (int64_t)M * 4 + 256, "workspace too small for the step");
   int32_t* tok = reinterpret_cast<int32_t*>(reinterpret_cast<uint8_t*>(ws) + ((need + 255) & ~int64_t(255)));
   FB_CUDA_TRY(cudaMemsetAsync(G, 0, sizeof(float) * (size_t)n, st));
-  const float gscale = (float)(1.0 / ((double)B * (T - 1)) / D.micro);
-  for (int j = 0; j < D.micro; ++j) {
+  const float gscale = (float)(1.0 / ((double)D.batch * (T - 1)) / D.micro);
+  for (int j = 0; j < passes; ++j) {
     TRY(fb_gather_batch(D.d_corpus, D.d_order, D.n_order, D.cursor + (int64_t)j * B, B, T, tok, st));
     TRY(fb_model_fwd_bwd(cfgp, P, shadow, G, tok, B, T, gscale, row_loss + (int64_t)j * M, 1, ws, need, st));
   }
   TRY(fb_sumsq_partials(G, n, part_g, st));
   TRY(fb_step_prepare(part_g, lr, bc1, bc2, opt.clip_norm, ctl, st));
   TRY(fb_adamw_step(P, G, m1, m2, shadow, n, opt, ctl, part_u, part_p, first_bad, st));
-  tele_finalize_kernel<<<1, 1024, 0, st>>>(row_loss, D.micro * M, 1.0 / ((double)B * (T - 1)) / D.micro, ctl, part_u,
-                                           part_p, first_bad, n, tele);
+  tele_finalize_kernel<<<1, 1024, 0, st>>>(row_loss, passes * M, 1.0 / ((double)D.batch * (T - 1)) / D.micro, ctl,
+                                           part_u, part_p, first_bad, n, tele);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }

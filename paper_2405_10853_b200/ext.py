@@ -77,7 +77,7 @@ class ModelCfg(C.Structure):
 
 class DataDesc(C.Structure):
     _fields_ = [("d_corpus", _vp), ("d_order", _vp), ("n_order", _i64), ("seq_len", C.c_int32),
-                ("batch", C.c_int32), ("micro", C.c_int32), ("pad", C.c_int32), ("cursor", _i64)]
+                ("batch", C.c_int32), ("micro", C.c_int32), ("fuse", C.c_int32), ("cursor", _i64)]
 
 
 _lib = None

@@ -25,7 +25,7 @@ N = ev.n_params
 w = torch.empty(N, device="cuda").normal_(0, 0.02)
 shadow, grad, _, _ = ev.buffers()
 ext.call("fb_cast_bf16", w.data_ptr(), shadow.data_ptr(), N, ext.stream_handle())
-B, T = c["B"], c["T"]
+B, T = int(os.environ.get("PM_B", c["B"])), c["T"]
 tok = torch.randint(33, 97, (B * T,), dtype=torch.int32, device="cuda")
 ws = ev.workspace(B, T)
 rl = torch.empty(B * T, dtype=torch.float64, device="cuda")
