@@ -68,7 +68,10 @@ def _dev(v, device="cuda"):
     if isinstance(v, t.Tensor):
         return v.to(device=device, dtype=t.float32).contiguous()
     data = v.data if isinstance(v, ParamVector) else np.asarray(v, dtype=np.float32)
-    return t.from_numpy(np.ascontiguousarray(data, dtype=np.float32)).to(device)
+    a = np.ascontiguousarray(data, dtype=np.float32)
+    if not a.flags.writeable:  # ParamVector storage is read-only; torch wants a writable host buffer
+        a = a.copy()
+    return t.from_numpy(a).to(device)
 
 
 @dataclass

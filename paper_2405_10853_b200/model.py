@@ -165,7 +165,10 @@ class LossEvaluator:
             data = params.data if isinstance(params, ParamVector) else np.asarray(params, dtype=np.float32)
             if data.size != self.n_params:
                 raise ParamError(f"parameter vector length {data.size} != model size {self.n_params}")
-            w = torch.from_numpy(np.ascontiguousarray(data, dtype=np.float32)).to(self.device)
+            a = np.ascontiguousarray(data, dtype=np.float32)
+            if not a.flags.writeable:  # ParamVector storage is read-only
+                a = a.copy()
+            w = torch.from_numpy(a).to(self.device)
         if w.numel() != self.n_params:
             raise ParamError(f"parameter vector length {w.numel()} != model size {self.n_params}")
         return w
