@@ -202,10 +202,15 @@ int fb_attn_bwd_ex(const void* d_qkv, const void* d_o, const void* d_do, const f
                    const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh,
                    int use_alibi, int flags, void* stream);
 /* 1: bitwise-reproducible training (reference test_trainer.py:56-63 replay contract): the
- * attention backward uses the fixed-order CUDA-core kernels instead of the tcgen05 kernel,
- * whose dQ partials are TMA reduce-added in arrival order. Every other kernel is
- * deterministic in both modes. Process-wide; 0 (default) = fastest. */
+ * tcgen05 attention backward stores each key block's dQ partial to its own slab and sums the
+ * slabs in key-block order, instead of TMA reduce-adding them in arrival order (it then needs
+ * the larger d_work of fb_attn_bwd_work_floats). Every other kernel is deterministic in both
+ * modes. Process-wide; the library default is 0 (dQ partials reduce-added in arrival order,
+ * with the small d_work above); the Python package turns 1 on when it loads the library
+ * (FB_DETERMINISTIC=0 opts out): the reference's replay semantics cost 1.4% of C4 step time. */
 int fb_set_deterministic(int enable);
+/* floats of d_work that fb_attn_bwd / fb_attn_bwd_ex need in the current mode */
+int64_t fb_attn_bwd_work_floats(int B, int T, int H, int dh);
 /* Fused LM head + mean next-token cross-entropy (model.py:114, :150, :226-229) for
  * rows [row0, row0 + rows) of a B x T batch: logits = x W^T on tcgen05 with the FB_EPI_CE_EXP
  * epilogue (no f32 logits in HBM: bf16 e = exp(x - m_chunk) plus (m, sum) per 32-column chunk),

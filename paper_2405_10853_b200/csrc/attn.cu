@@ -12,9 +12,10 @@
 // backward); this file holds the D = rowsum(dO o O) pre-pass, the dQ f32 -> bf16
 // finalisation and the C-ABI dispatch. Tensor-core path: T % 128 == 0, dh in {64, 128};
 // every other shape (the reference's desk configs: dh 4..32, short or ragged T) runs the
-// CUDA-core kernels of attn_generic.cu. Deterministic mode (fb_set_deterministic) routes
-// the backward to the fixed-order generic kernels as well (the tensor-core backward adds
-// dQ partials with TMA reduce-add in arrival order).
+// CUDA-core kernels of attn_generic.cu (fixed order by construction). Deterministic mode
+// (fb_set_deterministic): the tensor-core backward stores each key block's dQ partial into
+// its own slab instead of TMA reduce-adding it in arrival order, and dq_finalize_det_kernel
+// sums the slabs in key-block order.
 #include "common.cuh"
 
 namespace fb {
@@ -62,7 +63,7 @@ int attn_fwd_generic(const void* qkv, void* o, float* lse, int B, int T, int H, 
                      cudaStream_t st);
 int attn_bwd_generic(const void* qkv, const void* o, const void* dO, const float* lse, void* dqkv, float* work, int B,
                      int T, int H, int dh, int use_alibi, int d_ready, cudaStream_t st);
-int g_deterministic = 0;
+int g_deterministic = 0;  // fb_set_deterministic (the Python package turns it on at load)
 
 static bool tc_shape(int T, int dh) { return (dh == 64 || dh == 128) && T % 128 == 0; }
 
@@ -71,7 +72,32 @@ int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, uint8_t* live, int 
                        cudaStream_t st);
 template <int DH>
 int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live, const float* Dbuf,
-                       float* dq, void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st);
+                       float* dq, void* dqkv, int B, int T, int H, int use_alibi, int det, cudaStream_t st);
+
+// Deterministic mode: dQ[row] = sum over the key blocks kb <= row / 128 whose (128-row block,
+// kb) pair the forward marked live (exactly the pairs the backward wrote), in ascending kb
+// order, from the per-key-block slabs part[kb][B*T][d]; bf16 into dqkv[:, 0:d].
+__global__ void dq_finalize_det_kernel(const float* __restrict__ part, const uint8_t* __restrict__ live,
+                                       __nv_bfloat16* __restrict__ dqkv, int B, int T, int H, int dh) {
+  const int d = H * dh;
+  const int64_t rows = (int64_t)B * T, n8 = rows * d / 8;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = 8 * i, row = e / d;
+    const int c = (int)(e % d);
+    const int b = (int)(row / T), t = (int)(row % T), bh = b * H + c / dh, qb = t / 128;
+    const uint8_t* lv = live ? live + ((int64_t)bh * (T / 128) + qb) * (T / 64) : nullptr;
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int kb = 0; kb <= qb; ++kb) {
+      if (lv && !(lv[2 * kb] | lv[2 * kb + 1])) continue;  // dead pair: the backward wrote nothing
+      const float4* p = reinterpret_cast<const float4*>(part + ((int64_t)kb * rows + row) * d + c);
+      const float4 x = p[0], y = p[1];
+      acc[0] += x.x; acc[1] += x.y; acc[2] += x.z; acc[3] += x.w;
+      acc[4] += y.x; acc[5] += y.y; acc[6] += y.z; acc[7] += y.w;
+    }
+    *reinterpret_cast<uint4*>(dqkv + row * 3 * d + c) = make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]),
+                                                                  pack_bf16(acc[4], acc[5]), pack_bf16(acc[6], acc[7]));
+  }
+}
 
 template <int DH>
 static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const float* lse, const uint8_t* live,
@@ -80,16 +106,21 @@ static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const
   float* Dbuf = work;
   float* dq = work + (int64_t)B * H * T;
   const int nw = B * T * H;
+  const int det = g_deterministic;
+  float* part = dq + (int64_t)B * T * d;  // deterministic mode: T/128 slabs of [B*T][d]
   if (flags & FB_ATTN_D_READY) {  // D came from the out-projection dgrad epilogue: only zero dQ
-    FB_CUDA_TRY(cudaMemsetAsync(dq, 0, sizeof(float) * (size_t)B * T * d, st));
+    if (!det) FB_CUDA_TRY(cudaMemsetAsync(dq, 0, sizeof(float) * (size_t)B * T * d, st));
   } else {
-    attn_bwd_dot_kernel<<<(nw + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dO, Dbuf, dq, B, T,
-                                                      H, DH);
+    attn_bwd_dot_kernel<<<(nw + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dO, Dbuf,
+                                                      det ? nullptr : dq, B, T, H, DH);
     FB_LAUNCH_CHECK();
   }
-  int rc = attn_bwd_tc_launch<DH>(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
+  int rc = attn_bwd_tc_launch<DH>(qkv, dO, lse, live, Dbuf, det ? part : dq, dqkv, B, T, H, use_alibi, det, st);
   if (rc) return rc;
-  dq_finalize_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq, (__nv_bfloat16*)dqkv, B * T, d);
+  if (det)
+    dq_finalize_det_kernel<<<kNumSMs * 8, 256, 0, st>>>(part, live, (__nv_bfloat16*)dqkv, B, T, H, DH);
+  else
+    dq_finalize_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq, (__nv_bfloat16*)dqkv, B * T, d);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }
@@ -124,7 +155,7 @@ extern "C" int fb_attn_bwd_ex(const void* d_qkv, const void* d_o, const void* d_
   FB_REQUIRE(B > 0 && H > 0 && T > 0 && dh > 0, "attn_bwd: bad shape B=%d T=%d H=%d dh=%d", B, T, H, dh);
   FB_REQUIRE(d_work != nullptr, "attn_bwd: needs a work buffer of B*H*T + B*T*H*dh floats");
   cudaStream_t st = (cudaStream_t)stream;
-  if (!tc_shape(T, dh) || g_deterministic)
+  if (!tc_shape(T, dh))
     return attn_bwd_generic(d_qkv, d_o, d_do, d_lse, d_dqkv, d_work, B, T, H, dh, use_alibi, flags & FB_ATTN_D_READY,
                             st);
   const double fl = 2.0 * 2.0 * 2.0 * B * H * (double)T * (T + 1) / 2.0 * dh;  // bwd = 2x fwd
@@ -139,4 +170,10 @@ extern "C" int fb_attn_bwd_ex(const void* d_qkv, const void* d_o, const void* d_
 extern "C" int fb_set_deterministic(int enable) {
   fb::g_deterministic = enable ? 1 : 0;
   return FB_OK;
+}
+
+extern "C" int64_t fb_attn_bwd_work_floats(int B, int T, int H, int dh) {
+  if (B <= 0 || T <= 0 || H <= 0 || dh <= 0) return 0;
+  const int64_t base = (int64_t)B * H * T + (int64_t)B * T * H * dh;
+  return fb::g_deterministic && fb::tc_shape(T, dh) ? base + (int64_t)(T / 128) * B * T * H * dh : base;
 }

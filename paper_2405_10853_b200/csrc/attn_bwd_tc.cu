@@ -102,6 +102,22 @@ __device__ __forceinline__ void build_live_list(const uint8_t* __restrict__ live
   if (lane == 0) *nlive = (uint32_t)n;
 }
 
+// dQ box out: TMA reduce-add into the f32 accumulator (z = 0), or, in deterministic mode, a
+// plain TMA store into key block kb's own partial slab (z = kb) that dq_finalize_det_kernel
+// sums in ascending kb order (the reduce-adds of different key blocks land in arrival order).
+__device__ __forceinline__ void dq_out_box(const CUtensorMap* map, uint32_t src, int x, int y, int kb, int det) {
+  if (det)
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(x), "r"(y), "r"(kb)
+                 : "memory");
+  else
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(src), "r"(x), "r"(y), "r"(0)
+                 : "memory");
+}
+
 // ---------------------------------------------------------------------------------------
 // dh = 128 variant with 64-query tiles and a software pipeline across query tiles:
 //   MMA order per tile t:  [pds_full(t)]  S^T(t+1), dP^T(t+1)  dV(t)  dK(t)  [dq_empty(t-1)] dQ^T(t)
@@ -136,7 +152,8 @@ __global__ void __launch_bounds__(320, 1)
                          const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
                          const __grid_constant__ CUtensorMap tm_dkv,
                          const float* __restrict__ lse2, const uint8_t* __restrict__ live, const float* __restrict__ Dd,
-                         __nv_bfloat16* __restrict__ dqkv, int T, int H, float scale_log2, float scale, int use_alibi) {
+                         __nv_bfloat16* __restrict__ dqkv, int T, int H, float scale_log2, float scale, int use_alibi,
+                         int det) {
   using Cf = AttnBwd64Cfg;
   constexpr int DH = Cf::DH;
   extern __shared__ uint8_t smem_raw[];
@@ -317,11 +334,7 @@ __global__ void __launch_bounds__(320, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
       if ((tid & 127) == 0) {
-        asm volatile(
-            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                reinterpret_cast<uint64_t>(&tm_dq)),
-            "r"(sX + g * 32 * DH * 4), "r"(h * DH), "r"(row0 + q0 + 32 * g)
-            : "memory");
+        dq_out_box(&tm_dq, sX + g * 32 * DH * 4, h * DH, row0 + q0 + 32 * g, kb, det);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
@@ -486,7 +499,7 @@ __global__ void __launch_bounds__(320, 1)
                           const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv, const float* __restrict__ lse2,
                           const uint8_t* __restrict__ live, const float* __restrict__ Dd,
                           __nv_bfloat16* __restrict__ dqkv, int T, int H,
-                          float scale_log2, float scale, int use_alibi) {
+                          float scale_log2, float scale, int use_alibi, int det) {
   using Cf = AttnBwdD64Cfg;
   constexpr int DH = Cf::DH;
   extern __shared__ uint8_t smem_raw[];
@@ -657,11 +670,7 @@ __global__ void __launch_bounds__(320, 1)
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
       if (quad == 0 && lane == 0) {
-        asm volatile(
-            "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
-                reinterpret_cast<uint64_t>(&tm_dq)),
-            "r"(xbox), "r"(h * DH + 32 * g), "r"(row0 + q0)
-            : "memory");
+        dq_out_box(&tm_dq, xbox, h * DH + 32 * g, row0 + q0, kb, det);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     };
@@ -820,7 +829,7 @@ static int encode_box(CUtensorMap* m, const void* base, int64_t rows, int cols, 
 
 static int attn_bwd_tc64_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live,
                                 const float* Dbuf, float* dq,
-                                void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
+                                void* dqkv, int B, int T, int H, int use_alibi, int det, cudaStream_t st) {
   using Cf = AttnBwd64Cfg;
   constexpr int DH = 128;
   const int d = H * DH;
@@ -832,11 +841,13 @@ static int attn_bwd_tc64_launch(const void* qkv, const void* dO, const float* ls
   rc = encode_box(&to, dO, (int64_t)B * T, d, 64, DH / 64);
   if (rc) return rc;
   {
-    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)B * T};
-    cuuint64_t strides[1] = {(cuuint64_t)d * 4};
-    cuuint32_t box[2] = {DH, 32};  // one 32-query box per warpgroup
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = g_enc_bwd(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, es,
+    // {d, B*T, slabs}: slabs = 1 (reduce-add accumulator) or T/128 (deterministic per-key-block partials)
+    const int slabs = det ? T / 128 : 1;
+    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)B * T, (cuuint64_t)slabs};
+    cuuint64_t strides[2] = {(cuuint64_t)d * 4, (cuuint64_t)B * T * d * 4};
+    cuuint32_t box[3] = {DH, 32, 1};  // one 32-query box per warpgroup
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_enc_bwd(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dq, dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -851,14 +862,14 @@ static int attn_bwd_tc64_launch(const void* qkv, const void* dO, const float* ls
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale = 1.0f / sqrtf((float)DH);
   k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tkv, tq, to, tdq, tdkv, lse, live, Dbuf, (__nv_bfloat16*)dqkv, T, H,
-                                                 1.4426950408889634f * scale, scale, use_alibi);
+                                                 1.4426950408889634f * scale, scale, use_alibi, det);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }
 
 static int attn_bwd_tcd64_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live,
                                  const float* Dbuf, float* dq,
-                                 void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
+                                 void* dqkv, int B, int T, int H, int use_alibi, int det, cudaStream_t st) {
   using Cf = AttnBwdD64Cfg;
   constexpr int DH = 64;
   const int d = H * DH;
@@ -868,11 +879,12 @@ static int attn_bwd_tcd64_launch(const void* qkv, const void* dO, const float* l
   rc = encode_box(&to, dO, (int64_t)B * T, d, 128, 1);
   if (rc) return rc;
   {
-    cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)B * T};
-    cuuint64_t strides[1] = {(cuuint64_t)d * 4};
-    cuuint32_t box[2] = {32, 128};
-    cuuint32_t es[2] = {1, 1};
-    CUresult r = g_enc_bwd(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, dq, dims, strides, box, es,
+    const int slabs = det ? T / 128 : 1;
+    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)B * T, (cuuint64_t)slabs};
+    cuuint64_t strides[2] = {(cuuint64_t)d * 4, (cuuint64_t)B * T * d * 4};
+    cuuint32_t box[3] = {32, 128, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = g_enc_bwd(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dq, dims, strides, box, es,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -887,14 +899,14 @@ static int attn_bwd_tcd64_launch(const void* qkv, const void* dO, const float* l
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale = 1.0f / sqrtf((float)DH);
   k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tq, to, tdq, tdkv, lse, live, Dbuf, (__nv_bfloat16*)dqkv, T, H,
-                                                 1.4426950408889634f * scale, scale, use_alibi);
+                                                 1.4426950408889634f * scale, scale, use_alibi, det);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }
 
 template <int DH>
 int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live, const float* Dbuf,
-                       float* dq, void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
+                       float* dq, void* dqkv, int B, int T, int H, int use_alibi, int det, cudaStream_t st) {
   if (!g_enc_bwd) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -906,15 +918,15 @@ int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const 
     g_enc_bwd = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   FB_REQUIRE(T <= 16384, "attn_bwd: T=%d above 16384", T);
-  if (DH == 128) return attn_bwd_tc64_launch(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
-  if (DH == 64) return attn_bwd_tcd64_launch(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, st);
+  if (DH == 128) return attn_bwd_tc64_launch(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, det, st);
+  if (DH == 64) return attn_bwd_tcd64_launch(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, det, st);
   return FB_UNSUPPORTED;
 }
 
 template int attn_bwd_tc_launch<64>(const void*, const void*, const float*, const uint8_t*, const float*, float*,
-                                    void*, int, int, int, int, cudaStream_t);
+                                    void*, int, int, int, int, int, cudaStream_t);
 template int attn_bwd_tc_launch<128>(const void*, const void*, const float*, const uint8_t*, const float*, float*,
-                                     void*, int, int, int, int, cudaStream_t);
+                                     void*, int, int, int, int, int, cudaStream_t);
 
 }  // namespace fb
 

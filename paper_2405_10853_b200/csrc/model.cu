@@ -114,7 +114,7 @@ static WS carve(const fb_model_cfg& c, int B, int T, Arena& A) {
   w.dao = A.take<__nv_bfloat16>(M * d);
   w.dqkv = A.take<__nv_bfloat16>(M * 3 * d);
   w.dfc = A.take<__nv_bfloat16>(M * 4 * d);
-  w.attn_work = A.take<float>(B * H * T + M * d);
+  w.attn_work = A.take<float>(fb_attn_bwd_work_floats(B, T, (int)H, (int)(d / H)));
   w.ln_work = A.take<float>(2 * 592 * d);
   w.splitk = A.take<float>(kSplitKFloats);
   w.emb_work_bytes = fb_embed_bwd_work_bytes((int)M, (int)V);

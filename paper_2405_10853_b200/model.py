@@ -88,8 +88,11 @@ def check_gpu_shape(cfg: TinyLMConfig, T: int | None = None) -> None:
 
 
 def set_deterministic(enable: bool = True) -> None:
-    """Bitwise-reproducible training (reference tests/test_trainer.py:56-63): route the
-    attention backward to the fixed-order kernels (fb_set_deterministic). Process-wide."""
+    """Bitwise-reproducible training (reference tests/test_trainer.py:56-63; the package default,
+    FB_DETERMINISTIC=0 opts out at load): the
+    tcgen05 attention backward sums its per-key-block dQ slabs in key-block order. False trades
+    that for ~1.4% of C4 step time (dQ partials reduce-added in arrival order).
+    fb_set_deterministic; process-wide."""
     ext.call("fb_set_deterministic", int(bool(enable)))
 
 

@@ -77,9 +77,9 @@ class ClientSession:
     and the error names the local step. finish() only waits for the last rows."""
 
     max_lag = 2
-    # activation-workspace budget for fused micro-batches (C4: 61 GB at fuse 2; resident client end
-    # weights of a 1-GPU 8-client round need the rest of the 180 GB)
-    fuse_budget = int(float(os.environ.get("FB_FUSE_WS_GB", "64")) * 1e9)
+    # activation-workspace budget for fused micro-batches (C4: 65 GB at fuse 2 with the deterministic
+    # dQ slabs; the resident client end weights of a 1-GPU 8-client round need most of the rest)
+    fuse_budget = int(float(os.environ.get("FB_FUSE_WS_GB", "72")) * 1e9)
 
     def __init__(self, evaluator: LossEvaluator, batches: BatchIterator, adamw_cfg: AdamWConfig,
                  sched: ScheduleConfig):

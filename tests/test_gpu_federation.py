@@ -96,7 +96,7 @@ def test_concurrent_clients_match_sequential():
             res = fed.run_round(res.params, res.opt, 2)
             outs.append((res.params.tensor.cpu().numpy(), res.opt.momentum.tensor.cpu().numpy(), res.client_metrics))
     finally:
-        set_deterministic(False)
+        set_deterministic(True)
     assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
     assert np.array_equal(outs[0][1].view(np.uint32), outs[1][1].view(np.uint32))
     assert outs[0][2] == outs[1][2]

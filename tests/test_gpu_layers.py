@@ -63,7 +63,7 @@ def test_attention_fwd_bwd(fb, B, T, H, dh, alibi):
     do = torch.randn(B * T, d, device=dev).to(torch.bfloat16)
     o_ref.backward(do.float())
     dqkv = torch.empty_like(qkv)
-    work = torch.empty(B * H * T + B * T * d, dtype=torch.float32, device=dev)
+    work = torch.empty(int(fb.lib().fb_attn_bwd_work_floats(B, T, H, dh)), dtype=torch.float32, device=dev)
     fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse2.data_ptr(), live.data_ptr(),
             dqkv.data_ptr(), work.data_ptr(), B, T, H, dh, alibi, fb.stream_handle())
     torch.cuda.synchronize()
@@ -82,7 +82,7 @@ def _attn_run(fb, qkv, do, B, T, H, dh, live):
     o = torch.empty(B * T, d, dtype=torch.bfloat16, device=dev)
     lse2 = torch.empty(B * H * T, dtype=torch.float32, device=dev)
     dqkv = torch.empty_like(qkv)
-    work = torch.empty(B * H * T + B * T * d, dtype=torch.float32, device=dev)
+    work = torch.empty(int(fb.lib().fb_attn_bwd_work_floats(B, T, H, dh)), dtype=torch.float32, device=dev)
     lp = live.data_ptr() if live is not None else None
     fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), lp, B, T, H, dh, 1, fb.stream_handle())
     fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse2.data_ptr(), lp, dqkv.data_ptr(),
@@ -132,7 +132,7 @@ def test_attention_bwd_all_dead_map_zeroes(fb):
     fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), None, B, T, H, dh, 1, fb.stream_handle())
     live = torch.zeros(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device=dev)
     dqkv = torch.full_like(qkv, 3.0)
-    work = torch.empty(B * H * T + B * T * d, dtype=torch.float32, device=dev)
+    work = torch.empty(int(fb.lib().fb_attn_bwd_work_floats(B, T, H, dh)), dtype=torch.float32, device=dev)
     fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse2.data_ptr(), live.data_ptr(),
             dqkv.data_ptr(), work.data_ptr(), B, T, H, dh, 1, fb.stream_handle())
     torch.cuda.synchronize()
@@ -315,7 +315,7 @@ def test_outproj_dgrad_rowdot_feeds_attention_bwd(fb, B, T, H, dh):
     rc = fb.lib().fb_gemm_bf16_rowdot(M, d, d, dY.data_ptr(), d, 0, W.data_ptr(), d, 1, dO.data_ptr(), d,
                                       o.data_ptr(), d, D.data_ptr(), T, dh, fb.stream_handle())
     assert rc == 0
-    work = torch.empty(B * H * T + M * d, dtype=torch.float32, device=dev)
+    work = torch.empty(int(fb.lib().fb_attn_bwd_work_floats(B, T, H, dh)), dtype=torch.float32, device=dev)
     work[: B * H * T].copy_(D)
     work[B * H * T:].fill_(123.0)  # the D_READY path must zero dQ itself
     g1 = torch.empty_like(qkv)
@@ -328,3 +328,34 @@ def test_outproj_dgrad_rowdot_feeds_attention_bwd(fb, B, T, H, dh):
     torch.cuda.synchronize()
     torch.testing.assert_close(work[: B * H * T], work2[: B * H * T], atol=1e-3, rtol=1e-4)
     torch.testing.assert_close(g1.float(), g2.float(), atol=2e-2, rtol=2e-2)
+
+
+@pytest.mark.parametrize("B,T,H,dh", [(2, 512, 4, 128), (2, 1024, 3, 64), (1, 2048, 16, 128)])
+def test_attention_bwd_deterministic_mode(fb, B, T, H, dh):
+    """fb_set_deterministic(1): the tcgen05 backward stores per-key-block dQ slabs and sums them
+    in key-block order — two runs are bitwise equal; dK/dV are the default mode's bits and dQ
+    equals it up to f32 summation order."""
+    torch.manual_seed(9)
+    dev = torch.device("cuda")
+    d = H * dh
+    qkv = torch.randn(B * T, 3 * d, device=dev).to(torch.bfloat16)
+    do = torch.randn(B * T, d, device=dev).to(torch.bfloat16)
+    o = torch.empty(B * T, d, dtype=torch.bfloat16, device=dev)
+    lse2 = torch.empty(B * H * T, dtype=torch.float32, device=dev)
+    live = torch.empty(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device=dev)
+    st = fb.stream_handle()
+    fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), live.data_ptr(), B, T, H, dh, 1, st)
+    outs = []
+    for det in (0, 1, 1):
+        fb.call("fb_set_deterministic", det)
+        nw = int(fb.lib().fb_attn_bwd_work_floats(B, T, H, dh))
+        work = torch.empty(nw, dtype=torch.float32, device=dev)
+        dqkv = torch.empty_like(qkv)
+        fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse2.data_ptr(), live.data_ptr(),
+                dqkv.data_ptr(), work.data_ptr(), B, T, H, dh, 1, st)
+        outs.append(dqkv)
+    fb.call("fb_set_deterministic", 1)  # the library default
+    torch.cuda.synchronize()
+    assert torch.equal(outs[1], outs[2])                      # replay: bitwise
+    assert torch.equal(outs[0][:, d:], outs[1][:, d:])        # dK, dV: the same MMAs
+    torch.testing.assert_close(outs[1][:, :d].float(), outs[0][:, :d].float(), atol=1e-2, rtol=1e-2)

@@ -32,7 +32,8 @@ def test_library_exports_every_declared_symbol():
     assert L.fb_abi_version() == 1
     # every declared entry has a ctypes signature in the binding
     bound = set(ext.SIGNATURES) | {"fb_last_error", "fb_model_n_params", "fb_model_workspace_bytes",
-                                     "fb_embed_bwd_work_bytes", "fb_lmhead_ce_work_floats"}
+                                     "fb_embed_bwd_work_bytes", "fb_lmhead_ce_work_floats",
+                                     "fb_attn_bwd_work_floats"}
     assert set(syms) <= bound, set(syms) - bound
 
 

@@ -17,7 +17,7 @@ for B, T, H, dh in [(8, 2048, 16, 128), (8, 2048, 12, 64), (16, 1024, 8, 64)]:
     live = torch.empty(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device="cuda")
     do = torch.randn_like(o)
     dqkv = torch.empty_like(qkv)
-    work = torch.empty(B * H * T + B * T * d, device="cuda")
+    work = torch.empty(int(ext.lib().fb_attn_bwd_work_floats(B, T, H, dh)), device="cuda")
     st = ext.stream_handle()
     fwd = lambda: ext.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), live.data_ptr(), B, T, H, dh, 1, st)
     bwd = lambda: ext.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), live.data_ptr(), dqkv.data_ptr(),

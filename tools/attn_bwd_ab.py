@@ -20,7 +20,7 @@ for B, T, H, dh in [(16, 2048, 16, 128), (16, 2048, 12, 64)]:
     live = torch.empty(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device="cuda")
     do = torch.randn_like(o)
     dq = torch.empty_like(qkv)
-    work = torch.empty(B * H * T + B * T * d, device="cuda")
+    work = torch.empty(int(ext.lib().fb_attn_bwd_work_floats(B, T, H, dh)), device="cuda")
     st = ext.stream_handle()
     ext.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), live.data_ptr(), B, T, H, dh, 1, st)
     f = lambda: ext.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse.data_ptr(), live.data_ptr(),

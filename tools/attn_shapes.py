@@ -9,7 +9,7 @@ for B, T, H, dh in [(8, 2048, 16, 128), (2, 4096, 16, 128), (32, 1024, 16, 128),
     lse = torch.empty(B * H * T, device="cuda")
     live = torch.empty(B * H * (T // 128) * (T // 64), dtype=torch.uint8, device="cuda")
     do = torch.randn_like(o); dqkv = torch.empty_like(qkv)
-    work = torch.empty(B * H * T + B * T * d, device="cuda")
+    work = torch.empty(int(ext.lib().fb_attn_bwd_work_floats(B, T, H, dh)), device="cuda")
     st = ext.stream_handle()
     fwd = lambda: ext.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse.data_ptr(), live.data_ptr(), B, T, H, dh, 0, st)  # no alibi: all live
     fwd()

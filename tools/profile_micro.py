@@ -21,6 +21,8 @@ a = ap.parse_args()
 c = CONFIGS[a.config]
 cfg = TinyLMConfig(vocab_size=c["V"], context_len=c["T"], n_layers=c["L"], d_model=c["d"], n_heads=c["H"])
 ev = LossEvaluator(cfg)
+if os.environ.get("PM_DET"):
+    ext.call("fb_set_deterministic", 1)
 N = ev.n_params
 w = torch.empty(N, device="cuda").normal_(0, 0.02)
 shadow, grad, _, _ = ev.buffers()
