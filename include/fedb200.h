@@ -22,7 +22,7 @@ extern "C" {
 
 enum fb_status { FB_OK = 0, FB_BAD_ARG = 1, FB_CUDA_ERROR = 2, FB_NONFINITE = 3, FB_UNSUPPORTED = 4 };
 
-#define FB_ABI_VERSION 1
+#define FB_ABI_VERSION 2  /* 2: fused LM-head CE replaces fb_ce_fwd_bwd; fb_data_desc.fuse; deterministic attention bwd */
 #define FB_MAX_CLIENTS 64
 #define FB_MAX_REPLICAS 8  /* w' destinations besides w_out (peer GPUs), fb_fedagg_step_f32_peers */
 #define FB_RED_BLOCKS 1184 /* fixed reduction grid: 148 SMs x 8, deterministic partials */
