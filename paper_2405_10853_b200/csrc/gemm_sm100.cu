@@ -775,20 +775,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int row0 = m0 + quad * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * 256 + half * 128;
       float rd = 0.f;
-      // the next chunk's TMEM load is in flight while this chunk's epilogue runs (two register
-      // buffers, fully unrolled so they stay in registers)
-      uint32_t rbuf[2][32];
-      tmem_ld_32x32b_x32(taddr, rbuf[0]);
-#pragma unroll
+#pragma unroll 1
       for (int c = 0; c < 4; ++c) {
-        uint32_t(&r)[32] = rbuf[c & 1];
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(taddr + c * 32, r);
         tmem_ld_wait();
         if (c == 3) {
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(&tempty_bar[buf]);
-        } else {
-          tmem_ld_32x32b_x32(taddr + (c + 1) * 32, rbuf[(c + 1) & 1]);
         }
         const int col = n0 + c * 32;
         if (row0 < M && col < N) {
