@@ -22,7 +22,8 @@ extern "C" {
 
 enum fb_status { FB_OK = 0, FB_BAD_ARG = 1, FB_CUDA_ERROR = 2, FB_NONFINITE = 3, FB_UNSUPPORTED = 4 };
 
-#define FB_ABI_VERSION 2  /* 2: fused LM-head CE replaces fb_ce_fwd_bwd; fb_data_desc.fuse; deterministic attention bwd */
+#define FB_ABI_VERSION 3  /* 2: fused LM-head CE replaces fb_ce_fwd_bwd; fb_data_desc.fuse; deterministic attention bwd.
+                             3: attention bwd always fixed-order (ordered dQ partials), d_work adds box counters */
 #define FB_MAX_CLIENTS 64
 #define FB_MAX_REPLICAS 8  /* w' destinations besides w_out (peer GPUs), fb_fedagg_step_f32_peers */
 #define FB_RED_BLOCKS 1184 /* fixed reduction grid: 148 SMs x 8, deterministic partials */
@@ -196,20 +197,18 @@ int fb_attn_bwd(const void* d_qkv, const void* d_o, const void* d_do, const floa
                 const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh,
                 int use_alibi, void* stream);
 /* flags: FB_ATTN_D_READY = d_work[0 : B*H*T] already holds D = rowsum(dO o O)
- * (fb_gemm_bf16_rowdot), so the pre-pass only zeroes the dQ accumulator. */
+ * (fb_gemm_bf16_rowdot), so the backward skips its D pre-pass. */
 enum { FB_ATTN_D_READY = 1 };
 int fb_attn_bwd_ex(const void* d_qkv, const void* d_o, const void* d_do, const float* d_lse,
                    const uint8_t* d_live, void* d_dqkv, float* d_work, int B, int T, int H, int dh,
                    int use_alibi, int flags, void* stream);
-/* 1: bitwise-reproducible training (reference test_trainer.py:56-63 replay contract): the
- * tcgen05 attention backward stores each key block's dQ partial to its own slab and sums the
- * slabs in key-block order, instead of TMA reduce-adding them in arrival order (it then needs
- * the larger d_work of fb_attn_bwd_work_floats). Every other kernel is deterministic in both
- * modes. Process-wide; the library default is 0 (dQ partials reduce-added in arrival order,
- * with the small d_work above); the Python package turns 1 on when it loads the library
- * (FB_DETERMINISTIC=0 opts out): the reference's replay semantics cost 1.4% of C4 step time. */
+/* Kept for ABI compatibility: every kernel is fixed-order (bitwise reproducible, the reference's
+ * test_trainer.py:56-63 replay contract) whatever the flag. The tcgen05 attention backward adds
+ * each query block's per-key-block dQ partials in descending key-block order (per-box counters in
+ * d_work) and writes bf16 dQ itself; ABI 2's slab buffer and finalize pass are gone. */
 int fb_set_deterministic(int enable);
-/* floats of d_work that fb_attn_bwd / fb_attn_bwd_ex need in the current mode */
+/* floats of d_work that fb_attn_bwd / fb_attn_bwd_ex need: D [B*H*T], dQ partial sums [B*T*H*dh],
+ * box counters [B*H*ceil(T/32)] */
 int64_t fb_attn_bwd_work_floats(int B, int T, int H, int dh);
 /* Fused LM head + mean next-token cross-entropy (model.py:114, :150, :226-229) for
  * rows [row0, row0 + rows) of a B x T batch: logits = x W^T on tcgen05 with the FB_EPI_CE_EXP

@@ -12,18 +12,16 @@
 // backward); this file holds the D = rowsum(dO o O) pre-pass, the dQ f32 -> bf16
 // finalisation and the C-ABI dispatch. Tensor-core path: T % 128 == 0, dh in {64, 128};
 // every other shape (the reference's desk configs: dh 4..32, short or ragged T) runs the
-// CUDA-core kernels of attn_generic.cu (fixed order by construction). Deterministic mode
-// (fb_set_deterministic): the tensor-core backward stores each key block's dQ partial into
-// its own slab instead of TMA reduce-adding it in arrival order, and dq_finalize_det_kernel
-// sums the slabs in key-block order.
+// CUDA-core kernels of attn_generic.cu (fixed order by construction). Both backwards are
+// bitwise reproducible: the tensor-core one adds the key blocks' dQ partials in a fixed
+// (descending key block) order and writes bf16 dQ itself (attn_bwd_tc.cu, dq_order).
 #include "common.cuh"
 
 namespace fb {
 
-// D[bh][t] = sum_c dO * O, one warp per (row, head), 8-byte vector loads; the same warp
-// zeroes that (row, head) slice of the f32 dQ accumulator (saves a memset pass).
+// D[bh][t] = sum_c dO * O, one warp per (row, head), 8-byte vector loads
 __global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o, const __nv_bfloat16* __restrict__ dO,
-                                    float* __restrict__ D, float* __restrict__ dq, int B, int T, int H, int dh) {
+                                    float* __restrict__ D, int B, int T, int H, int dh) {
   const int gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (gw >= B * T * H) return;
@@ -39,23 +37,11 @@ __global__ void attn_bwd_dot_kernel(const __nv_bfloat16* __restrict__ o, const _
     const float2 a0 = __bfloat1622float2(ap[0]), a1 = __bfloat1622float2(ap[1]);
     const float2 g0 = __bfloat1622float2(gp[0]), g1 = __bfloat1622float2(gp[1]);
     s += a0.x * g0.x + a0.y * g0.y + a1.x * g1.x + a1.y * g1.y;
-    if (dq) *reinterpret_cast<float4*>(dq + (int64_t)row * d + h * dh + c) = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   s = warp_sum(s);
   if (lane == 0) {
     const int b = row / T, t = row % T;
     D[((int64_t)b * H + h) * T + t] = s;
-  }
-}
-
-// dqkv[:, 0:d] = bf16(dq accumulator): 8 columns per thread (two 16-byte loads, one 16-byte store)
-__global__ void dq_finalize_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dqkv, int rows, int d) {
-  const int64_t n8 = (int64_t)rows * d / 8;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = 8 * i, r = e / d, c = e % d;
-    const float4 x = *reinterpret_cast<const float4*>(acc + e), y = *reinterpret_cast<const float4*>(acc + e + 4);
-    *reinterpret_cast<uint4*>(dqkv + r * 3 * d + c) =
-        make_uint4(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w), pack_bf16(y.x, y.y), pack_bf16(y.z, y.w));
   }
 }
 
@@ -72,57 +58,24 @@ int attn_fwd_tc_launch(const void* qkv, void* o, float* lse, uint8_t* live, int 
                        cudaStream_t st);
 template <int DH>
 int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live, const float* Dbuf,
-                       float* dq, void* dqkv, int B, int T, int H, int use_alibi, int det, cudaStream_t st);
-
-// Deterministic mode: dQ[row] = sum over the key blocks kb <= row / 128 whose (128-row block,
-// kb) pair the forward marked live (exactly the pairs the backward wrote), in ascending kb
-// order, from the per-key-block slabs part[kb][B*T][d]; bf16 into dqkv[:, 0:d].
-__global__ void dq_finalize_det_kernel(const float* __restrict__ part, const uint8_t* __restrict__ live,
-                                       __nv_bfloat16* __restrict__ dqkv, int B, int T, int H, int dh) {
-  const int d = H * dh;
-  const int64_t rows = (int64_t)B * T, n8 = rows * d / 8;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n8; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = 8 * i, row = e / d;
-    const int c = (int)(e % d);
-    const int b = (int)(row / T), t = (int)(row % T), bh = b * H + c / dh, qb = t / 128;
-    const uint8_t* lv = live ? live + ((int64_t)bh * (T / 128) + qb) * (T / 64) : nullptr;
-    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    for (int kb = 0; kb <= qb; ++kb) {
-      if (lv && !(lv[2 * kb] | lv[2 * kb + 1])) continue;  // dead pair: the backward wrote nothing
-      const float4* p = reinterpret_cast<const float4*>(part + ((int64_t)kb * rows + row) * d + c);
-      const float4 x = p[0], y = p[1];
-      acc[0] += x.x; acc[1] += x.y; acc[2] += x.z; acc[3] += x.w;
-      acc[4] += y.x; acc[5] += y.y; acc[6] += y.z; acc[7] += y.w;
-    }
-    *reinterpret_cast<uint4*>(dqkv + row * 3 * d + c) = make_uint4(pack_bf16(acc[0], acc[1]), pack_bf16(acc[2], acc[3]),
-                                                                  pack_bf16(acc[4], acc[5]), pack_bf16(acc[6], acc[7]));
-  }
-}
+                       float* dq, uint32_t* sem, void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st);
 
 template <int DH>
 static int attn_bwd_launch(const void* qkv, const void* o, const void* dO, const float* lse, const uint8_t* live,
                            void* dqkv, float* work, int B, int T, int H, int use_alibi, int flags, cudaStream_t st) {
   const int d = H * DH;
-  float* Dbuf = work;
-  float* dq = work + (int64_t)B * H * T;
-  const int nw = B * T * H;
-  const int det = g_deterministic;
-  float* part = dq + (int64_t)B * T * d;  // deterministic mode: T/128 slabs of [B*T][d]
-  if (flags & FB_ATTN_D_READY) {  // D came from the out-projection dgrad epilogue: only zero dQ
-    if (!det) FB_CUDA_TRY(cudaMemsetAsync(dq, 0, sizeof(float) * (size_t)B * T * d, st));
-  } else {
-    attn_bwd_dot_kernel<<<(nw + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dO, Dbuf,
-                                                      det ? nullptr : dq, B, T, H, DH);
+  float* Dbuf = work;                                           // [B*H*T]
+  float* dq = work + (int64_t)B * H * T;                        // [B*T][d] f32 partial sums
+  uint32_t* sem = reinterpret_cast<uint32_t*>(dq + (int64_t)B * T * d);  // [B*H*T/32] box counters
+  if (!(flags & FB_ATTN_D_READY)) {
+    const int nw = B * T * H;
+    attn_bwd_dot_kernel<<<(nw + 7) / 8, 256, 0, st>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dO, Dbuf, B, T,
+                                                      H, DH);
     FB_LAUNCH_CHECK();
   }
-  int rc = attn_bwd_tc_launch<DH>(qkv, dO, lse, live, Dbuf, det ? part : dq, dqkv, B, T, H, use_alibi, det, st);
-  if (rc) return rc;
-  if (det)
-    dq_finalize_det_kernel<<<kNumSMs * 8, 256, 0, st>>>(part, live, (__nv_bfloat16*)dqkv, B, T, H, DH);
-  else
-    dq_finalize_kernel<<<kNumSMs * 8, 256, 0, st>>>(dq, (__nv_bfloat16*)dqkv, B * T, d);
-  FB_LAUNCH_CHECK();
-  return FB_OK;
+  // dQ is written into dqkv by the backward itself (ordered partials, attn_bwd_tc.cu dq_order):
+  // no accumulator memset, no finalize pass
+  return attn_bwd_tc_launch<DH>(qkv, dO, lse, live, Dbuf, dq, sem, dqkv, B, T, H, use_alibi, st);
 }
 
 }  // namespace fb
@@ -168,12 +121,12 @@ extern "C" int fb_attn_bwd_ex(const void* d_qkv, const void* d_o, const void* d_
 }
 
 extern "C" int fb_set_deterministic(int enable) {
-  fb::g_deterministic = enable ? 1 : 0;
+  fb::g_deterministic = enable ? 1 : 0;  // every kernel is fixed-order in both modes (ABI 3)
   return FB_OK;
 }
 
 extern "C" int64_t fb_attn_bwd_work_floats(int B, int T, int H, int dh) {
   if (B <= 0 || T <= 0 || H <= 0 || dh <= 0) return 0;
-  const int64_t base = (int64_t)B * H * T + (int64_t)B * T * H * dh;
-  return fb::g_deterministic && fb::tc_shape(T, dh) ? base + (int64_t)(T / 128) * B * T * H * dh : base;
+  // D [B*H*T] + dQ partial sums [B*T*H*dh] + box counters [B*H*ceil(T/32)] (u32)
+  return (int64_t)B * H * T + (int64_t)B * T * H * dh + (int64_t)B * H * ((T + 31) / 32);
 }

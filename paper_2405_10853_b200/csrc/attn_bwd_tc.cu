@@ -7,9 +7,9 @@
 //
 // CTA = 128 keys of one (b, h); loop over the causal query tiles. Two kernels:
 //   dh = 128  attn_bwd_tc64_kernel: 64-query tiles, P^T in TMEM (dV as an A-from-TMEM
-//             MMA), 3-stage Q/dO ring, dQ^T = K^T dS^T in its own TMEM columns, one TMA
-//             bulk reduce-add per warpgroup per tile, software pipeline across query
-//             tiles (elementwise of tile t+1 overlaps the MMAs of tile t).
+//             MMA), 3-stage Q/dO ring, dQ^T = K^T dS^T in its own TMEM columns, one
+//             ordered dQ box per warpgroup per tile (dq_order), software pipeline across
+//             query tiles (elementwise of tile t+1 overlaps the MMAs of tile t).
 //   dh = 64   attn_bwd_tcd64_kernel: 128-query tiles, dQ = dS K with dS^T read as an
 //             MN-major A operand, P/dS share a double-buffered smem tile.
 // Warp roles in both: warp 0 TMA producer, warp 1 TMEM owner + single-thread MMA issuer,
@@ -35,6 +35,20 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TRACE(slot) do { if (blockIdx.x == 4 && blockIdx.y == 5) g_attn_trace[(slot)] = gtimer(); } while (0)
 #else
 #define TRACE(slot) do {} while (0)
+#endif
+#ifdef FB_ATTN_PROF  // per-CTA start / end / ns spent in sem_wait_eq / SM id (tools/attn_dq_prof.py)
+__device__ unsigned long long g_attn_prof[8192 * 8];
+__device__ __forceinline__ unsigned long long ptimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define PROF_CTA() (blockIdx.y * gridDim.x + blockIdx.x)
+#define PROF_T0(v) const unsigned long long v = ptimer()
+#define PROF_ADD(slot, v) do { if (PROF_CTA() < 8192) atomicAdd(&g_attn_prof[PROF_CTA() * 8 + (slot)], ptimer() - (v)); } while (0)
+#else
+#define PROF_T0(v) do {} while (0)
+#define PROF_ADD(slot, v) do {} while (0)
 #endif
 
 __device__ __forceinline__ float ex2b(float x) {
@@ -102,20 +116,117 @@ __device__ __forceinline__ void build_live_list(const uint8_t* __restrict__ live
   if (lane == 0) *nlive = (uint32_t)n;
 }
 
-// dQ box out: TMA reduce-add into the f32 accumulator (z = 0), or, in deterministic mode, a
-// plain TMA store into key block kb's own partial slab (z = kb) that dq_finalize_det_kernel
-// sums in ascending kb order (the reduce-adds of different key blocks land in arrival order).
-__device__ __forceinline__ void dq_out_box(const CUtensorMap* map, uint32_t src, int x, int y, int kb, int det) {
-  if (det)
+// Ordered dQ accumulation (deterministic, no memset and no finalize pass).
+// The dQ rows of 128-query block m receive one partial from every live key block kb <= m, and
+// they arrive in DESCENDING kb order: CTA kb walks its query tiles upward from its diagonal, so
+// the CTA of the larger kb reaches block m first (FA4's causal semaphore order). Every dQ box
+// has a counter; the CTA of kb waits until it equals the number of live kb' in (kb, m], then
+//   first contributor (count 0): TMA store of its partial into the f32 accumulator;
+//   middle:                      TMA reduce-add (after the previous one COMPLETED);
+//   last (no live kb' < kb):     acc + own partial in registers, bf16 straight into dqkv.
+// A contributor bumps the counter one tile later, once its bulk op completed (the wait sits
+// where the staging box is recycled anyway). The sum order is fixed by the live map alone, so
+// dQ is bitwise reproducible. dq_order returns count | (last << 8) for (block m, key block kb);
+// kb = -1 counts every live key block of row block m. One full warp calls it.
+__device__ __forceinline__ uint32_t dq_order(const uint8_t* __restrict__ live, int bh, int T, int m, int kb) {
+  const int lane = threadIdx.x & 31;
+  uint32_t before = 0;
+  bool later = false;
+  for (int base = 0; base <= m; base += 32) {
+    const int k = base + lane;
+    bool ok = k <= m;
+    if (ok && live) {
+      const uint8_t* row = live + ((int64_t)bh * (T / 128) + m) * (T / 64) + 2 * k;
+      ok = (row[0] | row[1]) != 0;
+    }
+    before += __popc(__ballot_sync(0xffffffffu, ok && k > kb));
+    later |= __ballot_sync(0xffffffffu, ok && k < kb) != 0u;
+  }
+  return before | (later ? 0u : 0x100u);
+}
+// the same for one (m, kb) per lane (no ballot): the dQ warps tabulate 32 tiles at a time. The
+// map row is read as 32-bit words (two key blocks each), all loads in flight together.
+__device__ __forceinline__ uint32_t dq_order_lane(const uint8_t* __restrict__ live, int bh, int T, int m, int kb) {
+  uint32_t before = 0;
+  bool later = false;
+  if (!live) {
+    before = (uint32_t)(m > kb ? m - kb : 0);
+    later = kb > 0;
+  } else {
+    const uint8_t* row = live + ((int64_t)bh * (T / 128) + m) * (T / 64);
+    if ((T & 255) == 0) {
+      const uint32_t* w = reinterpret_cast<const uint32_t*>(row);
+      const int nw = m / 2 + 1;  // words holding key blocks 0..m
+#pragma unroll 8
+      for (int i = 0; i < nw; ++i) {
+        const uint32_t x = __ldg(w + i);
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+          const int k = 2 * i + hf;
+          const bool ok = k <= m && ((x >> (16 * hf)) & 0xffffu) != 0u;
+          before += (ok && k > kb) ? 1u : 0u;
+          later |= ok && k < kb;
+        }
+      }
+    } else {
+      for (int k = 0; k <= m; ++k) {
+        const bool ok = (row[2 * k] | row[2 * k + 1]) != 0;
+        before += (ok && k > kb) ? 1u : 0u;
+        later |= ok && k < kb;
+      }
+    }
+  }
+  return before | (later ? 0u : 0x100u);
+}
+
+// spin (one thread) until *p == v; a count above v or ~2^32 cycles without progress is a bug: trap
+// instead of hanging the GPU
+__device__ __forceinline__ void sem_wait_eq(const uint32_t* p, uint32_t v) {
+#ifdef FB_ATTN_PROF
+  const unsigned long long p0 = ptimer();
+#endif
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t x;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(x) : "l"(p) : "memory");
+    if (x == v) break;
+    if (x > v || clock64() - t0 > (1ll << 32)) __trap();
+    __nanosleep(64);
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");  // later TMA reduce-adds see the acquired data
+#ifdef FB_ATTN_PROF
+  if (PROF_CTA() < 8192) atomicAdd(&g_attn_prof[PROF_CTA() * 8 + 2], ptimer() - p0);
+#endif
+}
+// after cp.async.bulk.wait_group 0: publish this thread's completed bulk writes, bump the counter
+__device__ __forceinline__ void sem_release(uint32_t* p) {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
+}
+// a staged dQ box out (not the last contributor): TMA store for the first, reduce-add otherwise
+__device__ __forceinline__ void dq_out_box(const CUtensorMap* map, uint32_t src, int x, int y, bool first) {
+  if (first)
     asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                      reinterpret_cast<uint64_t>(map)),
-                 "r"(src), "r"(x), "r"(y), "r"(kb)
+                 "r"(src), "r"(x), "r"(y), "r"(0)
                  : "memory");
   else
     asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                      reinterpret_cast<uint64_t>(map)),
                  "r"(src), "r"(x), "r"(y), "r"(0)
                  : "memory");
+}
+// Row block kb of dQ gets no partial at all when every key block of it was dead (possible only
+// if even the diagonal underflowed): the CTA of key block kb writes those rows' zeros. Called by
+// whole warps (nthr threads, tid 0..nthr-1).
+__device__ __forceinline__ void zero_dead_rows(const uint8_t* __restrict__ live, int bh, int T, int kb, int DH, int H,
+                                               int row0, int h, __nv_bfloat16* __restrict__ dqkv, int tid, int nthr) {
+  if (!live) return;
+  if ((dq_order(live, bh, T, kb, -1) & 0xffu) != 0u) return;  // warp-uniform
+  for (int e = tid; e < 128 * DH / 8; e += nthr) {
+    const int rr = e / (DH / 8), c = (e % (DH / 8)) * 8;
+    *reinterpret_cast<uint4*>(dqkv + (int64_t)(row0 + kb * 128 + rr) * (3 * H * DH) + h * DH + c) = make_uint4(0, 0, 0, 0);
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -147,13 +258,13 @@ struct AttnBwd64Cfg {
   static_assert(SMEM <= 232448, "attention bwd (dh 128) smem");
 };
 
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_tc64_kernel(const __grid_constant__ CUtensorMap tm_kv, const __grid_constant__ CUtensorMap tm_q,
                          const __grid_constant__ CUtensorMap tm_do, const __grid_constant__ CUtensorMap tm_dq,
                          const __grid_constant__ CUtensorMap tm_dkv,
                          const float* __restrict__ lse2, const uint8_t* __restrict__ live, const float* __restrict__ Dd,
-                         __nv_bfloat16* __restrict__ dqkv, int T, int H, float scale_log2, float scale, int use_alibi,
-                         int det) {
+                         __nv_bfloat16* __restrict__ dqkv, float* __restrict__ dqacc, uint32_t* __restrict__ sem,
+                         int T, int H, float scale_log2, float scale, int use_alibi) {
   using Cf = AttnBwd64Cfg;
   constexpr int DH = Cf::DH;
   extern __shared__ uint8_t smem_raw[];
@@ -173,11 +284,21 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
   uint32_t* nlive_p = tmem_slot + 1;
   uint8_t* tl = reinterpret_cast<uint8_t*>(tmem_slot + 2);
+  uint64_t* staged = bar + 60;  // [2] warpgroup g's dQ box is in its staging area (4 warp arrivals)
+  uint64_t* sfree = bar + 62;   // [2] dQ warp g is done with that staging area
   float* sE0 = reinterpret_cast<float*>(smem + Cf::L_OFF);  // e[2][64] (double-buffered)
   float* sD0 = sE0 + 128;                                     // D[2][64]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x;
+#ifdef FB_ATTN_PROF
+  if (threadIdx.x == 0 && PROF_CTA() < 8192) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_attn_prof[PROF_CTA() * 8 + 0] = ptimer();
+    g_attn_prof[PROF_CTA() * 8 + 3] = smid;
+  }
+#endif
   const int bh = blockIdx.y, b = bh / H, h = bh % H;
   const int d = H * DH;
   const int row0 = b * T;
@@ -188,7 +309,6 @@ __global__ void __launch_bounds__(320, 1)
     tma_prefetch(&tm_kv);
     tma_prefetch(&tm_q);
     tma_prefetch(&tm_do);
-    tma_prefetch(&tm_dq);
     mbar_init(kv_full, 1);
     for (int s = 0; s < Cf::NQ; ++s) {
       mbar_init(&q_full[s], 1);
@@ -201,6 +321,10 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(pds_full, 8);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 8);
+    for (int g = 0; g < 2; ++g) {
+      mbar_init(&staged[g], 4);
+      mbar_init(&sfree[g], 1);
+    }
     fence_barrier_init();
 #ifndef FB_EXP_LATE_KV
     // K / V of this key block are needed whatever is live: start them before the TMEM
@@ -299,6 +423,49 @@ __global__ void __launch_bounds__(320, 1)
         umma_commit(&pds_free[b2]);
       }
     }
+  } else if (warp >= 10) {
+    // dQ warps: warp 10 + g turns warpgroup g's staged 32 x 128 boxes into dQ in the fixed order
+    // of dq_order: TMA store (first) / reduce-add (middle), bumping the box counter once the op
+    // completed, or acc + box -> bf16 dqkv (last). The counter waits, bulk-op completions and
+    // release fences stay off the compute warps.
+    const int g = warp - 10;
+    const float* Xg = reinterpret_cast<const float*>(smem + Cf::X_OFF) + g * 32 * DH;
+    uint32_t ords = 0;  // lane l: dq_order of tile (t & ~31) + l
+    for (int t = 0; t < nlive; ++t) {
+      const int q0 = (first + tl[t]) * 64, qrow = q0 + 32 * g;
+      if ((t & 31) == 0 && t + lane < nlive) ords = dq_order_lane(live, bh, T, (first + tl[t + lane]) >> 1, kb);
+      const uint32_t ord = __shfl_sync(0xffffffffu, ords, t & 31), cnt = ord & 0xffu;
+      uint32_t* bsem = sem + (int64_t)bh * (T / 32) + qrow / 32;
+      mbar_wait(&staged[g], t & 1);
+      if (lane == 0 && cnt) sem_wait_eq(bsem, cnt);  // every larger live key block has added its partial
+      __syncwarp();
+      if (ord & 0x100u) {  // last contributor: dQ = acc + partial, bf16 (lane: 4 dh columns x 32 rows)
+        const int c = 4 * lane;
+        const float* acc = dqacc + (int64_t)(row0 + qrow) * d + h * DH + c;
+        __nv_bfloat16* out = dqkv + (int64_t)(row0 + qrow) * (3 * d) + h * DH + c;
+        float4 a[32];  // every accumulator load in flight at once (one L2 round trip per box)
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          a[i] = cnt ? __ldcg(reinterpret_cast<const float4*>(acc + (int64_t)i * d)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          float4 x = *reinterpret_cast<const float4*>(Xg + i * DH + c);
+          if (cnt) x = make_float4(a[i].x + x.x, a[i].y + x.y, a[i].z + x.z, a[i].w + x.w);
+          *reinterpret_cast<uint2*>(out + (int64_t)i * (3 * d)) = make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfree[g]);
+      } else if (lane == 0) {
+        dq_out_box(&tm_dq, smem_u32(Xg), h * DH, row0 + qrow, cnt == 0);
+        bulk_commit();
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(&sfree[g]);
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        sem_release(bsem);  // at once: the next key block waits on it
+      }
+      __syncwarp();
+    }
+    if (g == 0) zero_dead_rows(live, bh, T, kb, DH, H, row0, h, dqkv, lane, 32);
   } else {
     // compute warps: g = warpgroup (query-column half), quad = TMEM lane quadrant
     const int g = (warp - 2) >> 2;
@@ -310,10 +477,7 @@ __global__ void __launch_bounds__(320, 1)
     const float slk = sl * (float)kj;
     const int tid = threadIdx.x - 64;  // 0..255
     float* Xs = reinterpret_cast<float*>(smem + Cf::X_OFF);
-    auto drain = [&](int t) {  // dQ^T(t) -> staging [64 q][128 dh] -> TMA reduce-add into dq rows
-      // each warpgroup g drains its own 32 query rows (one 32 x 128 reduce box, its own named
-      // barrier), so the two groups do not wait for each other's elementwise skew
-      const int q0 = (first + tl[t]) * 64;
+    auto drain = [&](int t) {  // dQ^T(t) -> warpgroup g's 32 x 128 staging box, handed to dQ warp g
       mbar_wait(dq_full, t & 1);
       tc_fence_after();
       uint32_t v[32];
@@ -322,24 +486,23 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
-      // this group's staging box of the previous reduce must have been read by TMA
-      if ((tid & 127) == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
+      PROF_T0(pf);
+      mbar_wait(&sfree[g], (t & 1) ^ 1);  // dQ warp g is done with this group's previous box
+      if (lane == 0 && quad == 0) PROF_ADD(6, pf);
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         const float2 sv2 = pk_mul(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), make_float2(scale, scale));
         Xs[(32 * g + i) * DH + r] = sv2.x;
         Xs[(32 * g + i + 1) * DH + r] = sv2.y;
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the TMA reads the box
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&staged[g]);
+      // publishes the e/D that load_ed wrote just before (read in the next tile's elementwise)
       asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
-      if ((tid & 127) == 0) {
-        dq_out_box(&tm_dq, sX + g * 32 * DH * 4, h * DH, row0 + q0 + 32 * g, kb, det);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
     };
     // e/D of tile t live in buffer t & 1; tile t+1's are prefetched before drain(t-1), whose
-    // warpgroup barriers publish them (all readers of that buffer finished tile t-1 earlier)
+    // warpgroup barrier publishes them (all readers of that buffer finished tile t-1 earlier)
     auto load_ed = [&](int t) {
       const int q0 = (first + tl[t]) * 64;
       float* E = sE0 + (t & 1) * 64;
@@ -420,12 +583,6 @@ __global__ void __launch_bounds__(320, 1)
       if (warp == 2 && lane == 0) TRACE(16 * t + 7);
     }
     if (nlive > 0) drain(nlive - 1);
-#ifdef FB_EXP_FULL_WAIT
-    if ((tid & 127) == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-#else
-    // exit only needs the staging box read (the reduce-adds complete with the grid)
-    if ((tid & 127) == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-#endif
     // dK, dV (the last dK/dV MMAs completed before the last dq_full): staged in the now idle
     // Q / dO rings in the 128B-swizzled [chunk][key][64] layout of the K tile, then one TMA
     // bulk store per matrix (coalesced, asynchronous) instead of per-row global stores
@@ -466,6 +623,9 @@ __global__ void __launch_bounds__(320, 1)
   }
   tc_fence_before();
   __syncthreads();
+#ifdef FB_ATTN_PROF
+  if (threadIdx.x == 0 && PROF_CTA() < 8192) g_attn_prof[PROF_CTA() * 8 + 1] = ptimer();
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -477,6 +637,9 @@ __global__ void __launch_bounds__(320, 1)
 // A = the dS^T smem image read MN-major) in its own TMEM columns, two 128 x 32 TMA
 // reduce boxes per tile (one per warpgroup), same cross-tile pipeline as tc64.
 //   TMEM: S^T [0,128)  dP^T [128,256)  dQ [256,320)  dV [320,384)  dK [384,448).
+// dQ staging buffers per warpgroup in the dh 64 kernel: 2 measured 10% slower (the extra 32 KB of
+// smem takes the L1 the E/D and map loads use)
+#define DQ_NBUF 1
 struct AttnBwdD64Cfg {
   static constexpr int DH = 64;
   static constexpr int KT = 128 * DH * 2;        // K or V tile (128 keys)
@@ -487,19 +650,20 @@ struct AttnBwdD64Cfg {
   static constexpr int Q_OFF = V_OFF + KT;       // [2]
   static constexpr int O_OFF = Q_OFF + 2 * QT;   // [2]
   static constexpr int P_OFF = O_OFF + 2 * QT;   // [2] P^T, then dS^T (shared per buffer)
-  static constexpr int X_OFF = P_OFF + 2 * PT;   // dQ staging: 2 boxes of 128 rows x 32 f32 (swizzled)
-  static constexpr int L_OFF = X_OFF + 128 * DH * 4;
+  static constexpr int X_OFF = P_OFF + 2 * PT;   // dQ staging [2 buffers][2 groups][128 rows x 32 f32] (swizzled)
+  static constexpr int L_OFF = X_OFF + DQ_NBUF * 128 * DH * 4;
   static constexpr int BAR_OFF = L_OFF + 2 * 128 * 4;
   static constexpr int SMEM = BAR_OFF + 512 + 1024;
   static_assert(SMEM <= 232448, "attention bwd (dh 64) smem");
 };
 
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(384, 1)
     attn_bwd_tcd64_kernel(const __grid_constant__ CUtensorMap tm_qkv, const __grid_constant__ CUtensorMap tm_do,
-                          const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv, const float* __restrict__ lse2,
+                          const __grid_constant__ CUtensorMap tm_dq, const __grid_constant__ CUtensorMap tm_dkv,
+                          const float* __restrict__ lse2,
                           const uint8_t* __restrict__ live, const float* __restrict__ Dd,
-                          __nv_bfloat16* __restrict__ dqkv, int T, int H,
-                          float scale_log2, float scale, int use_alibi, int det) {
+                          __nv_bfloat16* __restrict__ dqkv, float* __restrict__ dqacc,
+                          uint32_t* __restrict__ sem, int T, int H, float scale_log2, float scale, int use_alibi) {
   using Cf = AttnBwdD64Cfg;
   constexpr int DH = Cf::DH;
   extern __shared__ uint8_t smem_raw[];
@@ -521,11 +685,21 @@ __global__ void __launch_bounds__(320, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
   uint32_t* nlive_p = tmem_slot + 1;
   uint8_t* tl = reinterpret_cast<uint8_t*>(tmem_slot + 2);
+  uint64_t* staged = bar + 35;  // [g][buffer] warpgroup g's dQ box is staged (4 warp arrivals)
+  uint64_t* sfree = bar + 39;   // [g][buffer] dQ warp g is done with that staging buffer
   float* sE = reinterpret_cast<float*>(smem + Cf::L_OFF);
   float* sD = sE + 128;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = blockIdx.x;
+#ifdef FB_ATTN_PROF
+  if (threadIdx.x == 0 && PROF_CTA() < 8192) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_attn_prof[PROF_CTA() * 8 + 0] = ptimer();
+    g_attn_prof[PROF_CTA() * 8 + 3] = smid;
+  }
+#endif
   const int bh = blockIdx.y, b = bh / H, h = bh % H;
   const int d = H * DH;
   const int row0 = b * T;
@@ -535,7 +709,6 @@ __global__ void __launch_bounds__(320, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tm_qkv);
     tma_prefetch(&tm_do);
-    tma_prefetch(&tm_dq);
     mbar_init(kv_full, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(&q_full[s], 1);
@@ -550,6 +723,10 @@ __global__ void __launch_bounds__(320, 1)
     mbar_init(ds_full, 8);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 8);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&staged[i], 4);
+      mbar_init(&sfree[i], 1);
+    }
     fence_barrier_init();
   }
   if (warp == 2) build_live_list(live, bh, T, kb, first, ntiles, 0, tl, nlive_p);
@@ -638,6 +815,61 @@ __global__ void __launch_bounds__(320, 1)
         umma_commit(&pds_free[s]);
       }
     }
+  } else if (warp >= 10) {
+    // dQ warps: warp 10 + g turns warpgroup g's staged 128 x 32 boxes (dh columns 32g..32g+31)
+    // into dQ in the fixed order of dq_order, as in the dh 128 kernel; the staging is
+    // double-buffered here (box t in buffer t & 1), so one slow box does not stall the compute warps
+    const int g = warp - 10;
+    uint32_t ords = 0;  // lane l: dq_order of tile (t & ~31) + l
+    for (int t = 0; t < nlive; ++t) {
+      const int q0 = (first + tl[t]) * 128, sb = DQ_NBUF == 2 ? (t & 1) : 0;
+      const uint32_t xbox = sX + sb * 32768 + g * 16384;
+      if ((t & 31) == 0 && t + lane < nlive) ords = dq_order_lane(live, bh, T, first + tl[t + lane], kb);
+      const uint32_t ord = __shfl_sync(0xffffffffu, ords, t & 31), cnt = ord & 0xffu;
+      uint32_t* bsem = sem + ((int64_t)bh * (T / 128) + q0 / 128) * 2 + g;
+      mbar_wait(&staged[2 * g + sb], DQ_NBUF == 2 ? ((t >> 1) & 1) : (t & 1));
+      if (lane == 0 && cnt) sem_wait_eq(bsem, cnt);
+      __syncwarp();
+      if (ord & 0x100u) {  // last contributor: lane owns rows lane + 32k, 32 columns each
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {  // one row (8 accumulator loads in flight) at a time: register budget
+          const int r = lane + 32 * k;
+          const float* acc = dqacc + (int64_t)(row0 + q0 + r) * d + h * DH + 32 * g;
+          __nv_bfloat16* out = dqkv + (int64_t)(row0 + q0 + r) * (3 * d) + h * DH + 32 * g;
+          float4 a[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            a[q] = cnt ? __ldcg(reinterpret_cast<const float4*>(acc) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int q = 0; q < 8; q += 2) {
+            float4 x0, x1;
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(x0.x), "=f"(x0.y), "=f"(x0.z), "=f"(x0.w)
+                         : "r"(xbox + r * 128 + ((q ^ (r & 7)) << 4)));
+            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                         : "=f"(x1.x), "=f"(x1.y), "=f"(x1.z), "=f"(x1.w)
+                         : "r"(xbox + r * 128 + (((q + 1) ^ (r & 7)) << 4)));
+            if (cnt) {
+              x0 = make_float4(a[q].x + x0.x, a[q].y + x0.y, a[q].z + x0.z, a[q].w + x0.w);
+              x1 = make_float4(a[q + 1].x + x1.x, a[q + 1].y + x1.y, a[q + 1].z + x1.z, a[q + 1].w + x1.w);
+            }
+            *reinterpret_cast<uint4*>(out + 4 * q) =
+                make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sfree[2 * g + sb]);
+      } else if (lane == 0) {
+        dq_out_box(&tm_dq, xbox, h * DH + 32 * g, row0 + q0, cnt == 0);
+        bulk_commit();
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        mbar_arrive(&sfree[2 * g + sb]);
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        sem_release(bsem);
+      }
+      __syncwarp();
+    }
+    if (g == 0) zero_dead_rows(live, bh, T, kb, DH, H, row0, h, dqkv, lane, 32);
   } else {
     const int g = (warp - 2) >> 2;
     const int quad = warp & 3;
@@ -647,9 +879,7 @@ __global__ void __launch_bounds__(320, 1)
     const float sl = use_alibi ? exp2f(-8.0f * (float)(h + 1) / (float)H) * 1.4426950408889634f : 0.0f;
     const float slk = sl * (float)kj;
     const int tid = threadIdx.x - 64;
-    const uint32_t xbox = sX + g * 16384;  // this warpgroup's 128 x 32 f32 staging box
-    auto drain = [&](int t) {
-      const int q0 = (first + tl[t]) * 128;
+    auto drain = [&](int t) {  // dQ(t) -> warpgroup g's staging box, handed to dQ warp g
       mbar_wait(dq_full, t & 1);
       tc_fence_after();
       uint32_t v[32];
@@ -658,8 +888,11 @@ __global__ void __launch_bounds__(320, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
-      if (quad == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
+      PROF_T0(pf);
+      const int sb = DQ_NBUF == 2 ? (t & 1) : 0;
+      const uint32_t xbox = sX + sb * 32768 + g * 16384;  // this warpgroup's 128 x 32 f32 box
+      mbar_wait(&sfree[2 * g + sb], (DQ_NBUF == 2 ? ((t >> 1) & 1) : (t & 1)) ^ 1);  // dQ warp g is done with it
+      if (lane == 0 && quad == 0) PROF_ADD(6, pf);
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const uint32_t addr = xbox + r * 128 + ((q ^ (r & 7)) << 4);
@@ -667,12 +900,9 @@ __global__ void __launch_bounds__(320, 1)
                      "f"(__uint_as_float(v[4 * q + 1]) * scale), "f"(__uint_as_float(v[4 * q + 2]) * scale),
                      "f"(__uint_as_float(v[4 * q + 3]) * scale));
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
-      if (quad == 0 && lane == 0) {
-        dq_out_box(&tm_dq, xbox, h * DH + 32 * g, row0 + q0, kb, det);
-        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the TMA reads the box
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&staged[2 * g + sb]);
     };
     for (int t = 0; t < nlive; ++t) {
       const int s = t & 1;
@@ -754,7 +984,6 @@ __global__ void __launch_bounds__(320, 1)
       if (t > 0) drain(t - 1);
     }
     if (nlive > 0) drain(nlive - 1);
-    if (quad == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     // dK / dV staged in the idle Q / dO buffers (128B-swizzled [key][64]), two TMA bulk stores
     uint8_t* stK = smem + Cf::Q_OFF;
     uint8_t* stV = smem + Cf::O_OFF;
@@ -789,6 +1018,9 @@ __global__ void __launch_bounds__(320, 1)
   }
   tc_fence_before();
   __syncthreads();
+#ifdef FB_ATTN_PROF
+  if (threadIdx.x == 0 && PROF_CTA() < 8192) g_attn_prof[PROF_CTA() * 8 + 1] = ptimer();
+#endif
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
@@ -796,21 +1028,6 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_enc_bwd = nullptr;
-
-static int encode_rows_map(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_chunks) {
-  cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64)};
-  cuuint64_t strides[2] = {(cuuint64_t)cols * 2, 128};
-  cuuint32_t box[3] = {64, 128, (cuuint32_t)box_chunks};
-  cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = g_enc_bwd(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) {
-    set_error("attn bwd tensor map encode failed: %d", (int)r);
-    return FB_CUDA_ERROR;
-  }
-  return FB_OK;
-}
 
 static int encode_box(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_rows, int box_chunks) {
   cuuint64_t dims[3] = {64, (cuuint64_t)rows, (cuuint64_t)(cols / 64)};
@@ -827,86 +1044,79 @@ static int encode_box(CUtensorMap* m, const void* base, int64_t rows, int cols, 
   return FB_OK;
 }
 
+// {d, rows, 1} f32 map with box_cols x box_rows boxes (the dQ accumulator)
+static int encode_f32_box(CUtensorMap* m, void* base, int64_t rows, int d, int box_cols, int box_rows,
+                          CUtensorMapSwizzle swz) {
+  cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, 1};
+  cuuint64_t strides[2] = {(cuuint64_t)d * 4, (cuuint64_t)rows * d * 4};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_enc_bwd(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("attn bwd dq tensor map encode failed: %d", (int)r);
+    return FB_CUDA_ERROR;
+  }
+  return FB_OK;
+}
+
 static int attn_bwd_tc64_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live,
-                                const float* Dbuf, float* dq,
-                                void* dqkv, int B, int T, int H, int use_alibi, int det, cudaStream_t st) {
+                                const float* Dbuf, float* dq, uint32_t* sem,
+                                void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
   using Cf = AttnBwd64Cfg;
   constexpr int DH = 128;
   const int d = H * DH;
-  CUtensorMap tkv, tq, to, tdq;
+  CUtensorMap tkv, tq, to;
   int rc = encode_box(&tkv, qkv, (int64_t)B * T, 3 * d, 128, DH / 64);
   if (rc) return rc;
   rc = encode_box(&tq, qkv, (int64_t)B * T, 3 * d, 64, DH / 64);
   if (rc) return rc;
   rc = encode_box(&to, dO, (int64_t)B * T, d, 64, DH / 64);
   if (rc) return rc;
-  {
-    // {d, B*T, slabs}: slabs = 1 (reduce-add accumulator) or T/128 (deterministic per-key-block partials)
-    const int slabs = det ? T / 128 : 1;
-    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)B * T, (cuuint64_t)slabs};
-    cuuint64_t strides[2] = {(cuuint64_t)d * 4, (cuuint64_t)B * T * d * 4};
-    cuuint32_t box[3] = {DH, 32, 1};  // one 32-query box per warpgroup
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = g_enc_bwd(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dq, dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      set_error("attn bwd dq tensor map encode failed: %d", (int)r);
-      return FB_CUDA_ERROR;
-    }
-  }
+  CUtensorMap tdq;  // the f32 accumulator of the ordered dQ partials: one 32 x 128 box per warpgroup
+  rc = encode_f32_box(&tdq, dq, (int64_t)B * T, d, DH, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (rc) return rc;
   CUtensorMap tdkv;  // dK / dV store boxes: 128 keys x 128 dh (two 64-column chunks), 128B swizzle
   rc = encode_box(&tdkv, dqkv, (int64_t)B * T, 3 * d, 128, DH / 64);
   if (rc) return rc;
   auto k = attn_bwd_tc64_kernel;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale = 1.0f / sqrtf((float)DH);
-  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tkv, tq, to, tdq, tdkv, lse, live, Dbuf, (__nv_bfloat16*)dqkv, T, H,
-                                                 1.4426950408889634f * scale, scale, use_alibi, det);
+  k<<<dim3(T / 128, B * H), 384, Cf::SMEM, st>>>(tkv, tq, to, tdq, tdkv, lse, live, Dbuf, (__nv_bfloat16*)dqkv, dq,
+                                                 sem, T, H, 1.4426950408889634f * scale, scale, use_alibi);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }
 
 static int attn_bwd_tcd64_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live,
-                                 const float* Dbuf, float* dq,
-                                 void* dqkv, int B, int T, int H, int use_alibi, int det, cudaStream_t st) {
+                                 const float* Dbuf, float* dq, uint32_t* sem,
+                                 void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
   using Cf = AttnBwdD64Cfg;
   constexpr int DH = 64;
   const int d = H * DH;
-  CUtensorMap tq, to, tdq;
+  CUtensorMap tq, to;
   int rc = encode_box(&tq, qkv, (int64_t)B * T, 3 * d, 128, 1);
   if (rc) return rc;
   rc = encode_box(&to, dO, (int64_t)B * T, d, 128, 1);
   if (rc) return rc;
-  {
-    const int slabs = det ? T / 128 : 1;
-    cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)B * T, (cuuint64_t)slabs};
-    cuuint64_t strides[2] = {(cuuint64_t)d * 4, (cuuint64_t)B * T * d * 4};
-    cuuint32_t box[3] = {32, 128, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = g_enc_bwd(&tdq, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, dq, dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      set_error("attn bwd dq tensor map encode failed: %d", (int)r);
-      return FB_CUDA_ERROR;
-    }
-  }
+  CUtensorMap tdq;  // the f32 accumulator of the ordered dQ partials: 128 x 32 boxes, 128B swizzle
+  rc = encode_f32_box(&tdq, dq, (int64_t)B * T, d, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  if (rc) return rc;
   CUtensorMap tdkv;  // dK / dV store boxes: 128 keys x 64 dh, 128B swizzle
   rc = encode_box(&tdkv, dqkv, (int64_t)B * T, 3 * d, 128, 1);
   if (rc) return rc;
   auto k = attn_bwd_tcd64_kernel;
   FB_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
   const float scale = 1.0f / sqrtf((float)DH);
-  k<<<dim3(T / 128, B * H), 320, Cf::SMEM, st>>>(tq, to, tdq, tdkv, lse, live, Dbuf, (__nv_bfloat16*)dqkv, T, H,
-                                                 1.4426950408889634f * scale, scale, use_alibi, det);
+  k<<<dim3(T / 128, B * H), 384, Cf::SMEM, st>>>(tq, to, tdq, tdkv, lse, live, Dbuf, (__nv_bfloat16*)dqkv, dq, sem,
+                                                 T, H, 1.4426950408889634f * scale, scale, use_alibi);
   FB_LAUNCH_CHECK();
   return FB_OK;
 }
 
 template <int DH>
 int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const uint8_t* live, const float* Dbuf,
-                       float* dq, void* dqkv, int B, int T, int H, int use_alibi, int det, cudaStream_t st) {
+                       float* dq, uint32_t* sem, void* dqkv, int B, int T, int H, int use_alibi, cudaStream_t st) {
   if (!g_enc_bwd) {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -918,18 +1128,29 @@ int attn_bwd_tc_launch(const void* qkv, const void* dO, const float* lse, const 
     g_enc_bwd = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   FB_REQUIRE(T <= 16384, "attn_bwd: T=%d above 16384", T);
-  if (DH == 128) return attn_bwd_tc64_launch(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, det, st);
-  if (DH == 64) return attn_bwd_tcd64_launch(qkv, dO, lse, live, Dbuf, dq, dqkv, B, T, H, use_alibi, det, st);
+  // the box counters of dq_order start at 0 (B*H*T/32 words: 32 KB at the C4 shape)
+  FB_CUDA_TRY(cudaMemsetAsync(sem, 0, sizeof(uint32_t) * (size_t)B * H * (T / 32), st));
+  if (DH == 128) return attn_bwd_tc64_launch(qkv, dO, lse, live, Dbuf, dq, sem, dqkv, B, T, H, use_alibi, st);
+  if (DH == 64) return attn_bwd_tcd64_launch(qkv, dO, lse, live, Dbuf, dq, sem, dqkv, B, T, H, use_alibi, st);
   return FB_UNSUPPORTED;
 }
 
 template int attn_bwd_tc_launch<64>(const void*, const void*, const float*, const uint8_t*, const float*, float*,
-                                    void*, int, int, int, int, int, cudaStream_t);
+                                    uint32_t*, void*, int, int, int, int, cudaStream_t);
 template int attn_bwd_tc_launch<128>(const void*, const void*, const float*, const uint8_t*, const float*, float*,
-                                     void*, int, int, int, int, int, cudaStream_t);
+                                     uint32_t*, void*, int, int, int, int, cudaStream_t);
 
 }  // namespace fb
 
+#ifdef FB_ATTN_PROF
+extern "C" int fb_attn_prof_read(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, fb::g_attn_prof, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : 2;
+}
+extern "C" int fb_attn_prof_clear() {
+  static unsigned long long z[8192 * 8];
+  return cudaMemcpyToSymbol(fb::g_attn_prof, z, sizeof(z)) == cudaSuccess ? 0 : 2;
+}
+#endif
 #ifdef FB_ATTN_TRACE
 extern "C" int fb_attn_trace_read(unsigned long long* out, int n) {
   return cudaMemcpyFromSymbol(out, fb::g_attn_trace, n * sizeof(unsigned long long)) == cudaSuccess ? 0 : 2;

@@ -10,8 +10,7 @@
 // One warp per (b, h, row). Lanes split the head dim (lane owns c = lane + 32 e), so a
 // score is one warp reduction; keys (forward, dQ) or queries (dK/dV) are walked in
 // ascending order, so every output is a fixed-order sum: the backward is deterministic
-// (no atomics), which is also why it serves as the deterministic-mode backward for the
-// tensor-core shapes (fb_set_deterministic).
+// (no atomics).
 #include "common.cuh"
 
 namespace fb {

@@ -105,10 +105,9 @@ def test_attention_dead_block_skip_is_exact(fb, B, T, H, dh):
     o1, l1, g1 = _attn_run(fb, qkv, do, B, T, H, dh, live)
     o0, l0, g0 = _attn_run(fb, qkv, do, B, T, H, dh, None)
     assert torch.equal(o1, o0) and torch.equal(l1, l0)
-    # dK / dV come from one CTA each: bit-identical. dQ is reduce-added across key blocks by
-    # the TMA (f32 adds in arrival order), so it is identical only up to summation order.
-    assert torch.equal(g1[:, H * dh:], g0[:, H * dh:])
-    torch.testing.assert_close(g1[:, :H * dh].float(), g0[:, :H * dh].float(), atol=1e-2, rtol=1e-2)
+    # dK / dV come from one CTA each; dQ adds the key blocks' partials in descending key-block
+    # order, and a skipped (dead) partial is an exact 0 in the unmapped run: all bit-identical
+    assert torch.equal(g1, g0)
     m = live.view(B, H, T // 128, T // 64).cpu().numpy()
     causal = np.array([[kt <= 2 * qt + 1 for kt in range(T // 64)] for qt in range(T // 128)])
     vals = m[:, :, causal]
@@ -317,7 +316,7 @@ def test_outproj_dgrad_rowdot_feeds_attention_bwd(fb, B, T, H, dh):
     assert rc == 0
     work = torch.empty(int(fb.lib().fb_attn_bwd_work_floats(B, T, H, dh)), dtype=torch.float32, device=dev)
     work[: B * H * T].copy_(D)
-    work[B * H * T:].fill_(123.0)  # the D_READY path must zero dQ itself
+    work[B * H * T:].fill_(123.0)  # garbage accumulator and box counters: the call must not depend on them
     g1 = torch.empty_like(qkv)
     g2 = torch.empty_like(qkv)
     fb.call("fb_attn_bwd_ex", qkv.data_ptr(), o.data_ptr(), dO.data_ptr(), lse2.data_ptr(), live.data_ptr(),
@@ -330,11 +329,12 @@ def test_outproj_dgrad_rowdot_feeds_attention_bwd(fb, B, T, H, dh):
     torch.testing.assert_close(g1.float(), g2.float(), atol=2e-2, rtol=2e-2)
 
 
-@pytest.mark.parametrize("B,T,H,dh", [(2, 512, 4, 128), (2, 1024, 3, 64), (1, 2048, 16, 128)])
+@pytest.mark.parametrize("B,T,H,dh", [(2, 512, 4, 128), (2, 1024, 3, 64), (1, 2048, 16, 128), (2, 2048, 12, 64)])
 def test_attention_bwd_deterministic_mode(fb, B, T, H, dh):
-    """fb_set_deterministic(1): the tcgen05 backward stores per-key-block dQ slabs and sums them
-    in key-block order — two runs are bitwise equal; dK/dV are the default mode's bits and dQ
-    equals it up to f32 summation order."""
+    """The tcgen05 backward adds each query block's dQ partials in descending key-block order
+    (per-box counters) and writes bf16 dQ itself: every run is bitwise equal, whatever
+    fb_set_deterministic says (ABI 3), and no dQ byte of the output is left from before the call
+    (dqkv pre-filled with NaN)."""
     torch.manual_seed(9)
     dev = torch.device("cuda")
     d = H * dh
@@ -346,16 +346,16 @@ def test_attention_bwd_deterministic_mode(fb, B, T, H, dh):
     st = fb.stream_handle()
     fb.call("fb_attn_fwd", qkv.data_ptr(), o.data_ptr(), lse2.data_ptr(), live.data_ptr(), B, T, H, dh, 1, st)
     outs = []
-    for det in (0, 1, 1):
+    for det in (0, 1, 1, 0):
         fb.call("fb_set_deterministic", det)
         nw = int(fb.lib().fb_attn_bwd_work_floats(B, T, H, dh))
-        work = torch.empty(nw, dtype=torch.float32, device=dev)
-        dqkv = torch.empty_like(qkv)
+        work = torch.full((nw,), float("nan"), dtype=torch.float32, device=dev)
+        dqkv = torch.full_like(qkv, float("nan"))
         fb.call("fb_attn_bwd", qkv.data_ptr(), o.data_ptr(), do.data_ptr(), lse2.data_ptr(), live.data_ptr(),
                 dqkv.data_ptr(), work.data_ptr(), B, T, H, dh, 1, st)
         outs.append(dqkv)
     fb.call("fb_set_deterministic", 1)  # the library default
     torch.cuda.synchronize()
-    assert torch.equal(outs[1], outs[2])                      # replay: bitwise
-    assert torch.equal(outs[0][:, d:], outs[1][:, d:])        # dK, dV: the same MMAs
-    torch.testing.assert_close(outs[1][:, :d].float(), outs[0][:, :d].float(), atol=1e-2, rtol=1e-2)
+    assert torch.isfinite(outs[0].float()).all()
+    for x in outs[1:]:
+        assert torch.equal(outs[0], x)

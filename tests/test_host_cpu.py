@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     assert len(syms) >= 25
     missing = [s for s in syms if not hasattr(L, s)]
     assert not missing, missing
-    assert L.fb_abi_version() == 2
+    assert L.fb_abi_version() == 3
     # every declared entry has a ctypes signature in the binding
     bound = set(ext.SIGNATURES) | {"fb_last_error", "fb_model_n_params", "fb_model_workspace_bytes",
                                      "fb_embed_bwd_work_bytes", "fb_lmhead_ce_work_floats",
