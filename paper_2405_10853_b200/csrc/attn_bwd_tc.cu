@@ -7,7 +7,7 @@
 //
 // CTA = 128 keys of one (b, h); loop over the causal query tiles. Two kernels:
 //   dh = 128  attn_bwd_tc64_kernel: 64-query tiles, P^T in TMEM (dV as an A-from-TMEM
-//             MMA), 3-stage Q/dO ring, dQ^T = K^T dS^T in its own TMEM columns, one
+//             MMA), 2-stage Q/dO ring, dQ^T = K^T dS^T in its own TMEM columns, one
 //             ordered dQ box per warpgroup per tile (dq_order), software pipeline across
 //             query tiles (elementwise of tile t+1 overlaps the MMAs of tile t).
 //   dh = 64   attn_bwd_tcd64_kernel: 128-query tiles, dQ = dS K with dS^T read as an
@@ -234,15 +234,18 @@ __device__ __forceinline__ void zero_dead_rows(const uint8_t* __restrict__ live,
 //   MMA order per tile t:  [pds_full(t)]  S^T(t+1), dP^T(t+1)  dV(t)  dK(t)  [dq_empty(t-1)] dQ^T(t)
 //   so the elementwise phase of tile t+1 overlaps the dV/dK/dQ MMAs of tile t.
 //   dQ^T = K^T dS^T (M = dh = 128, N = 64 queries, K = 128 keys) has its own TMEM columns;
-//   it is drained by the compute warps of the NEXT tile through a dedicated smem staging
-//   box and ONE TMA bulk reduce-add per tile (dq rows [q0, q0+64) x 128 cols).
-//   P^T (bf16 pairs) goes to TMEM and dV = P^T dO is an A-from-TMEM MMA; the 32 KB of
-//   smem that P^T no longer needs buy a third Q / dO stage, so the loads of tile t+2 are
-//   not gated by the dV / dK MMAs of tile t.
+//   it is drained by the compute warps of the NEXT tile into their warpgroup's 32 x 128 f32
+//   staging box (double-buffered) and handed to a dQ warp, which adds it in the fixed
+//   order of dq_order. P^T (bf16 pairs) goes to TMEM and dV = P^T dO is an A-from-TMEM MMA;
+//   the 32 KB of smem that P^T no longer needs hold the second staging buffer (the Q / dO
+//   ring is 2 deep).
 //   TMEM: S^T [0,64)  dP^T [64,128)  dQ^T [128,192)  P^T[2] [192,256)  dV [256,384)  dK [384,512).
+// dQ staging buffers per warpgroup in the dh 128 kernel: 2 (the Q / dO ring gives up its third
+// stage for them) measured 0.977 vs 1.003 ms at the C4 shape with 1 buffer and NQ = 3
+#define DQ128_NBUF 2
 struct AttnBwd64Cfg {
   static constexpr int DH = 128;
-  static constexpr int NQ = 3;                   // Q / dO ring depth
+  static constexpr int NQ = DQ128_NBUF == 2 ? 2 : 3;  // Q / dO ring depth
   static constexpr int KT = 128 * DH * 2;        // K or V tile (128 keys)
   static constexpr int QT = 64 * DH * 2;         // Q or dO tile (64 queries)
   static constexpr int PT = 128 * 64 * 2;        // dS^T tile (128 keys x 64 q)
@@ -251,8 +254,8 @@ struct AttnBwd64Cfg {
   static constexpr int Q_OFF = V_OFF + KT;       // [NQ]
   static constexpr int O_OFF = Q_OFF + NQ * QT;  // [NQ]
   static constexpr int S_OFF = O_OFF + NQ * QT;  // [2]
-  static constexpr int X_OFF = S_OFF + 2 * PT;   // dQ staging: 64 rows x 128 f32
-  static constexpr int L_OFF = X_OFF + 64 * DH * 4;  // e[2][64], D[2][64]
+  static constexpr int X_OFF = S_OFF + 2 * PT;   // dQ staging: [DQ128_NBUF][64 rows x 128 f32]
+  static constexpr int L_OFF = X_OFF + DQ128_NBUF * 64 * DH * 4;  // e[2][64], D[2][64]
   static constexpr int BAR_OFF = L_OFF + 4 * 64 * 4;
   static constexpr int SMEM = BAR_OFF + 512 + 1024;  // mbarriers, TMEM slot, live count + list; align
   static_assert(SMEM <= 232448, "attention bwd (dh 128) smem");
@@ -284,8 +287,8 @@ __global__ void __launch_bounds__(384, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 20);
   uint32_t* nlive_p = tmem_slot + 1;
   uint8_t* tl = reinterpret_cast<uint8_t*>(tmem_slot + 2);
-  uint64_t* staged = bar + 60;  // [2] warpgroup g's dQ box is in its staging area (4 warp arrivals)
-  uint64_t* sfree = bar + 62;   // [2] dQ warp g is done with that staging area
+  uint64_t* staged = bar + 56;  // [g][buffer] warpgroup g's dQ box is staged (4 warp arrivals)
+  uint64_t* sfree = bar + 60;   // [g][buffer] dQ warp g is done with that staging buffer
   float* sE0 = reinterpret_cast<float*>(smem + Cf::L_OFF);  // e[2][64] (double-buffered)
   float* sD0 = sE0 + 128;                                     // D[2][64]
 
@@ -321,9 +324,9 @@ __global__ void __launch_bounds__(384, 1)
     mbar_init(pds_full, 8);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 8);
-    for (int g = 0; g < 2; ++g) {
-      mbar_init(&staged[g], 4);
-      mbar_init(&sfree[g], 1);
+    for (int i = 0; i < 4; ++i) {
+      mbar_init(&staged[i], 4);
+      mbar_init(&sfree[i], 1);
     }
     fence_barrier_init();
 #ifndef FB_EXP_LATE_KV
@@ -429,14 +432,16 @@ __global__ void __launch_bounds__(384, 1)
     // completed, or acc + box -> bf16 dqkv (last). The counter waits, bulk-op completions and
     // release fences stay off the compute warps.
     const int g = warp - 10;
-    const float* Xg = reinterpret_cast<const float*>(smem + Cf::X_OFF) + g * 32 * DH;
     uint32_t ords = 0;  // lane l: dq_order of tile (t & ~31) + l
     for (int t = 0; t < nlive; ++t) {
       const int q0 = (first + tl[t]) * 64, qrow = q0 + 32 * g;
+      const int sb = DQ128_NBUF == 2 ? (t & 1) : 0;
+      const uint32_t sph = DQ128_NBUF == 2 ? ((t >> 1) & 1) : (t & 1);
+      const float* Xg = reinterpret_cast<const float*>(smem + Cf::X_OFF) + (sb * 64 + g * 32) * DH;
       if ((t & 31) == 0 && t + lane < nlive) ords = dq_order_lane(live, bh, T, (first + tl[t + lane]) >> 1, kb);
       const uint32_t ord = __shfl_sync(0xffffffffu, ords, t & 31), cnt = ord & 0xffu;
       uint32_t* bsem = sem + (int64_t)bh * (T / 32) + qrow / 32;
-      mbar_wait(&staged[g], t & 1);
+      mbar_wait(&staged[2 * g + sb], sph);
       if (lane == 0 && cnt) sem_wait_eq(bsem, cnt);  // every larger live key block has added its partial
       __syncwarp();
       if (ord & 0x100u) {  // last contributor: dQ = acc + partial, bf16 (lane: 4 dh columns x 32 rows)
@@ -454,12 +459,12 @@ __global__ void __launch_bounds__(384, 1)
           *reinterpret_cast<uint2*>(out + (int64_t)i * (3 * d)) = make_uint2(pack_bf16(x.x, x.y), pack_bf16(x.z, x.w));
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&sfree[g]);
+        if (lane == 0) mbar_arrive(&sfree[2 * g + sb]);
       } else if (lane == 0) {
         dq_out_box(&tm_dq, smem_u32(Xg), h * DH, row0 + qrow, cnt == 0);
         bulk_commit();
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        mbar_arrive(&sfree[g]);
+        mbar_arrive(&sfree[2 * g + sb]);
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         sem_release(bsem);  // at once: the next key block waits on it
       }
@@ -487,17 +492,19 @@ __global__ void __launch_bounds__(384, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(dq_empty);
       PROF_T0(pf);
-      mbar_wait(&sfree[g], (t & 1) ^ 1);  // dQ warp g is done with this group's previous box
+      const int sb = DQ128_NBUF == 2 ? (t & 1) : 0;
+      mbar_wait(&sfree[2 * g + sb], (DQ128_NBUF == 2 ? ((t >> 1) & 1) : (t & 1)) ^ 1);  // dQ warp g is done with it
+      float* Xb = Xs + sb * 64 * DH;
       if (lane == 0 && quad == 0) PROF_ADD(6, pf);
 #pragma unroll
       for (int i = 0; i < 32; i += 2) {
         const float2 sv2 = pk_mul(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), make_float2(scale, scale));
-        Xs[(32 * g + i) * DH + r] = sv2.x;
-        Xs[(32 * g + i + 1) * DH + r] = sv2.y;
+        Xb[(32 * g + i) * DH + r] = sv2.x;
+        Xb[(32 * g + i + 1) * DH + r] = sv2.y;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the TMA reads the box
       __syncwarp();
-      if (lane == 0) mbar_arrive(&staged[g]);
+      if (lane == 0) mbar_arrive(&staged[2 * g + sb]);
       // publishes the e/D that load_ed wrote just before (read in the next tile's elementwise)
       asm volatile("bar.sync %0, 128;" ::"r"(2 + g) : "memory");
     };
