@@ -10,10 +10,10 @@
 //             MMA), 2-stage Q/dO ring, dQ^T = K^T dS^T in its own TMEM columns, one
 //             ordered dQ box per warpgroup per tile (dq_order), software pipeline across
 //             query tiles (elementwise of tile t+1 overlaps the MMAs of tile t).
-//   dh = 64   attn_bwd_tcd64_kernel: 128-query tiles, dQ = dS K with dS^T read as an
-//             MN-major A operand, P/dS share a double-buffered smem tile.
+//   dh = 64   attn_bwd_tcd64_kernel: 128-query tiles, P^T in TMEM (A-from-TMEM dV), dS^T in a
+//             double-buffered smem tile, dQ = dS K with dS^T read as an MN-major A operand.
 // Warp roles in both: warp 0 TMA producer, warp 1 TMEM owner + single-thread MMA issuer,
-// warps 2-9 elementwise (thread = TMEM lane).
+// warps 2-9 elementwise (thread = TMEM lane), warps 10-11 ordered dQ output (dq_order).
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
@@ -641,9 +641,11 @@ __global__ void __launch_bounds__(384, 1)
 
 // ---------------------------------------------------------------------------------------
 // dh = 64 variant of the pipelined backward: 128-query tiles, dQ = dS K (M = 128 queries,
-// A = the dS^T smem image read MN-major) in its own TMEM columns, two 128 x 32 TMA
-// reduce boxes per tile (one per warpgroup), same cross-tile pipeline as tc64.
-//   TMEM: S^T [0,128)  dP^T [128,256)  dQ [256,320)  dV [320,384)  dK [384,448).
+// A = the dS^T smem image read MN-major) in its own TMEM columns, two 128 x 32 dQ boxes per
+// tile (one per warpgroup). MMA order per tile t: [p_full(t)] dV(t) (P^T from TMEM)
+// S^T/dP^T(t+1) dK(t) [dq_empty] dQ(t): the compute warps never wait for dV before writing
+// dS^T (round 1 shared one smem tile between P^T and dS^T and stalled on it every tile).
+//   TMEM: S^T [0,128)  dP^T [128,256)  dQ [256,320)  dV [320,384)  dK [384,448)  P^T [448,512).
 // dQ staging buffers per warpgroup in the dh 64 kernel: 2 measured 10% slower (the extra 32 KB of
 // smem takes the L1 the E/D and map loads use)
 #define DQ_NBUF 1
@@ -683,12 +685,10 @@ __global__ void __launch_bounds__(384, 1)
   uint64_t* q_empty = bar + 5;    // [2]
   uint64_t* o_empty = bar + 7;    // [2]
   uint64_t* s_full = bar + 9;
-  uint64_t* p_full = bar + 10;
+  uint64_t* p_full = bar + 10;    // P^T(t) in TMEM and dS^T(t) in smem (8 compute warps)
   uint64_t* pds_free = bar + 11;  // [2]
   uint64_t* dq_full = bar + 13;
   uint64_t* dq_empty = bar + 14;
-  uint64_t* p_free = bar + 15;
-  uint64_t* ds_full = bar + 16;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 17);
   uint32_t* nlive_p = tmem_slot + 1;
   uint8_t* tl = reinterpret_cast<uint8_t*>(tmem_slot + 2);
@@ -726,8 +726,6 @@ __global__ void __launch_bounds__(384, 1)
     }
     mbar_init(s_full, 1);
     mbar_init(p_full, 8);
-    mbar_init(p_free, 1);
-    mbar_init(ds_full, 8);
     mbar_init(dq_full, 1);
     mbar_init(dq_empty, 8);
     for (int i = 0; i < 4; ++i) {
@@ -769,7 +767,7 @@ __global__ void __launch_bounds__(384, 1)
       constexpr uint32_t idSP = idesc_bf16_f32(128, 128, 0, 0);
       constexpr uint32_t idKV = idesc_bf16_f32(128, DH, 0, 1);
       constexpr uint32_t idQ = idesc_bf16_f32(128, DH, 1, 1);
-      const uint32_t tS = tmem, tP = tmem + 128, tQ = tmem + 256, tV = tmem + 320, tK = tmem + 384;
+      const uint32_t tS = tmem, tP = tmem + 128, tQ = tmem + 256, tV = tmem + 320, tK = tmem + 384, tPT = tmem + 448;
       auto issue_sp = [&](int t) {
         const int s = t & 1;
         const uint32_t sph = (t >> 1) & 1;
@@ -791,20 +789,16 @@ __global__ void __launch_bounds__(384, 1)
         const int s = t & 1;
         const uint32_t ph = t & 1;
         const uint32_t sQ = sQ0 + s * Cf::QT, sO = sO0 + s * Cf::QT;
-        const uint32_t sP = sP0 + s * Cf::PT, sS = sP;  // dS^T overwrites P^T after dV
-        mbar_wait(p_full, ph);
-        if (t + 1 < nlive) issue_sp(t + 1);
+        const uint32_t sS = sP0 + s * Cf::PT;  // dS^T(t)
+        mbar_wait(p_full, ph);  // P^T(t) in TMEM, dS^T(t) in smem
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {  // dV += P^T dO  (K = 128 queries)
-          const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
-          umma_f16(tV, smem_desc_sw128(sP + aoff, 16, 1024), smem_desc_sw128(sO + kk * 2048, 128 * 128, 1024), idKV,
-                   (t | kk) > 0);
-        }
+        for (int kk = 0; kk < 8; ++kk)  // dV += P^T dO  (K = 128 queries; P^T from TMEM)
+          umma_ts_b(tV, tPT + 8 * kk, smem_desc_sw128(sO + kk * 2048, 128 * 128, 1024), idKV, (t | kk) > 0);
         umma_commit(&o_empty[s]);
-        umma_commit(p_free);
-        mbar_wait(ds_full, ph);
-        tc_fence_after();
+        // S^T / dP^T(t+1) after dV(t): s_full(t+1) then also covers dV(t)'s read of P^T(t), which the
+        // compute warps overwrite with P^T(t+1)
+        if (t + 1 < nlive) issue_sp(t + 1);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // dK += dS^T Q
           const uint32_t aoff = (kk >> 2) * (128 * 128) + (kk & 3) * 32;
@@ -930,7 +924,7 @@ __global__ void __launch_bounds__(384, 1)
       tmem_ld_wait();
       if (t >= 2) mbar_wait(&pds_free[s], ((t >> 1) & 1) ^ 1);
       const uint32_t prow = sP0 + s * Cf::PT + r * 128;
-      uint32_t dsp[32];  // dS^T packed bf16x2, written once dV has consumed P^T
+      uint32_t ptm[32];  // this group's 64 queries of P^T as bf16 pairs -> TMEM (A of the dV MMA)
       // the causal mask only touches the diagonal tile: the other tiles run a mask-free copy
       auto elementwise = [&](auto diag_t) {
         constexpr bool kDiag = decltype(diag_t)::value;
@@ -960,34 +954,23 @@ __global__ void __launch_bounds__(384, 1)
               ds[i + 1] = d2.y;
             }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) dsp[c * 16 + q * 4 + i] = pack_bf16(ds[2 * i], ds[2 * i + 1]);
+            for (int i = 0; i < 4; ++i) ptm[c * 16 + q * 4 + i] = pack_bf16(p[2 * i], p[2 * i + 1]);
             const int kc = 8 * g + 4 * c + q;  // 8-query chunk 0..15
             const uint32_t sw = (kc >> 3) * (128 * 128) + (((kc & 7) ^ (r & 7)) << 4);
-            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(pack_bf16(p[0], p[1])),
-                         "r"(pack_bf16(p[2], p[3])), "r"(pack_bf16(p[4], p[5])), "r"(pack_bf16(p[6], p[7])));
+            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(pack_bf16(ds[0], ds[1])),
+                         "r"(pack_bf16(ds[2], ds[3])), "r"(pack_bf16(ds[4], ds[5])), "r"(pack_bf16(ds[6], ds[7])));
           }
         }
       };
       if (diag) elementwise(std::true_type{});
       else elementwise(std::false_type{});
+      // P^T(t) over P^T(t-1): dV(t-1) finished before s_full(t) fired (it was issued before S^T(t))
+      tmem_st_32x32b_x32(tmem + 448 + 32 * g + lane_off, ptm);
+      tmem_st_wait();
       tc_fence_before();
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full);
-      mbar_wait(p_free, ph);  // dV(t) has read P^T: overwrite with dS^T
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int kc = 8 * g + 4 * c + q;
-          const uint32_t sw = (kc >> 3) * (128 * 128) + (((kc & 7) ^ (r & 7)) << 4);
-          asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(prow + sw), "r"(dsp[c * 16 + q * 4]),
-                       "r"(dsp[c * 16 + q * 4 + 1]), "r"(dsp[c * 16 + q * 4 + 2]), "r"(dsp[c * 16 + q * 4 + 3]));
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mbar_arrive(ds_full);
       if (t > 0) drain(t - 1);
     }
     if (nlive > 0) drain(nlive - 1);
