@@ -63,6 +63,32 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
   asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u64of(a)), "l"(u64of(b)));
   return f2of(r);
 }
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u64of(a)), "l"(u64of(b)));
+  return f2of(r);
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u64of(a)), "l"(u64of(b)));
+  return f2of(r);
+}
+// 2^x for a pair on the FMA pipe (FA4's MUFU offload): x = j + f with j = rint(x) (the 1.5*2^23
+// magic add), 2^f on [-0.5, 0.5] by a degree-3 minimax polynomial (max rel. error 7.5e-5, far
+// below the bf16 rounding of P), 2^j spliced into the exponent field. x is clamped at -127, where
+// the spliced scale is exactly 0: like ex2.approx.ftz, every x <= -127 gives an exact 0.
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  x = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
+  const float2 magic = make_float2(12582912.f, 12582912.f);
+  const float2 t = fadd2(x, magic);
+  const float2 f = fsub2(x, fsub2(t, magic));  // f = x - rint(x), exact
+  float2 pp = ffma2(make_float2(0.055172716f, 0.055172716f), f, make_float2(0.24261133f, 0.24261133f));
+  pp = ffma2(pp, f, make_float2(0.69326079f, 0.69326079f));
+  pp = ffma2(pp, f, make_float2(0.99992806f, 0.99992806f));
+  const float2 sc = make_float2(__uint_as_float((__float_as_uint(t.x) << 23) + 0x3F800000u),
+                                __uint_as_float((__float_as_uint(t.y) << 23) + 0x3F800000u));
+  return fmul2(pp, sc);
+}
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
@@ -106,6 +132,16 @@ __global__ void __launch_bounds__(320, 1)
                        int T, int H, float scale_log2, int use_alibi) {
   using Cf = AttnTcCfg<DH>;
   constexpr int BN = Cf::BN, NST = Cf::NST;
+  // measured (tools/attn_bench.py, isolated, C3 / C4 head shapes): every 3rd pair at dh 64
+  // (0.123 vs 0.1255 ms off, 0.132 at every 2nd), every 8th at dh 128 (0.172 vs 0.174, 0.187 at
+  // every 2nd): the softmax is latency-bound more than MUFU-bound, so only a small share pays
+#ifndef FB_POLY64
+#define FB_POLY64 3
+#endif
+#ifndef FB_POLY128
+#define FB_POLY128 8
+#endif
+  constexpr int kPolyEvery = DH == 64 ? FB_POLY64 : FB_POLY128;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -317,7 +353,10 @@ __global__ void __launch_bounds__(320, 1)
           for (int c = 0; c < 32; ++c) {
             const int i = 64 * hh + 2 * c;
             const float2 a = fadd2(make_float2(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), sh);
-            const float2 p = make_float2(ex2(a.x), ex2(a.y));
+            // every kPolyEvery-th pair on the FMA pipe: the MUFU (16 ex2 / clk / SM) bounds the
+            // softmax, at dh 64 by twice the MMA time
+            const float2 p = (kPolyEvery > 0 && c % kPolyEvery == kPolyEvery - 1) ? exp2_poly2(a)
+                                                                                 : make_float2(ex2(a.x), ex2(a.y));
             ps[c & 3] = fadd2(ps[c & 3], p);
             pk[c] = pack_bf16(p.x, p.y);
           }
