@@ -833,29 +833,36 @@ __global__ void __launch_bounds__(384, 1)
       __syncwarp();
       if (ord & 0x100u) {  // last contributor: lane owns rows lane + 32k, 32 columns each
 #pragma unroll 1
-        for (int k = 0; k < 4; ++k) {  // one row (8 accumulator loads in flight) at a time: register budget
-          const int r = lane + 32 * k;
-          const float* acc = dqacc + (int64_t)(row0 + q0 + r) * d + h * DH + 32 * g;
-          __nv_bfloat16* out = dqkv + (int64_t)(row0 + q0 + r) * (3 * d) + h * DH + 32 * g;
-          float4 a[8];
+        for (int k0 = 0; k0 < 4; k0 += 2) {  // two rows (16 accumulator loads in flight) at a time
+          float4 a[16];
 #pragma unroll
-          for (int q = 0; q < 8; ++q)
-            a[q] = cnt ? __ldcg(reinterpret_cast<const float4*>(acc) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int kk = 0; kk < 2; ++kk) {
+            const float* acc = dqacc + (int64_t)(row0 + q0 + lane + 32 * (k0 + kk)) * d + h * DH + 32 * g;
 #pragma unroll
-          for (int q = 0; q < 8; q += 2) {
-            float4 x0, x1;
-            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                         : "=f"(x0.x), "=f"(x0.y), "=f"(x0.z), "=f"(x0.w)
-                         : "r"(xbox + r * 128 + ((q ^ (r & 7)) << 4)));
-            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                         : "=f"(x1.x), "=f"(x1.y), "=f"(x1.z), "=f"(x1.w)
-                         : "r"(xbox + r * 128 + (((q + 1) ^ (r & 7)) << 4)));
-            if (cnt) {
-              x0 = make_float4(a[q].x + x0.x, a[q].y + x0.y, a[q].z + x0.z, a[q].w + x0.w);
-              x1 = make_float4(a[q + 1].x + x1.x, a[q + 1].y + x1.y, a[q + 1].z + x1.z, a[q + 1].w + x1.w);
+            for (int q = 0; q < 8; ++q)
+              a[8 * kk + q] = cnt ? __ldcg(reinterpret_cast<const float4*>(acc) + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int kk = 0; kk < 2; ++kk) {
+            const int r = lane + 32 * (k0 + kk);
+            __nv_bfloat16* out = dqkv + (int64_t)(row0 + q0 + r) * (3 * d) + h * DH + 32 * g;
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+              float4 x0, x1;
+              asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                           : "=f"(x0.x), "=f"(x0.y), "=f"(x0.z), "=f"(x0.w)
+                           : "r"(xbox + r * 128 + ((q ^ (r & 7)) << 4)));
+              asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                           : "=f"(x1.x), "=f"(x1.y), "=f"(x1.z), "=f"(x1.w)
+                           : "r"(xbox + r * 128 + (((q + 1) ^ (r & 7)) << 4)));
+              const float4 a0 = a[8 * kk + q], a1 = a[8 * kk + q + 1];
+              if (cnt) {
+                x0 = make_float4(a0.x + x0.x, a0.y + x0.y, a0.z + x0.z, a0.w + x0.w);
+                x1 = make_float4(a1.x + x1.x, a1.y + x1.y, a1.z + x1.z, a1.w + x1.w);
+              }
+              *reinterpret_cast<uint4*>(out + 4 * q) =
+                  make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
             }
-            *reinterpret_cast<uint4*>(out + 4 * q) =
-                make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w), pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
           }
         }
         __syncwarp();
