@@ -142,6 +142,14 @@ __global__ void __launch_bounds__(320, 1)
 #define FB_POLY128 8
 #endif
   constexpr int kPolyEvery = DH == 64 ? FB_POLY64 : FB_POLY128;
+  // dh 64: S_g 128 + O_g 64 columns leave room for P_g in its own 64 columns [384 + 64 g), so S_g(t+1)
+  // need not wait for PV_g(t); dh 128 writes P over S_g's lower half
+#ifdef FB_EXP_NOSEPP
+  constexpr int kSepP = 0;
+#else
+  constexpr int kSepP = DH == 64 ? 1 : 0;
+#endif
+  constexpr uint32_t kPOff = kSepP ? 384 : 0;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   uint8_t* smem = smem_raw + (((raw + 1023) & ~1023u) - raw);
@@ -230,7 +238,8 @@ __global__ void __launch_bounds__(320, 1)
                    kd + (uint64_t)(((kk >> 2) * (BN * 128) + (kk & 3) * 32) >> 4), idS, kk > 0);
       };
       uint32_t o_acc[2] = {0u, 0u};
-      auto issue_pv = [&](int g, int t) {
+      // P_g(t) released by the softmax: returns whether the whole block is dead
+      auto wait_p = [&](int g, int t) {
         const int j = g ? t : t - start0;
         mbar_wait(&p_full[g], j & 1);
         FTRACE(t * 16 + 8 + g);
@@ -241,13 +250,15 @@ __global__ void __launch_bounds__(320, 1)
           e[0] = e[1] = dead ? 0 : 1;
         }
         mbar_wait(&v_full[t % NST], (t / NST) & 1);
-        if (dead) return;
+        return dead;
+      };
+      auto mma_pv = [&](int g, int t) {
         tc_fence_after();
         const uint64_t vd = smem_desc_sw128(sV + (t % NST) * Cf::KT, BN * 128, 1024);
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)  // V MN-major: 16 keys = 16 rows x 128 B
-          umma_ts(tmem + 256 + DH * g, tmem + 128 * g + 8 * kk, vd + (uint64_t)((kk * 2048) >> 4), idO,
-                  o_acc[g] | (uint32_t)(kk > 0));
+          umma_ts(tmem + 256 + DH * g, tmem + kPOff + 64 * g * kSepP + 128 * g * (1 - kSepP) + 8 * kk,
+                  vd + (uint64_t)((kk * 2048) >> 4), idO, o_acc[g] | (uint32_t)(kk > 0));
         o_acc[g] = 1u;
       };
       mbar_wait(q_full, 0);
@@ -260,14 +271,31 @@ __global__ void __launch_bounds__(320, 1)
       for (int t = 0; t < nkv; ++t) {
         for (int g = 0; g < 2; ++g) {
           const bool now = active(g, t), next = t + 1 < nkv && active(g, t + 1);
-          if (now) issue_pv(g, t);
-          FTRACE(t * 16 + 10 + g);
-          if (next) {
-            issue_s(g, t + 1);
-            umma_commit(&s_full[g]);  // also covers PV_g(t): the softmax may rescale O / overwrite P
-            FTRACE(t * 16 + 12 + g);
-          } else if (now) {
-            umma_commit(&o_done[g]);
+          if constexpr (kSepP) {
+            // P has its own columns: S_g(t+1) goes in first (the next softmax starts one PV
+            // earlier), PV_g(t) behind it, and o_done[g] tells the softmax when O and the P
+            // columns are free again
+            const bool dead = now && wait_p(g, t);
+            if (next) {
+              issue_s(g, t + 1);
+              umma_commit(&s_full[g]);
+              FTRACE(t * 16 + 12 + g);
+            }
+            if (now) {
+              if (!dead) mma_pv(g, t);
+              umma_commit(&o_done[g]);
+              FTRACE(t * 16 + 10 + g);
+            }
+          } else {
+            if (now && !wait_p(g, t)) mma_pv(g, t);
+            FTRACE(t * 16 + 10 + g);
+            if (next) {
+              issue_s(g, t + 1);
+              umma_commit(&s_full[g]);  // also covers PV_g(t): the softmax may rescale O / overwrite P
+              FTRACE(t * 16 + 12 + g);
+            } else if (now) {
+              umma_commit(&o_done[g]);
+            }
           }
         }
         umma_commit(&v_empty[t % NST]);
@@ -282,7 +310,8 @@ __global__ void __launch_bounds__(320, 1)
     const int qi = q0 + 128 * g + r;
     const int ntile = g ? (has1 ? nkv : 0) : nkv0;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    const uint32_t tS = tmem + lane_off + 128 * g, tP = tS;  // P over S's lower 64 columns
+    const uint32_t tS = tmem + lane_off + 128 * g;
+    const uint32_t tP = kSepP ? tmem + lane_off + kPOff + 64 * g : tS;  // own columns, or over S's lower 64
     const uint32_t tO = tmem + lane_off + 256 + DH * g;
     // Scores in log2 units: x_i = s_i c + sl (k0 + i - qi) = y_i + base with the
     // tile-independent y_i = s_i c + colb[i] (colb = sl i, an smem broadcast table) and the
@@ -332,6 +361,10 @@ __global__ void __launch_bounds__(320, 1)
       // a block dead in all four warps skips its PV MMA and is marked for the backward.
       // Bit-identical to computing it: the skipped terms are exact zeros.
       const bool wdead = __all_sync(0xffffffffu, mx < m - 127.0f);
+      if (kSepP && j > 0) {  // PV_g(j-1) done: O = PV(0..j-1) and the P columns are free
+        mbar_wait(&o_done[g], (j - 1) & 1);
+        tc_fence_after();
+      }
       if (lane == 0) dead_flag[4 * g + quad] = wdead ? 1 : 0;
       if (wdead) {
         uint32_t z[32];
@@ -366,7 +399,8 @@ __global__ void __launch_bounds__(320, 1)
         const float rs = s01.x + s01.y;
         l = l * alpha + rs;
         m = m_new;
-        // O holds exactly PV(0..j-1): s_full(j) was committed after PV(j-1)
+        // O holds exactly PV(0..j-1): s_full(j) was committed after PV(j-1) (dh 128) or
+        // o_done was waited for above (dh 64)
         if (j > 0 && __any_sync(0xffffffffu, alpha != 1.0f)) {
 #pragma unroll
           for (int c = 0; c < DH / 32; ++c) {
@@ -387,7 +421,7 @@ __global__ void __launch_bounds__(320, 1)
       if (quad == 0 && lane == 0) FTRACE((j + (g ? 0 : start0)) * 16 + 6 + g);
     }
     if (ntile > 0) {  // warps of an absent second Q tile (T % 256 == 128) have nothing to write
-      mbar_wait(&o_done[g], 0);
+      mbar_wait(&o_done[g], kSepP ? ((ntile - 1) & 1) : 0);
       tc_fence_after();
       const float il = 1.0f / l;
       // O staged in this group's Q tile (free once every PV_g, hence every S_g, completed) in
