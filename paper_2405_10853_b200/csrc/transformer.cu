@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ x
 #pragma unroll
       for (int j = 0; j < VPT; j += 4) {
         float4 v = make_float4(o[j], o[j + 1], o[j + 2], o[j + 3]);
-        if (dres) {
+        if (dres) {  // read here, not with x / dy: hoisting it measured 259 vs 217 us at d = 2048
           float4 r = *reinterpret_cast<const float4*>(dres + base + j);
           v.x += r.x; v.y += r.y; v.z += r.z; v.w += r.w;
         }
@@ -408,6 +408,89 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const float* __restrict__ x
       work[((int64_t)blockIdx.x * 2 + 0) * d + c0 + j] = pg[j];
       work[((int64_t)blockIdx.x * 2 + 1) * d + c0 + j] = pb[j];
     }
+  }
+}
+
+#ifndef LNW_MINB
+#define LNW_MINB 2  // 2 CTAs / SM also at d = 768 (128-register cap)
+#endif
+// Narrow rows (d = 128 * NV4 <= 768: C2 / C3): one WARP per row, lane owns float4 columns
+// 4 (lane + 32 j), so a row is two warp reductions (no CTA barrier per row, unlike ln_bwd_kernel,
+// which measured 50-57% of HBM at d = 512 / 768). dgamma / dbeta partials stay in registers per
+// warp and are summed over the CTA's 8 warps in fixed order at the end -> work[blockIdx][2][d],
+// the same layout ln_bwd_reduce_kernel takes. Deterministic.
+template <int NV4>
+__global__ void __launch_bounds__(256, LNW_MINB) ln_bwd_warp_kernel(const float* __restrict__ x, const float* __restrict__ gamma,
+                                                          const float* __restrict__ mean_in,
+                                                          const float* __restrict__ rstd_in, const float* __restrict__ dy,
+                                                          const float* __restrict__ dres, float* __restrict__ dx,
+                                                          __nv_bfloat16* __restrict__ dx_bf16, float* __restrict__ work,
+                                                          int rows) {
+  constexpr int d = 128 * NV4;
+  // per-warp dgamma / dbeta partials live in smem ([warp][2][d], each lane its own float4
+  // columns: no conflicts, no barrier), so the registers hold x, dy and dres of a row at once:
+  // one memory round trip per row
+  extern __shared__ float4 part4[];
+  float* part = reinterpret_cast<float*>(part4);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int nw = gridDim.x * 8;
+  float4* pgw = part4 + (size_t)w * 2 * (d / 4);
+  float4* pbw = pgw + d / 4;
+#pragma unroll
+  for (int j = 0; j < NV4; ++j) pgw[32 * j + lane] = pbw[32 * j + lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int row = blockIdx.x * 8 + w; row < rows; row += nw) {
+    const int64_t base = (int64_t)row * d;
+    float4 xv[NV4], gv[NV4], rv[NV4];
+#pragma unroll
+    for (int j = 0; j < NV4; ++j) {
+      xv[j] = __ldcs(reinterpret_cast<const float4*>(x + base + 128 * j) + lane);
+      gv[j] = __ldcs(reinterpret_cast<const float4*>(dy + base + 128 * j) + lane);
+      rv[j] = dres ? __ldcs(reinterpret_cast<const float4*>(dres + base + 128 * j) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const float mu = __ldg(mean_in + row), rs = __ldg(rstd_in + row);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV4; ++j) {
+      const float4 gm = __ldg(reinterpret_cast<const float4*>(gamma + 128 * j) + lane);
+      float4 pg = pgw[32 * j + lane], pb = pbw[32 * j + lane];
+      float* xe = reinterpret_cast<float*>(&xv[j]);
+      float* ge = reinterpret_cast<float*>(&gv[j]);
+      const float* gme = reinterpret_cast<const float*>(&gm);
+      float* pge = reinterpret_cast<float*>(&pg);
+      float* pbe = reinterpret_cast<float*>(&pb);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float xh = (xe[k] - mu) * rs;
+        pge[k] += ge[k] * xh;
+        pbe[k] += ge[k];
+        const float g = ge[k] * gme[k];
+        xe[k] = xh;
+        ge[k] = g;
+        s1 += g;
+        s2 += g * xh;
+      }
+      pgw[32 * j + lane] = pg;
+      pbw[32 * j + lane] = pb;
+    }
+    s1 = warp_sum(s1) * (1.0f / d);
+    s2 = warp_sum(s2) * (1.0f / d);
+#pragma unroll
+    for (int j = 0; j < NV4; ++j) {
+      const float4 o = make_float4(rs * (gv[j].x - s1 - xv[j].x * s2) + rv[j].x, rs * (gv[j].y - s1 - xv[j].y * s2) + rv[j].y,
+                                   rs * (gv[j].z - s1 - xv[j].z * s2) + rv[j].z, rs * (gv[j].w - s1 - xv[j].w * s2) + rv[j].w);
+      *(reinterpret_cast<float4*>(dx + base + 128 * j) + lane) = o;
+      if (dx_bf16)
+        *(reinterpret_cast<uint2*>(dx_bf16 + base + 128 * j) + lane) = make_uint2(pack_bf16(o.x, o.y), pack_bf16(o.z, o.w));
+    }
+  }
+  // CTA partials: warps 0..7 summed in that order
+  __syncthreads();
+  for (int c = threadIdx.x; c < 2 * d; c += 256) {
+    const int pass = c / d, cc = c % d;
+    float a = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a += part[(size_t)i * 2 * d + pass * d + cc];
+    work[((int64_t)blockIdx.x * 2 + pass) * d + cc] = a;
   }
 }
 
@@ -672,8 +755,27 @@ extern "C" int fb_ln_bwd(const float* d_x, const float* d_gamma, const float* d_
                          float* d_dbeta, float* d_work, int rows, int d, void* stream) {
   FB_REQUIRE(rows > 0 && d > 0 && d <= 4096, "ln_bwd: bad shape rows=%d d=%d", rows, d);
   FB_REQUIRE(d_work != nullptr, "ln_bwd: needs a work buffer of %d floats", 2 * kLnBwdBlocks * d);
-  const int vpt = (d + 255) / 256;
   cudaStream_t st = (cudaStream_t)stream;
+  if ((d == 512 || d == 768) && (uintptr_t)d_x % 16 == 0 && (uintptr_t)d_dy % 16 == 0 && (uintptr_t)d_dx % 16 == 0 &&
+      (uintptr_t)d_dres % 16 == 0 && (uintptr_t)d_dx_bf16 % 8 == 0) {
+    // one resident wave, 2 CTAs / SM
+    const int wgrid = std::min((rows + 7) / 8, kNumSMs * LNW_MINB);
+    const int smem = 8 * 2 * d * 4;
+    if (d == 512) {
+      FB_CUDA_TRY(cudaFuncSetAttribute(ln_bwd_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      ln_bwd_warp_kernel<4><<<wgrid, 256, smem, st>>>(d_x, d_gamma, d_mean, d_rstd, d_dy, d_dres, d_dx,
+                                                      (__nv_bfloat16*)d_dx_bf16, d_work, rows);
+    } else {
+      FB_CUDA_TRY(cudaFuncSetAttribute(ln_bwd_warp_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      ln_bwd_warp_kernel<6><<<wgrid, 256, smem, st>>>(d_x, d_gamma, d_mean, d_rstd, d_dy, d_dres, d_dx,
+                                                      (__nv_bfloat16*)d_dx_bf16, d_work, rows);
+    }
+    FB_LAUNCH_CHECK();
+    ln_bwd_reduce_kernel<<<(d + 15) / 16, 256, 0, st>>>(d_work, wgrid, d, d_dgamma, d_dbeta);
+    FB_LAUNCH_CHECK();
+    return FB_OK;
+  }
+  const int vpt = (d + 255) / 256;
   const int grid = std::min(rows, kLnBwdBlocks);
 #define CALL_B(N) ln_bwd_kernel<N><<<grid, 256, 0, st>>>(d_x, d_gamma, d_mean, d_rstd, d_dy, d_dres, d_dx, (__nv_bfloat16*)d_dx_bf16, d_work, rows, d)
   if (vpt <= 1) CALL_B(1);

@@ -138,8 +138,11 @@ def test_attention_bwd_all_dead_map_zeroes(fb):
     assert (dqkv.float() == 0).all()
 
 
-@pytest.mark.parametrize("rows,d", [(256, 512), (100, 768), (64, 2048), (33, 128), (5003, 2048)])
+@pytest.mark.parametrize("rows,d", [(256, 512), (100, 768), (64, 2048), (33, 128), (5003, 2048), (20011, 512),
+                                    (9001, 768)])
 def test_layernorm(fb, rows, d):
+    """fb_ln_fwd / fb_ln_bwd vs torch; d = 512 / 768 take the warp-per-row backward (grid-looped at
+    the larger row counts), the others the CTA-per-row one."""
     torch.manual_seed(1)
     dev = torch.device("cuda")
     x = torch.randn(rows, d, device=dev) * 2 + 0.5
