@@ -8,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2405_10853_b200 import ext  # noqa: E402
 
 ext.lib()
-B, T, H, dh = 8, 2048, 16, 128
+B, T, H, dh = 8, 2048, int(os.environ.get("AO_H", 16)), int(os.environ.get("AO_DH", 128))
 d = H * dh
 qkv = torch.randn(B * T, 3 * d, device="cuda").to(torch.bfloat16)
 o = torch.empty(B * T, d, dtype=torch.bfloat16, device="cuda")
