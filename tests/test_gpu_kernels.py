@@ -246,3 +246,44 @@ def test_gemm_splitk_head_dgrad(fb, M, N, K):
             ws.data_ptr(), ws.numel() * 4, fb.stream_handle())
     torch.cuda.synchronize()
     torch.testing.assert_close(C, A.float() @ B.float(), atol=2e-3 * K ** 0.5, rtol=1e-4)
+
+
+@pytest.mark.parametrize("N", [1024 * 37 + 4, 3_000_004, 1024 * 1000])
+@pytest.mark.parametrize("K", [1, 3, 8])
+def test_fedagg_bulk_staged_path_is_bitwise_the_register_path(fb, N, K):
+    """K <= 8 and n % 4 == 0 take the cp.async.bulk-staged aggregation (whole and partial 1024-
+    parameter chunks); FB_AGG_NO_BULK=1 forces the per-thread-load kernel. w', m', the pseudo-
+    gradient and the first-bad index must be bitwise the same; the f64 norm side reductions
+    (atomically summed across CTAs) to 1e-12."""
+    import os
+    dev = torch.device("cuda")
+    gen = torch.Generator(device=dev).manual_seed(N + K)
+    w = torch.empty(N, device=dev).normal_(0, 0.02, generator=gen)
+    m = torch.empty(N, device=dev).normal_(0, 1e-3, generator=gen)
+    cl = [w + torch.empty(N, device=dev).normal_(0, 2e-3, generator=gen) for _ in range(K)]
+    cl[-1][N - 3] = float("nan")  # a non-finite client entry: w' there is NaN, first_bad = N - 3
+    nk = (C.c_int64 * K)(*[1000 + 7 * k for k in range(K)])
+    ptrs = (C.c_void_p * K)(*[t.data_ptr() for t in cl])
+    outs = []
+    for no_bulk in ("0", "1"):
+        os.environ["FB_AGG_NO_BULK"] = no_bulk
+        try:
+            wo, mo = torch.empty_like(w), torch.empty_like(m)
+            pg = torch.empty(N, dtype=torch.float64, device=dev)
+            st = torch.zeros(6 + K, dtype=torch.float64, device=dev)
+            bad = torch.zeros(1, dtype=torch.int64, device=dev)
+            fb.call("fb_fedagg_step_f32", ptrs, nk, K, 1, w.data_ptr(), m.data_ptr(), wo.data_ptr(), mo.data_ptr(), N,
+                    0.7, 0.9, 1, st.data_ptr(), bad.data_ptr(), pg.data_ptr(), fb.stream_handle())
+            wr, mr = torch.empty_like(w), torch.empty_like(m)
+            fb.call("fb_fedagg_round_norms_f32", ptrs, nk, K, 1, w.data_ptr(), m.data_ptr(), wr.data_ptr(),
+                    mr.data_ptr(), N, 0.7, 0.9, 1, st[:6 + K].data_ptr(), None, fb.stream_handle())
+            torch.cuda.synchronize()
+            outs.append((wo, mo, pg, bad.clone(), st.clone(), wr, mr))
+        finally:
+            os.environ.pop("FB_AGG_NO_BULK", None)
+    (a, b) = outs
+    for x, y in zip(a[:3] + a[5:], b[:3] + b[5:]):
+        assert torch.equal(x.view(torch.int32) if x.dtype == torch.float32 else x.view(torch.int64),
+                           y.view(torch.int32) if y.dtype == torch.float32 else y.view(torch.int64))
+    assert int(a[3].item()) == int(b[3].item()) == N - 3
+    torch.testing.assert_close(a[4], b[4], rtol=1e-12, atol=0, equal_nan=True)
