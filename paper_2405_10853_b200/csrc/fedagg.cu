@@ -33,10 +33,11 @@ namespace fb {
 // warps of f64 math) per SM. Same per-element math, same vector -> thread mapping: bit-identical.
 // C4 (K 8, 1.339 B): 12.9 -> 11.1 ms = 77% -> 90% of HBM; K 4: 62% -> 79%. Clients only / 3 stages
 // 80%; one CTA per SM with 3-4 stages 48-56% (8 warps cannot keep up with the f64 math).
-constexpr int kBulkChunk = 1024;  // parameters per CTA iteration (256 threads x 4)
+// The kernel takes any VEC (chunk = 256 VEC), but only K <= 8 pays: K 9-16 staged in 512-chunks
+// measured equal to the register kernel (74%), K 17-40 in 256-chunks slower (55% vs 77%), so the
+// launch keeps the bulk path for K <= 8.
 constexpr int kBulkStages = 2;
 constexpr int kBulkMaxK = 8;
-constexpr int kBulkSlots = kBulkMaxK + 2;  // clients, then w and m
 // A/B switch for the bulk-staged path (any value but "0" turns it off)
 static bool getenv_flag(const char* name) {
   const char* v = getenv(name);
@@ -148,28 +149,25 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
   }
   unsigned long long bad = ~0ull;
   const int64_t nvec = n / VEC;
-  // BULK: client chunks staged in smem (see kBulkChunk); iteration `it` of this CTA covers
-  // parameters [c * 1024, (c + 1) * 1024) with c = blockIdx.x + it * gridDim.x
+  // BULK: input chunks staged in smem (bulk_g2s); iteration `it` of this CTA covers
+  // parameters [c * CH, (c + 1) * CH) with c = blockIdx.x + it * gridDim.x
   extern __shared__ __align__(128) uint8_t agg_stage[];
   __shared__ __align__(8) uint64_t agg_full[kBulkStages];
   // chunks, the last one possibly partial (n % 4 == 0 keeps every copy a multiple of 16 bytes)
-  const int64_t nchunk = BULK ? (n + kBulkChunk - 1) / kBulkChunk : 0;
+  constexpr int CH = 256 * VEC;  // parameters per CTA iteration (256 threads x VEC)
+  const int slots = K + 2;        // stage layout: K clients, then w, then m, CH floats each
+  const int64_t nchunk = BULK ? (n + CH - 1) / CH : 0;
   auto issue_chunk = [&](int64_t it) {  // thread 0: chunk `it` into stage it % kBulkStages
     const int64_t c = (int64_t)blockIdx.x + it * gridDim.x;
     if (c >= nchunk) return;
     const int st = (int)(it % kBulkStages);
-    const int ns = kBulkSlots > kBulkMaxK ? K + 2 : K;
-    const uint32_t bytes = (uint32_t)(std::min<int64_t>(kBulkChunk, n - c * kBulkChunk) * 4);
-    sm100::mbar_arrive_expect_tx(&agg_full[st], (uint32_t)ns * bytes);
+    const uint32_t bytes = (uint32_t)(std::min<int64_t>(CH, n - c * CH) * 4);
+    sm100::mbar_arrive_expect_tx(&agg_full[st], (uint32_t)slots * bytes);
+    uint8_t* base = agg_stage + (size_t)st * slots * CH * 4;
     for (int k = 0; k < K; ++k)
-      bulk_g2s(agg_stage + ((size_t)st * kBulkSlots + k) * kBulkChunk * 4,
-               reinterpret_cast<const float*>(P.src[k]) + c * kBulkChunk, bytes, &agg_full[st]);
-    if (kBulkSlots > kBulkMaxK) {
-      bulk_g2s(agg_stage + ((size_t)st * kBulkSlots + kBulkMaxK) * kBulkChunk * 4, w + c * kBulkChunk, bytes,
-               &agg_full[st]);
-      bulk_g2s(agg_stage + ((size_t)st * kBulkSlots + kBulkMaxK + 1) * kBulkChunk * 4, m + c * kBulkChunk, bytes,
-               &agg_full[st]);
-    }
+      bulk_g2s(base + (size_t)k * CH * 4, reinterpret_cast<const float*>(P.src[k]) + c * CH, bytes, &agg_full[st]);
+    bulk_g2s(base + (size_t)K * CH * 4, w + c * CH, bytes, &agg_full[st]);
+    bulk_g2s(base + (size_t)(K + 1) * CH * 4, m + c * CH, bytes, &agg_full[st]);
   };
   if constexpr (BULK) {
     if (threadIdx.x == 0) {
@@ -196,16 +194,17 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
       __syncthreads();
       if (threadIdx.x == 0) issue_chunk(it + kBulkStages - 1);
       sm100::mbar_wait(&agg_full[it % kBulkStages], (uint32_t)((it / kBulkStages) & 1));
-      stage = reinterpret_cast<const float*>(agg_stage) + (size_t)(it % kBulkStages) * kBulkSlots * kBulkChunk;
+      stage = reinterpret_cast<const float*>(agg_stage) + (size_t)(it % kBulkStages) * slots * CH + VEC * threadIdx.x;
     }
     const int64_t v = act ? v0 : nvec - 1;
     const int64_t j0 = v * VEC;
     float wv[VEC], mv[VEC];
-    if constexpr (BULK && kBulkSlots > kBulkMaxK) {
-      const float4 a = *reinterpret_cast<const float4*>(stage + kBulkMaxK * kBulkChunk + 4 * threadIdx.x);
-      const float4 b = *reinterpret_cast<const float4*>(stage + (kBulkMaxK + 1) * kBulkChunk + 4 * threadIdx.x);
-      wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w;
-      mv[0] = b.x; mv[1] = b.y; mv[2] = b.z; mv[3] = b.w;
+    if constexpr (BULK) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        wv[e] = stage[K * CH + e];
+        mv[e] = stage[(K + 1) * CH + e];
+      }
     } else if constexpr (VEC == 4) {
       float4 a = ld_stream_f4(w + j0), b = ld_stream_f4(m + j0);
       wv[0] = a.x; wv[1] = a.y; wv[2] = a.z; wv[3] = a.w;
@@ -233,8 +232,8 @@ __global__ void __launch_bounds__(256, 2) fedagg_kernel(AggParams<TIn> P, int K,
           if (k0 + j < K) {
             const float* src = reinterpret_cast<const float*>(P.src[k0 + j]) + j0;
             if constexpr (BULK) {
-              const float4 t = *reinterpret_cast<const float4*>(stage + (k0 + j) * kBulkChunk + 4 * threadIdx.x);
-              c[j][0] = t.x; c[j][1] = t.y; c[j][2] = t.z; c[j][3] = t.w;
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) c[j][e] = stage[(k0 + j) * CH + e];
             } else if constexpr (VEC == 4) {
               float4 t = ld_stream_f4(src);
               c[j][0] = t.x; c[j][1] = t.y; c[j][2] = t.z; c[j][3] = t.w;
@@ -479,20 +478,22 @@ static int launch_fedagg(const TIn* const* src, const int64_t* n_k, int K, int d
   } while (0)
   if constexpr (sizeof(TIn) == 4) {
     if (aligned && K <= kBulkMaxK && n % 4 == 0 && !getenv_flag("FB_AGG_NO_BULK")) {
-      const int64_t nchunk = (n + kBulkChunk - 1) / kBulkChunk;
-      const int smem = kBulkStages * kBulkSlots * kBulkChunk * 4;
+      const int vec = 4;
+      const int64_t nchunk = (n + 256 * vec - 1) / (256 * vec);
+      const int smem = kBulkStages * (K + 2) * 256 * vec * 4;
       const int blocks = (int)std::min<int64_t>(nchunk, kNumSMs * (smem <= 110 * 1024 ? 2 : 1));  // all resident
-#define FB_AGG_BULK(D_, S_)                                                                                     \
+#define FB_AGG_BULK(VEC_, D_, KB_, S_)                                                                          \
   do {                                                                                                          \
-    auto kf = fedagg_kernel<float, 4, D_, S_, 8, 1>;                                                            \
+    auto kf = fedagg_kernel<float, VEC_, D_, S_, KB_, 1>;                                                       \
     FB_CUDA_TRY(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));                   \
     kf<<<blocks, threads, smem, st>>>(P, K, deterministic, 0.0, total, w, m, w_out, m_out, n, eta, mu, nesterov, \
                                       stats, (unsigned long long*)first_bad, pg_out, client_norms, n_fixed);    \
   } while (0)
-      if (depth <= 3) {
-        if (stats) FB_AGG_BULK(3, 1); else FB_AGG_BULK(3, 0);
+      // tree depth D >= floor(log2 K) + 1
+      if (K <= 7) {
+        if (stats) FB_AGG_BULK(4, 3, 8, 1); else FB_AGG_BULK(4, 3, 8, 0);
       } else {
-        if (stats) FB_AGG_BULK(4, 1); else FB_AGG_BULK(4, 0);
+        if (stats) FB_AGG_BULK(4, 4, 8, 1); else FB_AGG_BULK(4, 4, 8, 0);
       }
 #undef FB_AGG_BULK
       FB_LAUNCH_CHECK();

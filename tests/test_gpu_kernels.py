@@ -251,8 +251,8 @@ def test_gemm_splitk_head_dgrad(fb, M, N, K):
 @pytest.mark.parametrize("N", [1024 * 37 + 4, 3_000_004, 1024 * 1000])
 @pytest.mark.parametrize("K", [1, 3, 8])
 def test_fedagg_bulk_staged_path_is_bitwise_the_register_path(fb, N, K):
-    """K <= 8 and n % 4 == 0 take the cp.async.bulk-staged aggregation (whole and partial 1024-
-    parameter chunks); FB_AGG_NO_BULK=1 forces the per-thread-load kernel. w', m', the pseudo-
+    """K <= 8 and n % 4 == 0 take the cp.async.bulk-staged aggregation (whole and partial chunks
+    of 1024 parameters); FB_AGG_NO_BULK=1 forces the per-thread-load kernel. w', m', the pseudo-
     gradient and the first-bad index must be bitwise the same; the f64 norm side reductions
     (atomically summed across CTAs) to 1e-12."""
     import os
