@@ -124,10 +124,11 @@ def launches_per_step(c, fuse=1):
     # CUB scan ~2, run bounds, runs: ~10)
     wg = [(d, 4 * d), (4 * d, d), (d, d), (3 * d, d)]
     red = sum(1 for (mm, nn) in wg if splitk_splits(mm, nn, M) > 1 or tail_split(mm, nn, M) > 1)
-    # attention bwd: 3 launches (D pre-pass, kernel, dQ finalize); 2 when the out-projection dgrad
-    # forms D in its epilogue (fb_gemm_bf16_rowdot: 2-SM raster, i.e. >= 74 256x256 tiles)
+    # attention bwd: 2 kernels (D pre-pass, the backward itself, which writes dQ: no finalize since
+    # the ordered dQ) plus a 32 KB counter memset; 1 kernel when the out-projection dgrad forms D in
+    # its epilogue (fb_gemm_bf16_rowdot: 2-SM raster, i.e. >= 74 256x256 tiles)
     rowdot = M >= 256 and d >= 256 and (M // 256) * (d // 256) >= 74
-    bwd = 2 + L * (15 - rowdot + red) + 10
+    bwd = 2 + L * (14 - rowdot + red) + 10
     return c["micro"] // fuse * (fwd + bwd) + 4  # + sumsq, step_prepare, adamw, telemetry
 
 
