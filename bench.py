@@ -119,7 +119,7 @@ def launches_per_step(c, fuse=1):
     # + chunks x (head GEMM with the CE epilogue, ce_lse, ce_grad, head dgrad, head wgrad)
     hd = min(M, 8192)  # head-dgrad rows per chunk: a last-wave split or a classic split-K adds one reduction
     fwd = 1 + 1 + 7 * L + 1 + 5 * chunks + chunks * (tail_split(hd, d, c["V"]) > 1 or splitk_splits(hd, d, c["V"]) > 1)
-    # backward: ln_f bwd(2) + L x (dgelu, wgrad, dgrad, wgrad, ln bwd(2), dgrad, wgrad, attn bwd(3), dgrad, wgrad,
+    # backward: ln_f bwd(2) + L x (dgelu, wgrad, dgrad, wgrad, ln bwd(2), dgrad, wgrad, attn bwd(2), dgrad, wgrad,
     # ln bwd(2)) + split-K reduction launches + sorted embedding bwd (iota, CUB sort ~4, run flags,
     # CUB scan ~2, run bounds, runs: ~10)
     wg = [(d, 4 * d), (4 * d, d), (d, d), (3 * d, d)]
