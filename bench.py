@@ -112,7 +112,13 @@ def tail_split(M, N, K):
 
 def launches_per_step(c, fuse=1):
     """Kernel launches of our library per local step (fb_train_step), from the runtime's schedule
-    (`fuse` micro-batches per forward/backward pass, ClientSession.fuse)."""
+    (`fuse` micro-batches per forward/backward pass, the last pass the remainder; ClientSession.fuse)."""
+    full, rem = divmod(c["micro"], fuse)
+    per = [launches_per_pass(c, fuse)] * full + ([launches_per_pass(c, rem)] if rem else [])
+    return sum(per) + 4  # + sumsq, step_prepare, adamw, telemetry
+
+
+def launches_per_pass(c, fuse):
     L, d, M = c["L"], c["d"], c["B"] * fuse * c["T"]
     chunks = math.ceil(M / 8192)
     # forward: gather + embed + L x (ln, qkv, attn, proj, ln, fc, proj2) + ln_f
@@ -129,7 +135,7 @@ def launches_per_step(c, fuse=1):
     # its epilogue (fb_gemm_bf16_rowdot: 2-SM raster, i.e. >= 74 256x256 tiles)
     rowdot = M >= 256 and d >= 256 and (M // 256) * (d // 256) >= 74
     bwd = 2 + L * (14 - rowdot + red) + 10
-    return c["micro"] // fuse * (fwd + bwd) + 4  # + sumsq, step_prepare, adamw, telemetry
+    return fwd + bwd
 
 
 def peaks():

@@ -254,9 +254,10 @@ typedef struct {
   const int64_t* d_order;   /* this client's sample order (data.py:141-144) */
   int64_t n_order;          /* n_k */
   int32_t seq_len, batch, micro;
-  int32_t fuse;             /* micro-batches per forward/backward pass (0 or 1 = one; must divide micro):
-                               the same rows and the same per-token gradient scale, so the same step;
-                               fewer, larger GEMMs / attention grids. Workspace for batch * fuse rows */
+  int32_t fuse;             /* micro-batches per forward/backward pass (0 or 1 = one; the last pass takes
+                               the remainder when fuse does not divide micro): the same rows and the same
+                               per-token gradient scale, so the same step; fewer, larger GEMMs / attention
+                               grids. Workspace for batch * fuse rows */
   int64_t cursor;           /* sample cursor at the start of this step */
 } fb_data_desc;
 

@@ -286,12 +286,13 @@ extern "C" int fb_train_step(const fb_model_cfg* cfgp, float* P, void* shadow, f
   const fb_model_cfg& c = *cfgp;
   const fb_data_desc& D = *data;
   cudaStream_t st = (cudaStream_t)stream;
-  const int fuse = D.fuse > 1 ? D.fuse : 1;
   FB_REQUIRE(D.micro >= 1 && D.batch >= 1, "micro_batches and batch_size must be >= 1");
-  FB_REQUIRE(D.micro % fuse == 0, "fuse=%d must divide micro_batches=%d", fuse, D.micro);
-  // one forward/backward pass covers `fuse` consecutive micro-batches: micro-batch i's rows are
-  // order[cursor + i*B + r], so pass j is the contiguous cursor range [cursor + j*fuse*B, +fuse*B)
-  const int B = D.batch * fuse, T = D.seq_len, M = B * T, passes = D.micro / fuse;
+  const int fuse = D.fuse > 1 ? (D.fuse < D.micro ? D.fuse : D.micro) : 1;
+  // one forward/backward pass covers `fuse` consecutive micro-batches (the last pass the remainder
+  // when fuse does not divide micro): micro-batch i's rows are order[cursor + i*B + r], so pass j
+  // is the contiguous cursor range [cursor + j*fuse*B, + its rows); the per-token gradient scale
+  // below does not depend on the passes
+  const int B = D.batch * fuse, T = D.seq_len, M = B * T, passes = (D.micro + fuse - 1) / fuse;
   const int64_t n = layout_of(c).total;
   double* part_g = scratch;
   double* part_u = scratch + FB_RED_BLOCKS;
@@ -305,13 +306,14 @@ extern "C" int fb_train_step(const fb_model_cfg* cfgp, float* P, void* shadow, f
   FB_CUDA_TRY(cudaMemsetAsync(G, 0, sizeof(float) * (size_t)n, st));
   const float gscale = (float)(1.0 / ((double)D.batch * (T - 1)) / D.micro);
   for (int j = 0; j < passes; ++j) {
-    TRY(fb_gather_batch(D.d_corpus, D.d_order, D.n_order, D.cursor + (int64_t)j * B, B, T, tok, st));
-    TRY(fb_model_fwd_bwd(cfgp, P, shadow, G, tok, B, T, gscale, row_loss + (int64_t)j * M, 1, ws, need, st));
+    const int Bj = D.batch * std::min(fuse, D.micro - j * fuse);  // rows of this pass
+    TRY(fb_gather_batch(D.d_corpus, D.d_order, D.n_order, D.cursor + (int64_t)j * B, Bj, T, tok, st));
+    TRY(fb_model_fwd_bwd(cfgp, P, shadow, G, tok, Bj, T, gscale, row_loss + (int64_t)j * M, 1, ws, need, st));
   }
   TRY(fb_sumsq_partials(G, n, part_g, st));
   TRY(fb_step_prepare(part_g, lr, bc1, bc2, opt.clip_norm, ctl, st));
   TRY(fb_adamw_step(P, G, m1, m2, shadow, n, opt, ctl, part_u, part_p, first_bad, st));
-  tele_finalize_kernel<<<1, 1024, 0, st>>>(row_loss, passes * M, 1.0 / ((double)D.batch * (T - 1)) / D.micro, ctl,
+  tele_finalize_kernel<<<1, 1024, 0, st>>>(row_loss, D.micro * D.batch * T, 1.0 / ((double)D.batch * (T - 1)) / D.micro, ctl,
                                            part_u, part_p, first_bad, n, tele);
   FB_LAUNCH_CHECK();
   return FB_OK;

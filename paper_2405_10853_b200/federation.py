@@ -66,6 +66,10 @@ class Federation:
         # tools/concurrent_clients.py). Results are the same as sequential training.
         self.P = max(1, min(int(concurrent_clients), len(self.mine) or 1))
         self.evs = [self.ev] + [LossEvaluator(model_cfg) for _ in range(self.P - 1)]
+        if self.P > 1:  # P workspaces live at once: each client gets 1/P of the fused-pass budget
+            from .trainer import ClientSession
+            for e in self.evs:
+                e.fuse_budget = ClientSession.fuse_budget // self.P
         self.streams = [torch.cuda.Stream() for _ in range(self.P)] if self.P > 1 else []
         self.iters = {k: BatchIterator(corpus, split.shards[k], batch_size, data_seed) for k in self.mine}
         self.n_k = {k: split.shards[k].n_k for k in range(self.K)}

@@ -55,12 +55,13 @@ class RoundBuffers:
 
 
 def fused_micro(micro_batches: int, batch_size: int, ws_bytes, budget_bytes: int) -> int:
-    """Micro-batches per forward/backward pass (fb_data_desc.fuse): the largest of 4, 2, 1 that
-    divides micro_batches and whose activation workspace ws_bytes(rows) fits the budget. Same rows
-    and the same per-token gradient scale, hence the same local step; fewer, larger passes
-    (measured at the bench shapes: C4 fuse 2 -3.7% step time; C2 fuse 4 -19%, C3 fuse 4 -11%)."""
-    for f in (4, 2, 1):
-        if micro_batches % f == 0 and (f == 1 or ws_bytes(batch_size * f) <= budget_bytes):
+    """Micro-batches per forward/backward pass (fb_data_desc.fuse): the largest of 4, 3, 2, 1 (at most
+    micro_batches) whose activation workspace ws_bytes(rows) fits the budget; when it does not divide
+    micro_batches the last pass takes the remainder. Same rows and the same per-token gradient scale,
+    hence the same local step; fewer, larger passes (measured at the bench shapes: C4 fuse 2 -3.7%
+    step time, fuse 3 a further ~1%; C2 fuse 4 -19%, C3 fuse 4 -11%)."""
+    for f in (4, 3, 2, 1):
+        if f <= micro_batches and (f == 1 or ws_bytes(batch_size * f) <= budget_bytes):
             return f
     return 1
 
@@ -77,9 +78,10 @@ class ClientSession:
     and the error names the local step. finish() only waits for the last rows."""
 
     max_lag = 2
-    # activation-workspace budget for fused micro-batches (C4: 65 GB at fuse 2 with the deterministic
-    # dQ slabs; the resident client end weights of a 1-GPU 8-client round need most of the rest)
-    fuse_budget = int(float(os.environ.get("FB_FUSE_WS_GB", "72")) * 1e9)
+    # activation-workspace budget for fused micro-batches. C4: 61 GB at fuse 2, 91 GB at fuse 3, 122 GB
+    # at fuse 4; a 1-GPU 8-client C4 round also holds the model state (24 GB), the 8 client end weights
+    # (43 GB) and the round-end buffers (~16 GB) on the 192 GB B200, so 96 GB (fuse 3) leaves ~18 GB
+    fuse_budget = int(float(os.environ.get("FB_FUSE_WS_GB", "96")) * 1e9)
 
     def __init__(self, evaluator: LossEvaluator, batches: BatchIterator, adamw_cfg: AdamWConfig,
                  sched: ScheduleConfig):
@@ -113,9 +115,11 @@ class ClientSession:
         self.st = ext.stream_handle()
         ext.call("fb_cast_bf16", self.w.data_ptr(), self.shadow.data_ptr(), self.w.numel(), self.st)
         B, T = task.batch_size, self.T
+        # an evaluator shared out to P concurrent clients carries its share of the budget
+        budget = getattr(ev, "fuse_budget", None) or self.fuse_budget
         self.fuse = fused_micro(task.micro_batches, B,
                                 lambda rows: int(ext.lib().fb_model_workspace_bytes(C.byref(ev._mcfg), rows, T)),
-                                self.fuse_budget)
+                                budget)
         self.ws = ev.workspace(B * self.fuse, T, extra=B * self.fuse * T * 4 + 512)
         rb = getattr(ev, "_round_bufs", None)
         if rb is None:
