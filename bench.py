@@ -221,6 +221,8 @@ def run_ours(args, cfgname):
     adamw = AdamWConfig()
     W, K = args.warmup, args.steps
     P = max(1, args.concurrent)  # clients trained concurrently on this GPU (own stream + evaluator each)
+    if P > 1:  # as in Federation: P workspaces at once share the fused-pass budget
+        ev.fuse_budget = ClientSession.fuse_budget // P
     task = TrainTask(1, client, W + K, 0, c["B"], c["micro"], {"data": 99}, "bench")
     sess = ClientSession(ev, it, adamw, sched).begin(w0, task)
     fuse = sess.fuse
@@ -231,7 +233,9 @@ def run_ours(args, cfgname):
         st_i = torch.cuda.Stream()
         with torch.cuda.stream(st_i):
             it_i = data.BatchIterator(corpus, split.shards[k2], c["B"], 99)
-            s_i = ClientSession(LossEvaluator(cfg), it_i, adamw, sched).begin(
+            ev_i = LossEvaluator(cfg)
+            ev_i.fuse_budget = ClientSession.fuse_budget // P
+            s_i = ClientSession(ev_i, it_i, adamw, sched).begin(
                 w0, TrainTask(1, k2, W + K, 0, c["B"], c["micro"], {"data": 99}, "bench"))
         extra.append((s_i, st_i))
 
