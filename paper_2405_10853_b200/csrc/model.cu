@@ -105,7 +105,10 @@ static WS carve(const fb_model_cfg& c, int B, int T, Arena& A) {
   w.meanf = A.take<float>(M);
   w.rstdf = A.take<float>(M);
   w.lnf = A.take<__nv_bfloat16>(M * d);
-  w.chunk = (int)std::min<int64_t>(M, 8192);
+#ifndef FB_LMHEAD_CHUNK
+#define FB_LMHEAD_CHUNK 32768
+#endif
+  w.chunk = (int)std::min<int64_t>(M, FB_LMHEAD_CHUNK);
   w.ce_work = A.take<float>(fb_lmhead_ce_work_floats(w.chunk, (int)V));  // chunk (max, sum) pairs + lse
   w.dlogits = A.take<__nv_bfloat16>((int64_t)w.chunk * V);
   w.dx = A.take<float>(M * d);
