@@ -1059,7 +1059,12 @@ extern "C" int fb_gemm_bf16(int M, int N, int K, const void* d_A, int64_t lda, i
   const int tiles2 = ((M + 255) / 256) * ((N + 255) / 256);
   const int ks = g_split_ws ? g_split_n : 1;
   const bool a_2d = a_major && M % 64, b_2d = b_major && N % 64;
+#ifndef FB_OLD_KSPLIT
+  // a split-K call keeps the 2-SM kernel even when its units do not fill the first wave
+  const bool use2 = g_gemm_2sm && M >= 256 && N >= 256 && (tiles2 * ks >= kNumSMs / 2 || ks > 1) && !a_2d && !b_2d;
+#else
   const bool use2 = g_gemm_2sm && M >= 256 && N >= 256 && tiles2 * ks >= kNumSMs / 2 && !a_2d && !b_2d;
+#endif
   const int tiles256 = ((M + BM - 1) / BM) * ((N + 255) / 256) * ks;
   const int BN = (use2 || (N >= 256 && tiles256 >= kNumSMs)) ? 256 : 128;
   CUtensorMap ta, tb;
@@ -1226,6 +1231,25 @@ static int plan_tail_split(int tiles, int num_kb, int max_pieces, int& F) {
   }
   return best_t <= 0.96 * base ? best : 1;
 }
+
+// Full split-K for the 2-SM kernel (fewer output tiles than CTA pairs): the split S minimises
+// waves(S) * (k-blocks per unit + 2) + partial traffic, in units of one 256x256x64 k-block of a
+// CTA pair (~2.2 MB of HBM traffic at the power-capped clock). Filling the first wave is not
+// enough: 4 tiles x 19 splits = 76 units is two waves for two units (51% busy), 4 x 18 = 72 one.
+static int plan_ksplit(int tiles, int num_kb, int64_t mn, int max_split) {
+  const int P = kNumSMs / 2;
+  int best = 1;
+  double best_t = 1e30;
+  // S = 1 with fewer tiles than CTA pairs would leave the 2-SM kernel; start at 2 then
+  for (int S = tiles < P && max_split >= 2 ? 2 : 1; S <= std::min(max_split, 64); ++S) {
+    const int per = (num_kb + S - 1) / S;
+    if (S > 1 && (per < 16 || (S - 1) * per >= num_kb)) break;
+    const int waves = (tiles * S + P - 1) / P;
+    const double t = waves * (per + 2.0) + (S > 1 ? (S + 2) * (double)mn * 4 / 2.2e6 + 8.0 : 0.0);
+    if (t < best_t) { best_t = t; best = S; }
+  }
+  return best;
+}
 }  // namespace fb
 
 // Split-K GEMM for short-M/N, long-K products (weight gradients over many tokens):
@@ -1264,6 +1288,11 @@ extern "C" int fb_gemm_bf16_splitk(int M, int N, int K, const void* d_A, int64_t
       }
     }
     ksplit = 1;
+#ifndef FB_OLD_KSPLIT
+    if (g_gemm_2sm && M >= 256 && N >= 256 && tiles2 < kNumSMs / 2 && !ragged && d_ws)
+      ksplit = plan_ksplit(tiles2, num_kb, (int64_t)M * N, (int)std::min<int64_t>(64, ws_bytes / ((int64_t)M * N * 4)));
+    else
+#endif
     while (tiles2 * ksplit < kNumSMs / 2 && num_kb / (ksplit + 1) >= 16) ++ksplit;
   }
   // every split must own >= 1 k-block (ceil-sized splits: the last ones could be empty)
