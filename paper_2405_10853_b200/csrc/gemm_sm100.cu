@@ -545,11 +545,35 @@ __device__ __forceinline__ void partial_chunk_tma(const CUtensorMap* map, uint8_
   }
 }
 
+// Per-row epilogue inputs that do not depend on the accumulator (dGELU pre-activation,
+// residual stream): loaded for the NEXT chunk (and the tile's first chunk before its
+// accumulator is ready), so the load latency hides behind the current chunk / the main loop.
+// At C2 / C3 widths (K = 512 / 768) the main loop of a tile is short and the epilogue with
+// an exposed ~1 us load per chunk was the bound.
+template <int EPI>
+constexpr bool kEpiPrefetch = EPI == FB_EPI_DGELU || EPI == FB_EPI_RESID_F32 || EPI == FB_EPI_RESID_F32_BF16;
+template <int EPI>
+__device__ __forceinline__ void epi_prefetch(const EpiArgs& e, int64_t row, int col, int M, int N, uint4 (&pf)[8]) {
+  if constexpr (kEpiPrefetch<EPI>) {
+    if (row < M && col + 32 <= N) {
+      if constexpr (EPI == FB_EPI_DGELU) {
+        const uint4* P = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(e.aux) + row * e.ld_aux + col);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pf[q] = P[q];
+      } else {
+        const uint4* R = reinterpret_cast<const uint4*>(reinterpret_cast<const float*>(e.aux) + row * e.ld_aux + col);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) pf[q] = R[q];
+      }
+    }
+  }
+}
+
 // One 32-column chunk of one warp: lane = row (row0 + lane), r[] = TMEM accumulator values.
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& e, const EpiMaps& mp, uint8_t* stg, int lane,
                                                    int64_t row, int row0, int col, int split, int M, int N,
-                                                   const uint32_t (&r)[32], float& rd) {
+                                                   const uint32_t (&r)[32], float& rd, const uint4 (&pf)[8]) {
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
@@ -562,7 +586,8 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& e, const EpiMa
     if (in && full) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float4 c = *reinterpret_cast<const float4*>(R + 4 * q);
+        const float4 c = EPI == FB_EPI_ACC_F32 ? *reinterpret_cast<const float4*>(R + 4 * q)
+                                               : *reinterpret_cast<const float4*>(&pf[q]);
         v[4 * q] += c.x; v[4 * q + 1] += c.y; v[4 * q + 2] += c.z; v[4 * q + 3] += c.w;
       }
     } else if (in) {
@@ -588,7 +613,7 @@ __device__ __forceinline__ void epilogue_chunk_tma(const EpiArgs& e, const EpiMa
     if (in && full) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        uint4 pk = *reinterpret_cast<const uint4*>(P + 8 * q);
+        const uint4 pk = pf[q];
         const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&pk);
 #pragma unroll
         for (int i = 0; i < 8; i += 2) {
@@ -700,6 +725,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
   const int num_n = (N + 255) / 256;
   const int num_tiles = num_m * num_n;
   const int num_kb = (K + BK - 1) / BK;
+  // epilogue inputs one chunk ahead only where the main loop is short (C2 / C3: dGELU +17%,
+  // out-projection residual +5%); at K = 2048 the early loads measured 1-4% slower
+  const bool early = K <= 1024;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -797,15 +825,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
       const int n0 = nb * 256 + half * 128;
       const int buf = it & 1;
       const uint32_t use = it >> 1;
+      const int row0 = m0 + quad * 32;
+      uint4 pf[8];
+      if (piece < 0 && early) epi_prefetch<EPI>(ep, row0 + lane, n0, M, N, pf);
       mbar_wait(&tfull_bar[buf], use & 1);
       tc_fence_after();
-      const int row0 = m0 + quad * 32;
       const uint32_t taddr = tmem_base + ((uint32_t)(quad * 32) << 16) + buf * 256 + half * 128;
       float rd = 0.f;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {
         uint32_t r[32];
         tmem_ld_32x32b_x32(taddr + c * 32, r);
+        uint4 cur[8];
+        if (early) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q) cur[q] = pf[q];
+          if (c < 3 && piece < 0) epi_prefetch<EPI>(ep, row0 + lane, n0 + (c + 1) * 32, M, N, pf);
+        } else if (piece < 0) {
+          epi_prefetch<EPI>(ep, row0 + lane, n0 + c * 32, M, N, cur);
+        }
         tmem_ld_wait();
         if (c == 3) {
           tc_fence_before();
@@ -817,7 +855,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kGemmThreads, 1)
           if (piece >= 0)
             partial_chunk_tma(&maps.Part, stg, lane, col - nb * 256, row0 - mb * 256, piece, r);
           else
-            epilogue_chunk_tma<EPI>(ep, maps, stg, lane, row0 + lane, row0, col, u / num_tiles, M, N, r, rd);
+            epilogue_chunk_tma<EPI>(ep, maps, stg, lane, row0 + lane, row0, col, u / num_tiles, M, N, r, rd, cur);
         }
         if constexpr (EPI == FB_EPI_BF16_ROWDOT) {  // head boundary: D[b][h][t] of this lane's row
           if ((col + 32) % ep.rd_dh == 0) {

@@ -16,6 +16,8 @@ shapes = [  # name, M, N, K, a_major, b_major, epi
     ("fc_dgrad", Mt, 2048, 8192, 0, 1, "f32"), ("qkv_wgrad", 6144, 2048, Mt, 1, 1, "acc_f32"),
     ("proj_wgrad", 2048, 2048, Mt, 1, 1, "acc_f32"), ("head_fwd", 8192, 32000, 2048, 0, 0, "f32"),
     ("c2_qkv_wgrad", 1536, 512, Mt, 1, 1, "acc_f32"), ("c2_proj_wgrad", 512, 512, Mt, 1, 1, "acc_f32"),
+    ("c2_fc2_dgrad_dgelu", 262144, 2048, 512, 0, 1, "dgelu"), ("c2_fc_fwd_gelu", 262144, 2048, 512, 0, 0, "gelu"),
+    ("c2_proj2_fwd_resid", 262144, 512, 2048, 0, 0, "resid_f32"), ("c2_proj_fwd_resid", 262144, 512, 512, 0, 0, "resid_f32"),
 ]
 ONLY = [x for x in os.environ.get("GB_ONLY", "").split(",") if x]
 for name, M, N, K, am, bm, epi in shapes:
