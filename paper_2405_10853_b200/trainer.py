@@ -83,10 +83,11 @@ class ClientSession:
     and the error names the local step. finish() only waits for the last rows."""
 
     max_lag = 2
-    # activation-workspace budget for fused micro-batches. C4: 61 GB at fuse 2, 91 GB at fuse 3, 122 GB
+    # activation-workspace budget for fused micro-batches. C4: 62 GB at fuse 2, 93 GB at fuse 3, 123 GB
     # at fuse 4; a 1-GPU 8-client C4 round also holds the model state (24 GB), the 8 client end weights
-    # (43 GB) and the round-end buffers (~16 GB) on the 192 GB B200, so 96 GB (fuse 3) leaves ~18 GB
-    fuse_budget = int(float(os.environ.get("FB_FUSE_WS_GB", "96")) * 1e9)
+    # (43 GB) and the round-end buffers (~16 GB) on the 192 GB B200, so fuse 3 leaves ~16 GB. 100 GB
+    # also admits C3's whole step (fuse 16: 96.9 GB; +1% vs fuse 8, profiles/r02_c3_fuse_budget.txt)
+    fuse_budget = int(float(os.environ.get("FB_FUSE_WS_GB", "100")) * 1e9)
 
     def __init__(self, evaluator: LossEvaluator, batches: BatchIterator, adamw_cfg: AdamWConfig,
                  sched: ScheduleConfig):
